@@ -1,0 +1,26 @@
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    config.addinivalue_line("markers", "slow: longer CPU statistics tests")
+
+
+@pytest.fixture(scope="session")
+def cfg():
+    with open(os.path.join(ROOT, "config", "thresholds.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="session")
+def P(cfg):
+    import oracle
+    return oracle.make_params(cfg)

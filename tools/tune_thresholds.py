@@ -1,0 +1,174 @@
+#!/usr/bin/env python3
+"""Threshold tuning for the Selection Cuts and the vertex tests.
+
+PAPER.md gives the cut *quantities* (Eq. 2-5, Sec. IV-C) but not their numeric
+thresholds; it states the tuning target instead: the cuts keep "over 98.5% of
+true triplet combinations" (Sec. IV-A) and the vertex selection identifies
+"over 94% of signal events" (abstract, Sec. VI-A).  This script reproduces that
+methodology on generated truth (synth/) using ONLY the oracle (oracle/), and
+writes config/thresholds.json (reading R4).
+
+  python tools/tune_thresholds.py [--frames N] [--write]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+
+CFG_PATH = os.path.join(ROOT, "config", "thresholds.json")
+
+# fixed by the paper
+PAPER_FIXED = {"cuts_max": 768,    # Sec. VI "a set value of 768"
+               "chi2_max": 32.0,   # Sec. IV-B "chi2 error of smaller than 32"
+               "target_r": 19.0}   # Sec. IV-C "disk with a radius of 19mm"
+
+
+def true_hits(d, f):
+    """{particle: {layer: global hit index}} for frame f (truth)."""
+    hp, off = d["hit_particle"], d["offsets"]
+    out = {}
+    for layer in range(4):
+        for g in range(int(off[4 * f + layer]), int(off[4 * f + layer + 1])):
+            if hp[g] >= 0:
+                out.setdefault(int(hp[g]), {})[layer] = g
+    return out
+
+
+def cut_variables(cfg, d, f, P):
+    """Eq. 2-5 cut variables of every reconstructible (4-layer) true triplet."""
+    R = cfg["layer_r"]
+    x, y, z = d["x"], d["y"], d["z"]
+    rows = []
+    for pid, lay in true_hits(d, f).items():
+        if len(lay) < 4:
+            continue
+        a, b, c = lay[0], lay[1], lay[2]
+        h = [(float(x[g]), float(y[g]), float(z[g])) for g in (a, b, c)]
+        dl = oracle.tan_lambda(h[1][2], h[2][2], R[1], R[2]) - oracle.tan_lambda(h[0][2], h[1][2], R[0], R[1])
+        c01 = oracle.cos_phi(h[0][0], h[0][1], h[1][0], h[1][1], R[0], R[1])
+        c12 = oracle.cos_phi(h[1][0], h[1][1], h[2][0], h[2][1], R[1], R[2])
+        rt = oracle.circle_radius(*h)
+        rows.append((abs(dl), c01, c12, abs(rt)))
+    return rows
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--frames", type=int, default=4000)
+    ap.add_argument("--signal-frames", type=int, default=4000)
+    ap.add_argument("--write", action="store_true")
+    ap.add_argument("--q", type=float, default=0.998, help="per-cut retention quantile")
+    ap.add_argument("--qv", type=float, default=0.995, help="per-test vertex quantile")
+    a = ap.parse_args()
+
+    cfg = json.load(open(CFG_PATH))
+    cfg.update(PAPER_FIXED)
+    seed_tune = 7001  # tuning sample seeds differ from every test / bench seed
+    bg = synth.generate(synth.preset("phase1_bg", seed=seed_tune), a.frames, truth=True)
+    sig_cfg = synth.preset("signal_only", seed=seed_tune + 1)
+    sig = synth.generate(sig_cfg, a.signal_frames, truth=True)
+
+    # ---------------- selection cuts: per-cut quantiles on true 4-hit triplets
+    P = oracle.make_params(cfg)
+    rows = []
+    for d in (bg, sig):
+        for f in range(d["n_frames"]):
+            rows += cut_variables(cfg, d, f, P)
+    v = np.array(rows)
+    q = a.q
+    cfg["dlambda_max"] = float(np.quantile(v[:, 0], q))
+    cfg["cos_phi01_min"] = float(np.quantile(v[:, 1], 1 - q))
+    cfg["cos_phi12_min"] = float(np.quantile(v[:, 2], 1 - q))
+    cfg["rt_min"] = float(np.quantile(v[:, 3], (1 - q) / 2))
+    cfg["rt_max"] = float(np.quantile(v[:, 3], 1 - (1 - q) / 2))
+    P = oracle.make_params(cfg)
+
+    # combined retention + funnel on background
+    fr = oracle.Frames(bg)
+    funnel = np.zeros(5)
+    kept_true = n_true = 0
+    for f in range(bg["n_frames"]):
+        cands, res = oracle.select(P, fr, f)
+        funnel += np.array(list(res.funnel), dtype=float)
+        th = true_hits(bg, f)
+        want = {(lay[0] - int(bg["offsets"][4 * f]), lay[1] - int(bg["offsets"][4 * f + 1]),
+                 lay[2] - int(bg["offsets"][4 * f + 2])) for lay in th.values() if len(lay) == 4}
+        got = {(c.i0, c.i1, c.i2) for c in cands}
+        n_true += len(want)
+        kept_true += len(want & got)
+    print(f"selection: true 4-hit triplet retention {kept_true / max(n_true, 1):.4f} "
+          f"({kept_true}/{n_true}); funnel kept fractions {np.round(funnel[1:] / funnel[0], 4)}")
+
+    # ---------------- vertex tests: tune on reconstructed true signal triples
+    vac = dict(cfg, e_window=1e9, chi2_vertex_max=1e30, target_dist_max=1e9, p_total_max=1e9)
+    Pv = oracle.make_params(vac)
+    frs = oracle.Frames(sig)
+    dE, chi, tdist, ptot = [], [], [], []
+    for f in range(sig["n_frames"]):
+        res, tracks = oracle.process_frame(Pv, frs, f)
+        parts = synth.particles(sig_cfg, f)
+        th = true_hits(sig, f)
+        # map track -> particle if its 4 hits are one particle's hits
+        owner = []
+        for t in tracks:
+            own = None
+            for pid, lay in th.items():
+                if len(lay) == 4 and all(lay[l] - int(sig["offsets"][4 * f + l]) == t.hit[l] for l in range(4)):
+                    own = pid
+            owner.append(own)
+        sigp = [i for i, p in enumerate(parts) if p["kind"] in (1, 2)]
+        idx = {}
+        for ti, o in enumerate(owner):
+            if o in sigp and o not in idx:
+                idx[o] = ti
+        if len(idx) < 3:
+            continue
+        vt = []
+        for ti in [idx[s] for s in sigp]:
+            t = tracks[ti]
+            g0 = int(sig["offsets"][4 * f]) + t.hit[0]
+            vt.append(oracle.VTrack(t.kappa, t.cos_theta01, t.cx, t.cy,
+                                    (float(sig["x"][g0]), float(sig["y"][g0]), float(sig["z"][g0]))))
+        if not (vt[0].kappa > 0 and vt[1].kappa > 0 and vt[2].kappa < 0):
+            continue
+        r2, verts = oracle.vertex_frame(Pv, vt)
+        if not verts:
+            continue
+        e = sum(np.sqrt((0.299792458 / abs(t.kappa)) ** 2 + 0.51099895 ** 2) for t in vt) - 105.6583755
+        dE.append(abs(e))
+        chi.append(verts[0].chi2)
+        tdist.append(verts[0].target_dist)
+        ptot.append(verts[0].p_total)
+    dE, chi, tdist, ptot = map(np.array, (dE, chi, tdist, ptot))
+    qv = a.qv
+    cfg["e_window"] = float(np.quantile(dE, qv))
+    cfg["chi2_vertex_max"] = float(np.quantile(chi, qv))
+    cfg["target_dist_max"] = float(np.quantile(tdist, qv))
+    cfg["p_total_max"] = float(np.quantile(ptot, qv))
+    print(f"vertex: {len(dE)} fully reconstructed signal triples; thresholds at {qv} quantiles: "
+          f"e_window {cfg['e_window']:.3f} chi2 {cfg['chi2_vertex_max']:.3f} "
+          f"target_dist {cfg['target_dist_max']:.3f} p_total {cfg['p_total_max']:.3f}")
+    for k in ["dlambda_max", "cos_phi01_min", "cos_phi12_min", "rt_min", "rt_max"]:
+        print(f"  {k} = {cfg[k]:.6g}")
+    cfg["_provenance"] = ("written by tools/tune_thresholds.py (oracle/ + synth/ only), seeds 7001/7002, "
+                          f"{a.frames} phase1_bg + {a.signal_frames} signal_only frames, per-cut quantile {q}, "
+                          f"vertex quantile {qv}")
+    if a.write:
+        with open(CFG_PATH, "w") as fh:
+            json.dump(cfg, fh, indent=2)
+            fh.write("\n")
+        print("wrote", CFG_PATH)
+
+
+if __name__ == "__main__":
+    main()
