@@ -1,0 +1,452 @@
+// m3e_device.cuh -- per-frame device math of the Mu3e online event selection
+// (PAPER.md = arXiv 2206.11535).  Selection cuts and the triplet fit run in fp32
+// (one lane per combination / per candidate); the rarely executed vertex stage
+// runs in fp64.  This file shares nothing with oracle/ (the CPU reference); the
+// readings R<n> it follows are listed in DESIGN.md.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "m3e.h"
+
+namespace m3e {
+
+constexpr float kPiF = 3.14159265358979323846f;
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kMuMass = 105.6583755;   // MeV (PDG), m_mu c^2 of Eq. 1
+constexpr double kEMass = 0.51099895;     // MeV (PDG)
+constexpr double kPtConv = 0.299792458;   // MeV/c per (T mm)
+constexpr int kMaxLayerHits = 1024;       // 10-bit candidate index fields
+
+// Kernel-side parameters, derived once on the host from m3e_params.
+struct DevParams {
+    float R[4];                 // layer radii
+    float inv_dr01, inv_dr12;   // 1/(R1-R0), 1/(R2-R1)         (Eq. 2)
+    float inv_r0r1, inv_r1r2;   // 1/(R0 R1), 1/(R1 R2)         (Eq. 4)
+    float dl_max, c01_min, c12_min, rt_min, rt_max;
+    float chl;                  // sigma_MS = chl * k  (Highland at p = ptb / k, R7)
+    float chi2_max;
+    float R3sq;                 // layer-3 radius squared
+    int cuts_max, max_tracks, max_combs;
+    // vertex stage (fp64)
+    double ptb;                 // kPtConv * B: p = ptb / k
+    double chl_d;
+    double e_window, rlim, sig_pix2, chi2v_max, tdist_max, ptot_max, target_r, target_half;
+};
+
+struct Frame {                  // one frame's hits, pointers to its first hit
+    const float* x;
+    const float* y;
+    const float* z;
+    int s[4];                   // layer starts relative to the frame's first hit
+    int n[4];                   // hits per layer
+};
+
+__device__ __forceinline__ float3 hit(const Frame& F, int layer, int i) {
+    int g = F.s[layer] + i;
+    return make_float3(F.x[g], F.y[g], F.z[g]);
+}
+
+// ---------------------------------------------------------------- Eq. 5 ----
+// r_tc = d01 d12 d20 / (2 [(h0 - h1) x (h2 - h1)]_z); > 0 clockwise (R5);
+// collinear -> +inf.
+__device__ __forceinline__ float circle_radius(float3 h0, float3 h1, float3 h2) {
+    float ax = h0.x - h1.x, ay = h0.y - h1.y, bx = h2.x - h1.x, by = h2.y - h1.y;
+    float cz = ax * by - ay * bx;
+    if (cz == 0.0f) return __int_as_float(0x7f800000);
+    float cx = h2.x - h0.x, cy = h2.y - h0.y;
+    float d01 = sqrtf(ax * ax + ay * ay), d12 = sqrtf(bx * bx + by * by), d20 = sqrtf(cx * cx + cy * cy);
+    return d01 * d12 * d20 / (2.0f * cz);
+}
+
+// ------------------------------------------------------- Selection Cuts ----
+// Tests of Alg. 2 in order: Delta-lambda (Eq. 2-3), Phi_01, Phi_12 (Eq. 4), r_tc
+// (Eq. 5).  Returns true if the combination survives; rt = Eq. 5 radius.
+__device__ __forceinline__ bool pass_cuts(const DevParams& P, const Frame& F, int i0, int i1, int i2,
+                                          float& rt) {
+    const int g0 = F.s[0] + i0, g1 = F.s[1] + i1, g2 = F.s[2] + i2;
+    const float z0 = F.z[g0], z1 = F.z[g1], z2 = F.z[g2];
+    const float dl = (z2 - z1) * P.inv_dr12 - (z1 - z0) * P.inv_dr01;
+    if (!(fabsf(dl) <= P.dl_max)) return false;
+    const float x0 = F.x[g0], y0 = F.y[g0], x1 = F.x[g1], y1 = F.y[g1];
+    if (!((x0 * x1 + y0 * y1) * P.inv_r0r1 >= P.c01_min)) return false;
+    const float x2 = F.x[g2], y2 = F.y[g2];
+    if (!((x1 * x2 + y1 * y2) * P.inv_r1r2 >= P.c12_min)) return false;
+    rt = circle_radius(make_float3(x0, y0, z0), make_float3(x1, y1, z1), make_float3(x2, y2, z2));
+    const float ar = fabsf(rt);
+    return ar >= P.rt_min && ar <= P.rt_max;
+}
+
+// Warp-cooperative enumeration of all n0 n1 n2 combinations of one frame in the
+// row-major order of Alg. 2 (i0 outer, i2 inner), 32 consecutive combinations per
+// step; survivors are compacted with a ballot + popc prefix so that stored
+// candidates keep the enumeration order.  Stops once more than cuts_max survive
+// (the frame then overflows, R3).  emit(pos, packed, rt) is called for pos <
+// cuts_max.  Returns min(#survivors, cuts_max + 1) (warp-uniform).
+template <class Emit>
+__device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame& F, Emit emit) {
+    const int lane = threadIdx.x & 31;
+    const int n0 = F.n[0], n1 = F.n[1], n2 = F.n[2];
+    const long long total = (long long)n0 * n1 * n2;
+    if (total == 0) return 0;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    // mixed-radix digits of the lane's first combination and of the step 32
+    const int n12 = n1 * n2;
+    int i0 = lane / n12, rem = lane - i0 * n12;
+    int i1 = rem / n2, i2 = rem - i1 * n2;
+    const int a = 32 / n12, r32 = 32 - a * n12, b = r32 / n2, c = r32 - b * n2;
+    int count = 0;
+    for (long long base = 0; base < total; base += 32) {
+        const bool valid = i0 < n0;
+        float rt = 0.0f;
+        const bool pass = valid && pass_cuts(P, F, i0, i1, i2, rt);
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (pass) {
+            const int pos = count + __popc(m & lt_mask);
+            if (pos < P.cuts_max) emit(pos, (uint32_t)i0 | ((uint32_t)i1 << 10) | ((uint32_t)i2 << 20), rt);
+        }
+        count += __popc(m);
+        if (count > P.cuts_max) return P.cuts_max + 1;
+        // advance (i0, i1, i2) by 32 in radix (n0, n1, n2)
+        i2 += c;
+        if (i2 >= n2) { i2 -= n2; ++i1; }
+        i1 += b;
+        if (i1 >= n1) { i1 -= n1; ++i0; }
+        i0 += a;
+    }
+    return count;
+}
+
+// ------------------------------------------------------------ Triplet Fit ----
+// Single-triplet fit (Sec. IV-B-1, Eq. 6, readings R6-R8).  Each arc's bending
+// angle Phi and polar angle theta are linearised in the 3D curvature k around
+// the arc's circle solution (radius r_tc of Eq. 5) with analytic derivatives of
+//   1/k^2 = d^2 / (4 sin^2(Phi/2)) + z^2 / Phi^2 ,   cos theta = z k / Phi.
+// Around k_ref = (k_C01 + k_C12)/2, delta = k - k_ref:
+//   Phi_MS(delta)   = al_phi + b_phi delta,  Theta_MS(delta) = al_th + b_th delta
+// and chi2 = Phi_MS^2 w_phi + Theta_MS^2 w_th is minimised in closed form.
+struct Triplet {
+    int q;                       // +1 clockwise (e+), -1
+    float kref, al_phi, b_phi, al_th, b_th, w_phi, w_th;
+    float khat;                  // |kappa_t|
+    float var;                   // sigma^2_kappa,t = 1 / (b_phi^2 w_phi + b_th^2 w_th)
+    // arc data kept for the extensions
+    float phc[2], kc[2], dphi[2];
+};
+
+__device__ __forceinline__ bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2, float rtc,
+                                            Triplet& T) {
+    if (!(fabsf(rtc) < __int_as_float(0x7f800000))) return false;
+    T.q = rtc > 0.0f ? 1 : -1;
+    const float r = fabsf(rtc);
+    float th[2], sth0 = 0.0f, dth[2];
+    const float3 H[3] = {h0, h1, h2};
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        const float dx = H[a + 1].x - H[a].x, dy = H[a + 1].y - H[a].y, z = H[a + 1].z - H[a].z;
+        const float d = sqrtf(dx * dx + dy * dy);
+        float s = d / (2.0f * r);
+        s = fminf(s, 1.0f);
+        const float phc = 2.0f * asinf(s);
+        const float den = sqrtf(r * r * phc * phc + z * z);
+        const float kc = phc / den;
+        const float cth = z / den, sth = r * phc / den;
+        const float ch = sqrtf(fmaxf(0.0f, 1.0f - s * s));     // cos(Phi_C / 2)
+        // dPhi/dk = (2/k^3) / (d^2 cos(Phi/2) / (4 sin^3(Phi/2)) + 2 z^2/Phi^3), sin(Phi_C/2) = d/(2r)
+        const float dphi = (2.0f / (kc * kc * kc)) / (r * r * ch / s + 2.0f * z * z / (phc * phc * phc));
+        // dtheta/dk = -z (Phi - k Phi') / (Phi^2 sin theta)
+        dth[a] = -z * (phc - kc * dphi) / (phc * phc * sth);
+        th[a] = atan2f(sth, cth);
+        if (a == 0) sth0 = sth;
+        T.phc[a] = phc;
+        T.kc[a] = kc;
+        T.dphi[a] = dphi;
+    }
+    const float dk = T.kc[1] - T.kc[0];
+    T.kref = 0.5f * (T.kc[0] + T.kc[1]);
+    T.b_phi = 0.5f * T.q * (T.dphi[0] + T.dphi[1]);
+    T.al_phi = 0.25f * T.q * dk * (T.dphi[0] - T.dphi[1]);
+    T.b_th = dth[1] - dth[0];
+    T.al_th = (th[1] - th[0]) - 0.5f * dk * (dth[1] + dth[0]);
+    const float sig = P.chl * T.kref;
+    T.w_th = 1.0f / (sig * sig);
+    T.w_phi = sth0 * sth0 * T.w_th;
+    const float A = T.b_phi * T.b_phi * T.w_phi + T.b_th * T.b_th * T.w_th;
+    if (!(A > 0.0f)) return false;
+    const float B = T.al_phi * T.b_phi * T.w_phi + T.al_th * T.b_th * T.w_th;
+    T.khat = T.kref - B / A;
+    T.var = 1.0f / A;
+    return true;
+}
+
+// chi2_t (Eq. 6, linearised) at signed global curvature kappa (Eq. 7)
+__device__ __forceinline__ float triplet_chi2(const Triplet& T, float kappa) {
+    const float del = T.q * kappa - T.kref;
+    const float fp = T.al_phi + T.b_phi * del, ft = T.al_th + T.b_th * del;
+    return fp * fp * T.w_phi + ft * ft * T.w_th;
+}
+
+// exact short-arc bending angle: root of d^2/(4 sin^2(Phi/2)) + z^2/Phi^2 = 1/k^2
+// on (0, pi] by Newton from `start` (the linearised value).  false if no short arc
+// of curvature k joins the hits (1/k^2 < d^2/4 + z^2/pi^2).
+__device__ __forceinline__ bool arc_phi(float d, float z, float k, float start, float& phi) {
+    if (!(k > 0.0f)) return false;
+    const float R2 = 1.0f / (k * k);
+    if (R2 < 0.25f * d * d + z * z * (1.0f / (kPiF * kPiF))) return false;
+    float p = fminf(fmaxf(start, 1e-6f), kPiF);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        float s, c;
+        sincosf(0.5f * p, &s, &c);
+        const float f = d * d / (4.0f * s * s) + z * z / (p * p) - R2;
+        const float fp = -d * d * c / (4.0f * s * s * s) - 2.0f * z * z / (p * p * p);
+        p = fminf(fmaxf(p - f / fp, 1e-7f), kPiF);
+    }
+    phi = p;
+    return true;
+}
+
+// Sec. IV-B-2 "Using this preliminary helix, the hit position in the fourth
+// layer is estimated" (R9): continue the arc h1 -> h2 of curvature k past h2 to
+// its first crossing of the layer-3 cylinder.
+__device__ __forceinline__ bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet& T,
+                                            float3& out) {
+    const float k = T.khat;
+    const float dx = h2.x - h1.x, dy = h2.y - h1.y, z = h2.z - h1.z;
+    const float d = sqrtf(dx * dx + dy * dy);
+    float phi;
+    if (!arc_phi(d, z, k, T.phc[1] + T.dphi[1] * (k - T.kc[1]), phi)) return false;
+    const float cth = fminf(fmaxf(z * k / phi, -1.0f), 1.0f);
+    const float sth = sqrtf(1.0f - cth * cth);
+    const float psi = atan2f(dy, dx) - T.q * 0.5f * phi;     // heading at h2
+    const float rt = sth / k;
+    float sp, cp;
+    sincosf(psi, &sp, &cp);
+    const float cx = h2.x + T.q * rt * sp, cy = h2.y - T.q * rt * cp;
+    const float C = sqrtf(cx * cx + cy * cy);
+    if (C == 0.0f) return false;
+    const float arg = (P.R3sq - C * C - rt * rt) / (2.0f * rt * C);
+    if (arg > 1.0f || arg < -1.0f) return false;
+    const float phic = atan2f(cy, cx), da = acosf(arg);
+    const float phi0 = atan2f(h2.y - cy, h2.x - cx);
+    float best = 1e30f;
+#pragma unroll
+    for (int s = -1; s <= 1; s += 2) {
+        float t = fmodf(T.q * (phi0 - (phic + s * da)), 2.0f * kPiF);
+        if (t < 0.0f) t += 2.0f * kPiF;
+        if (t > 0.0f && t < best) best = t;
+    }
+    const float ph = phi0 - T.q * best;
+    float s2, c2;
+    sincosf(ph, &s2, &c2);
+    out = make_float3(cx + rt * c2, cy + rt * s2, h2.z + cth / k * best);
+    return true;
+}
+
+// Track Reconstruction of one candidate (Sec. IV-B-2, Alg. 3, Eq. 7-8, R9-R11).
+struct FitOut {
+    int status;                  // 0 ok ... 6 domain, as m3e_fit_record.status
+    int hit3;
+    float kappa1, kappa2, var1, var2, kappa, chi2, cth01, cx, cy;
+};
+
+__device__ __forceinline__ FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, int i2,
+                                                float rtc) {
+    FitOut o;
+    o.status = 0; o.hit3 = -1;
+    o.kappa1 = o.kappa2 = o.var1 = o.var2 = o.kappa = o.chi2 = o.cth01 = o.cx = o.cy = 0.0f;
+    const float3 h0 = hit(F, 0, i0), h1 = hit(F, 1, i1), h2 = hit(F, 2, i2);
+    Triplet T1, T2;
+    if (!fit_triplet(P, h0, h1, h2, rtc, T1)) { o.status = 1; return o; }
+    o.kappa1 = T1.q * T1.khat;
+    o.var1 = T1.var;
+    float3 pred;
+    if (!extrapolate(P, h1, h2, T1, pred)) { o.status = 2; return o; }
+    if (F.n[3] == 0) { o.status = 3; return o; }
+    // find_closest_layer3_hit: 3D Euclidean, lowest index on ties (R10)
+    float best = __int_as_float(0x7f800000);
+    int bi = 0;
+    for (int i = 0; i < F.n[3]; ++i) {
+        const float3 h = hit(F, 3, i);
+        const float ex = h.x - pred.x, ey = h.y - pred.y, ez = h.z - pred.z;
+        const float d2 = ex * ex + ey * ey + ez * ez;
+        if (d2 < best) { best = d2; bi = i; }
+    }
+    o.hit3 = bi;
+    const float3 h3 = hit(F, 3, bi);
+    if (!fit_triplet(P, h1, h2, h3, circle_radius(h1, h2, h3), T2)) { o.status = 4; return o; }
+    o.kappa2 = T2.q * T2.khat;
+    o.var2 = T2.var;
+    // Eq. 8 weighted mean, Eq. 7 global chi2
+    const float w1 = 1.0f / T1.var, w2 = 1.0f / T2.var;
+    const float kb = (o.kappa1 * w1 + o.kappa2 * w2) / (w1 + w2);
+    o.kappa = kb;
+    o.chi2 = triplet_chi2(T1, kb) + triplet_chi2(T2, kb);
+    if (!(o.chi2 < P.chi2_max)) { o.status = 5; return o; }
+    // track parameters: polar angle of arc 01 at |kappa-bar|, transverse circle (R11)
+    const float k = fabsf(kb);
+    const int q = kb > 0.0f ? 1 : -1;
+    const float dx = h1.x - h0.x, dy = h1.y - h0.y, z01 = h1.z - h0.z;
+    const float d01 = sqrtf(dx * dx + dy * dy);
+    float phi01;
+    if (!arc_phi(d01, z01, k, T1.phc[0] + T1.dphi[0] * (k - T1.kc[0]), phi01)) { o.status = 6; return o; }
+    const float cth = fminf(fmaxf(z01 * k / phi01, -1.0f), 1.0f);
+    const float rt = sqrtf(1.0f - cth * cth) / k;
+    const float off = sqrtf(fmaxf(0.0f, rt * rt - 0.25f * d01 * d01));
+    const float ux = dx / d01, uy = dy / d01;
+    o.cth01 = cth;
+    o.cx = 0.5f * (h0.x + h1.x) + q * off * uy;   // clockwise: centre right of the chord
+    o.cy = 0.5f * (h0.y + h1.y) - q * off * ux;
+    return o;
+}
+
+// ------------------------------------------------------------- Vertex Fit ----
+// fp64, Sec. IV-C + Alg. 4 phase 2 for one (e+, e+, e-) triple (R12-R16).
+struct VTrk {
+    int q;
+    double k, cth, sth, cx, cy, rt, h0x, h0y, h0z, p, E, sms;
+};
+
+__device__ __forceinline__ VTrk make_vtrk(const DevParams& P, const m3e_track& t, const Frame& F) {
+    VTrk v;
+    v.q = t.kappa > 0.0f ? 1 : -1;
+    v.k = fabs((double)t.kappa);
+    v.cth = (double)t.cos_theta01;
+    v.sth = sqrt(fmax(0.0, 1.0 - v.cth * v.cth));
+    v.cx = (double)t.cx;
+    v.cy = (double)t.cy;
+    v.rt = v.sth / v.k;
+    const int g = F.s[0] + t.hit[0];
+    v.h0x = (double)F.x[g];
+    v.h0y = (double)F.y[g];
+    v.h0z = (double)F.z[g];
+    v.p = P.ptb / v.k;
+    v.E = sqrt(v.p * v.p + kEMass * kEMass);
+    v.sms = P.chl_d * v.k;   // Highland at p (R7)
+    return v;
+}
+
+__device__ __forceinline__ double wrap_pi(double a) {
+    while (a > kPi) a -= 2.0 * kPi;
+    while (a <= -kPi) a += 2.0 * kPi;
+    return a;
+}
+
+// signed turning angle from point (px,py) on the track circle to the layer-0 hit,
+// in the direction of motion, wrapped to (-pi, pi] (R12)
+__device__ __forceinline__ double turn_to_h0(const VTrk& t, double px, double py) {
+    return wrap_pi(t.q * (atan2(py - t.cy, px - t.cx) - atan2(t.h0y - t.cy, t.h0x - t.cx)));
+}
+
+// circle-circle intersections; 0 or 2 points {x0,y0,x1,y1}
+__device__ __forceinline__ int intersect(const VTrk& A, const VTrk& B, double o[4]) {
+    const double dx = B.cx - A.cx, dy = B.cy - A.cy, D = hypot(dx, dy);
+    if (D == 0.0 || D > A.rt + B.rt || D < fabs(A.rt - B.rt)) return 0;
+    const double a = (A.rt * A.rt - B.rt * B.rt + D * D) / (2.0 * D);
+    const double h = sqrt(fmax(0.0, A.rt * A.rt - a * a));
+    const double ux = dx / D, uy = dy / D;
+    o[0] = A.cx + a * ux - h * uy; o[1] = A.cy + a * uy + h * ux;
+    o[2] = A.cx + a * ux + h * uy; o[3] = A.cy + a * uy - h * ux;
+    return 2;
+}
+
+__device__ __forceinline__ double seg_dist(double px, double py, double ax, double ay, double bx, double by) {
+    const double vx = bx - ax, vy = by - ay;
+    double t = ((px - ax) * vx + (py - ay) * vy) / (vx * vx + vy * vy);
+    t = fmin(fmax(t, 0.0), 1.0);
+    return hypot(px - ax - t * vx, py - ay - t * vy);
+}
+
+// distance to the double hollow-cone target surface (R14)
+__device__ __forceinline__ double target_distance(const DevParams& P, double x, double y, double z) {
+    const double rho = hypot(x, y), R = P.target_r, L = P.target_half;
+    return fmin(seg_dist(rho, z, 0.0, -L, R, 0.0), seg_dist(rho, z, R, 0.0, 0.0, L));
+}
+
+struct VResult {
+    int found;                   // some intersection choice produced a vertex
+    int pass;
+    double x, y, z, chi2, tdist, ptot;
+};
+
+static __device__ __noinline__ VResult vertex_triple(const DevParams* __restrict__ Pp, const VTrk T[3]) {
+    const DevParams& P = *Pp;
+    VResult best;
+    best.found = 0; best.pass = 0;
+    best.x = best.y = best.z = best.tdist = best.ptot = 0.0;
+    best.chi2 = 1e300;
+    const int pr[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+    double pts[3][2][2];
+    int npt[3];
+    for (int pi = 0; pi < 3; ++pi) {
+        double o[4];
+        if (intersect(T[pr[pi][0]], T[pr[pi][1]], o) == 0) return best;   // "the track triplet is skipped"
+        npt[pi] = 0;
+        for (int s = 0; s < 2; ++s) {
+            if (hypot(o[2 * s], o[2 * s + 1]) <= P.rlim) {
+                pts[pi][npt[pi]][0] = o[2 * s];
+                pts[pi][npt[pi]][1] = o[2 * s + 1];
+                ++npt[pi];
+            }
+        }
+        if (npt[pi] == 0) return best;
+    }
+    for (int s0 = 0; s0 < npt[0]; ++s0)
+        for (int s1 = 0; s1 < npt[1]; ++s1)
+            for (int s2 = 0; s2 < npt[2]; ++s2) {
+                const int sel[3] = {s0, s1, s2};
+                double mx = 0.0, my = 0.0, ws = 0.0;
+                for (int pi = 0; pi < 3; ++pi) {                           // Eq. 10 (R13), Eq. 9
+                    const double px = pts[pi][sel[pi]][0], py = pts[pi][sel[pi]][1];
+                    const VTrk& A = T[pr[pi][0]];
+                    const VTrk& B = T[pr[pi][1]];
+                    const double sa = A.rt * fabs(turn_to_h0(A, px, py));
+                    const double sb = B.rt * fabs(turn_to_h0(B, px, py));
+                    const double s2v = 0.5 * (A.sms * A.sms * sa * sa + B.sms * B.sms * sb * sb) + P.sig_pix2;
+                    mx += px / s2v; my += py / s2v; ws += 1.0 / s2v;
+                }
+                mx /= ws; my /= ws;
+                double pcx[3], pcy[3], pcz[3], sg[3], mz = 0.0, wz = 0.0;
+                bool bad = false;
+                for (int t = 0; t < 3; ++t) {                              // Fig. 6, Eq. 11
+                    const VTrk& A = T[t];
+                    const double dx = mx - A.cx, dy = my - A.cy, dn = hypot(dx, dy);
+                    if (dn == 0.0) { bad = true; break; }
+                    pcx[t] = A.cx + A.rt * dx / dn;
+                    pcy[t] = A.cy + A.rt * dy / dn;
+                    const double dphi = turn_to_h0(A, pcx[t], pcy[t]);
+                    pcz[t] = A.h0z - dphi * A.cth / A.k;
+                    const double s = A.rt * fabs(dphi);
+                    sg[t] = A.sms * A.sms * s * s + P.sig_pix2;
+                    mz += pcz[t] / sg[t]; wz += 1.0 / sg[t];
+                }
+                if (bad) continue;
+                mz /= wz;
+                double chi = 0.0;                                          // Eq. 12 (R15)
+                for (int t = 0; t < 3; ++t) {
+                    const double ex = pcx[t] - mx, ey = pcy[t] - my, ez = pcz[t] - mz;
+                    chi += (ex * ex + ey * ey + ez * ez) / sg[t];
+                }
+                if (chi < best.chi2) {
+                    best.found = 1;
+                    best.chi2 = chi;
+                    best.x = mx; best.y = my; best.z = mz;
+                    double px = 0.0, py = 0.0, pz = 0.0;
+                    for (int t = 0; t < 3; ++t) {
+                        const VTrk& A = T[t];
+                        const double ph = atan2(pcy[t] - A.cy, pcx[t] - A.cx);
+                        px += A.p * A.sth * A.q * sin(ph);
+                        py += A.p * A.sth * (-A.q * cos(ph));
+                        pz += A.p * A.cth;
+                    }
+                    best.ptot = sqrt(px * px + py * py + pz * pz);
+                }
+            }
+    if (best.found) {
+        best.tdist = target_distance(P, best.x, best.y, best.z);
+        best.pass = best.chi2 <= P.chi2v_max && best.tdist <= P.tdist_max && best.ptot <= P.ptot_max;
+    }
+    return best;
+}
+
+}  // namespace m3e

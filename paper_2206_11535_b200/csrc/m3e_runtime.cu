@@ -1,0 +1,542 @@
+// m3e_runtime.cu -- C ABI of libm3e.so (include/m3e.h): context and workspace
+// management, parameter validation, the device-buffer entry points, and the
+// host-buffer path that streams chunks host->device on two CUDA streams so the
+// copy of chunk c+1 overlaps the filter of chunk c (Sec. V-A/V-B:
+// "one chunk to be transferred to and processed by the GPU, while the next one
+// is filled"; "CUDA streams are used").
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "m3e.h"
+#include "m3e_device.cuh"
+#include "m3e_kernels.h"
+
+using namespace m3e;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return M3E_ERR_CUDA;
+}
+#define CK(call)                                          \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// one independent set of device workspace (a CUDA stream's worth)
+struct Workspace {
+    uint32_t* ticket = nullptr;
+    uint4* status = nullptr;
+    size_t status_n = 0;
+    uint32_t* pool_idx = nullptr;
+    float* pool_rt = nullptr;
+    m3e_fit_record* pool_rec = nullptr;
+    m3e_track* pool_trk = nullptr;
+    size_t pool_stride = 0, trk_stride = 0;
+    int pool_ctas = 0;
+    uint32_t epoch = 0;
+    size_t bytes = 0;
+};
+
+// device staging of one chunk for m3e_filter_host
+struct Chunk {
+    float *x = nullptr, *y = nullptr, *z = nullptr;
+    uint32_t* offsets = nullptr;
+    uint8_t* reason = nullptr;
+    m3e_frame_out* frames = nullptr;
+    m3e_track* tracks = nullptr;
+    m3e_vertex* vertices = nullptr;
+    uint32_t* kept_frame = nullptr;
+    uint32_t* kept_offsets = nullptr;
+    float *kx = nullptr, *ky = nullptr, *kz = nullptr;
+    m3e_summary* summary = nullptr;      // device
+    m3e_summary* h_summary = nullptr;    // pinned host
+    uint64_t cap_frames = 0, cap_hits = 0, cap_tracks = 0;
+    cudaEvent_t ev_summary = nullptr, ev_free = nullptr;
+    bool used = false;
+};
+
+}  // namespace
+
+struct m3e_context {
+    int device = 0;
+    int sms = 148;
+    uint64_t max_frames = 0, max_hits = 0;
+    Workspace ws[2];
+    cudaStream_t st[2] = {nullptr, nullptr};
+    Chunk ch[2];
+    uint64_t chunk_frames = 0;
+};
+
+namespace {
+
+void free_ws(Workspace& w) {
+    cudaFree(w.ticket);
+    cudaFree(w.status);
+    cudaFree(w.pool_idx);
+    cudaFree(w.pool_rt);
+    cudaFree(w.pool_rec);
+    cudaFree(w.pool_trk);
+    w = Workspace{};
+}
+
+void free_chunk(Chunk& c) {
+    cudaFree(c.x); cudaFree(c.y); cudaFree(c.z); cudaFree(c.offsets);
+    cudaFree(c.reason); cudaFree(c.frames); cudaFree(c.tracks); cudaFree(c.vertices);
+    cudaFree(c.kept_frame); cudaFree(c.kept_offsets); cudaFree(c.kx); cudaFree(c.ky); cudaFree(c.kz);
+    cudaFree(c.summary);
+    if (c.h_summary) cudaFreeHost(c.h_summary);
+    if (c.ev_summary) cudaEventDestroy(c.ev_summary);
+    if (c.ev_free) cudaEventDestroy(c.ev_free);
+    c = Chunk{};
+}
+
+int validate(const m3e_params* p) {
+    if (!p) return fail(M3E_ERR_INVALID_ARGUMENT, "params is NULL");
+    for (int l = 0; l < 4; ++l)
+        if (!(p->layer_r[l] > 0) || (l && !(p->layer_r[l] > p->layer_r[l - 1])))
+            return fail(M3E_ERR_INVALID_ARGUMENT, "layer_r must be positive and increasing");
+    if (!(p->b_field > 0)) return fail(M3E_ERR_INVALID_ARGUMENT, "b_field must be > 0");
+    if (p->cuts_max < 1 || p->cuts_max > kMaxCutsCap)
+        return fail(M3E_ERR_INVALID_ARGUMENT, "cuts_max must be in [1, 1023]");
+    if (p->max_tracks < 1 || p->max_tracks > kMaxTracksCap)
+        return fail(M3E_ERR_INVALID_ARGUMENT, "max_tracks must be in [1, 128]");
+    if (p->max_combs < 0 || p->max_combs + 1 > kMaxCombsCap)
+        return fail(M3E_ERR_INVALID_ARGUMENT, "max_combs must be in [0, 255]");
+    if (!(p->x_over_x0 > 0)) return fail(M3E_ERR_INVALID_ARGUMENT, "x_over_x0 must be > 0");
+    if (!(p->target_r > 0) || !(p->target_half > 0))
+        return fail(M3E_ERR_INVALID_ARGUMENT, "target dimensions must be > 0");
+    return M3E_OK;
+}
+
+DevParams make_dev_params(const m3e_params* p) {
+    DevParams d;
+    for (int l = 0; l < 4; ++l) d.R[l] = (float)p->layer_r[l];
+    d.inv_dr01 = (float)(1.0 / (p->layer_r[1] - p->layer_r[0]));
+    d.inv_dr12 = (float)(1.0 / (p->layer_r[2] - p->layer_r[1]));
+    d.inv_r0r1 = (float)(1.0 / (p->layer_r[0] * p->layer_r[1]));
+    d.inv_r1r2 = (float)(1.0 / (p->layer_r[1] * p->layer_r[2]));
+    d.dl_max = (float)p->dlambda_max;
+    d.c01_min = (float)p->cos_phi01_min;
+    d.c12_min = (float)p->cos_phi12_min;
+    d.rt_min = (float)p->rt_min;
+    d.rt_max = (float)p->rt_max;
+    const double X = p->x_over_x0;
+    // Highland (R7): sigma = 13.6 MeV / p * sqrt(X) (1 + 0.038 ln X), p = PT_CONV B / k
+    const double chl = 13.6 * std::sqrt(X) * (1.0 + 0.038 * std::log(X)) / (kPtConv * p->b_field);
+    d.chl = (float)chl;
+    d.chi2_max = (float)p->chi2_max;
+    d.R3sq = (float)(p->layer_r[3] * p->layer_r[3]);
+    d.cuts_max = p->cuts_max;
+    d.max_tracks = p->max_tracks;
+    d.max_combs = p->max_combs;
+    d.ptb = kPtConv * p->b_field;
+    d.chl_d = chl;
+    d.e_window = p->e_window;
+    d.rlim = p->target_r + p->xy_margin;
+    d.sig_pix2 = p->sigma_pixel * p->sigma_pixel;
+    d.chi2v_max = p->chi2_vertex_max;
+    d.tdist_max = p->target_dist_max;
+    d.ptot_max = p->p_total_max;
+    d.target_r = p->target_r;
+    d.target_half = p->target_half;
+    return d;
+}
+
+// frames per batch: keep a batch's hits within the shared-memory window
+int choose_fb(uint64_t F, uint64_t H) {
+    if (F == 0) return kFB;
+    const double mean = (double)H / (double)F;
+    int fb = (int)((double)kHCap / (1.25 * std::max(mean, 1.0)));
+    return std::max(8, std::min(kFB, fb));
+}
+
+int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p, int fb, int ctas) {
+    if (!w.ticket) {
+        CK(cudaMalloc(&w.ticket, 16));
+        w.bytes += 16;
+    }
+    if (w.status_n < nbatch) {
+        cudaFree(w.status);
+        w.bytes -= w.status_n * sizeof(uint4);
+        const size_t n = std::max<size_t>(nbatch, 1024);
+        CK(cudaMalloc(&w.status, n * sizeof(uint4)));
+        CK(cudaMemset(w.status, 0, n * sizeof(uint4)));
+        w.status_n = n;
+        w.bytes += n * sizeof(uint4);
+        w.epoch = 0;
+    }
+    const size_t ps = (size_t)fb * p->cuts_max, ts = (size_t)fb * p->max_tracks;
+    if (w.pool_ctas < ctas || w.pool_stride < ps || w.trk_stride < ts) {
+        cudaFree(w.pool_idx); cudaFree(w.pool_rt); cudaFree(w.pool_rec); cudaFree(w.pool_trk);
+        const size_t PS = std::max(ps, (size_t)kFB * 768), TS = std::max(ts, (size_t)kFB * 64);
+        const int n = std::max(ctas, w.pool_ctas);
+        CK(cudaMalloc(&w.pool_idx, PS * n * sizeof(uint32_t)));
+        CK(cudaMalloc(&w.pool_rt, PS * n * sizeof(float)));
+        CK(cudaMalloc(&w.pool_rec, PS * n * sizeof(m3e_fit_record)));
+        CK(cudaMalloc(&w.pool_trk, TS * n * sizeof(m3e_track)));
+        w.pool_stride = PS;
+        w.trk_stride = TS;
+        w.pool_ctas = n;
+        w.bytes += PS * n * (sizeof(uint32_t) + sizeof(float) + sizeof(m3e_fit_record)) + TS * n * sizeof(m3e_track);
+    }
+    (void)c;
+    return M3E_OK;
+}
+
+uint32_t next_epoch(Workspace& w) {
+    w.epoch = (w.epoch + 1) & 0x3FFFFFFFu;
+    if (w.epoch == 0) w.epoch = 1;
+    return w.epoch;
+}
+
+// common launch of one mode over frames [0, F)
+int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, const float* x, const float* y,
+             const float* z, const uint32_t* offsets, uint64_t F, uint64_t H, KArgs a, cudaStream_t s) {
+    int rc = validate(p);
+    if (rc) return rc;
+    if (F >= (1ull << 31)) return fail(M3E_ERR_INVALID_ARGUMENT, "too many frames in one call");
+    if (F == 0) return M3E_OK;
+    if (!x || !y || !z || !offsets) return fail(M3E_ERR_INVALID_ARGUMENT, "input pointer is NULL");
+    const int fb = choose_fb(F, H);
+    const uint64_t nbatch = (F + fb - 1) / fb;
+    const int bps = blocks_per_sm(mode);
+    const int grid = (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * bps);
+    rc = ensure_ws(ctx, w, nbatch, p, fb, grid);
+    if (rc) return rc;
+    a.P = make_dev_params(p);
+    a.x = x; a.y = y; a.z = z; a.offsets = offsets;
+    a.F = (uint32_t)F;
+    a.fb = fb;
+    a.nbatch = (uint32_t)nbatch;
+    a.ticket = w.ticket;
+    a.status = w.status;
+    a.epoch = next_epoch(w);
+    a.pool_idx = w.pool_idx; a.pool_rt = w.pool_rt; a.pool_rec = w.pool_rec; a.pool_trk = w.pool_trk;
+    a.pool_stride = w.pool_stride;
+    a.trk_stride = w.trk_stride;
+    CK(cudaMemsetAsync(w.ticket, 0, sizeof(uint32_t), s));
+    if (a.out.summary) CK(cudaMemsetAsync(a.out.summary, 0, sizeof(m3e_summary), s));
+    CK(launch_filter(mode, a, grid, s));
+    return M3E_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* m3e_version(void) { return "m3e-b200 0.1 (sm_100a)"; }
+const char* m3e_last_error(void) { return g_err.c_str(); }
+
+int m3e_create(m3e_context** out, int device, uint64_t max_frames, uint64_t max_hits) {
+    if (!out) return fail(M3E_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(M3E_ERR_NO_DEVICE, "no CUDA device");
+    if (device < 0 || device >= n) return fail(M3E_ERR_INVALID_ARGUMENT, "bad device ordinal");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(M3E_ERR_NO_DEVICE, "libm3e is built for sm_100a (B200)");
+    m3e_context* c = new m3e_context();
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    c->max_frames = max_frames;
+    c->max_hits = max_hits;
+    for (int i = 0; i < 2; ++i) {
+        if (cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) != cudaSuccess) {
+            delete c;
+            return fail(M3E_ERR_CUDA, "stream creation failed");
+        }
+    }
+    *out = c;
+    return M3E_OK;
+}
+
+int m3e_destroy(m3e_context* c) {
+    if (!c) return M3E_OK;
+    cudaSetDevice(c->device);
+    for (int i = 0; i < 2; ++i) {
+        if (c->st[i]) cudaStreamSynchronize(c->st[i]);
+        free_ws(c->ws[i]);
+        free_chunk(c->ch[i]);
+        if (c->st[i]) cudaStreamDestroy(c->st[i]);
+    }
+    delete c;
+    return M3E_OK;
+}
+
+uint64_t m3e_workspace_bytes(const m3e_context* c) { return c ? c->ws[0].bytes + c->ws[1].bytes : 0; }
+
+int m3e_filter(m3e_context* ctx, const m3e_params* p, const float* x, const float* y, const float* z,
+               const uint32_t* offsets, uint64_t F, uint64_t H, const m3e_outputs* out, void* stream) {
+    if (!ctx || !out) return fail(M3E_ERR_INVALID_ARGUMENT, "ctx/out is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    KArgs a{};
+    a.out = *out;
+    if (F == 0) {
+        if (out->summary) CK(cudaMemsetAsync(out->summary, 0, sizeof(m3e_summary), s));
+        return M3E_OK;
+    }
+    return run_mode(ctx, ctx->ws[0], kModeFull, p, x, y, z, offsets, F, H, a, s);
+}
+
+int m3e_select_triplets(m3e_context* ctx, const m3e_params* p, const float* x, const float* y, const float* z,
+                        const uint32_t* offsets, uint64_t F, uint64_t H, uint32_t* cand, float* cand_rt,
+                        m3e_frame_out* frames, void* stream) {
+    if (!ctx || !cand || !cand_rt || !frames) return fail(M3E_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    KArgs a{};
+    a.s_cand = cand;
+    a.s_rt = cand_rt;
+    a.out.frames = frames;
+    return run_mode(ctx, ctx->ws[0], kModeSelect, p, x, y, z, offsets, F, H, a, s);
+}
+
+int m3e_fit_tracks(m3e_context* ctx, const m3e_params* p, const float* x, const float* y, const float* z,
+                   const uint32_t* offsets, uint64_t F, uint64_t H, const uint32_t* cand, const float* cand_rt,
+                   const uint16_t* n_cand, m3e_fit_record* rec, m3e_track* tracks, m3e_frame_out* frames,
+                   void* stream) {
+    if (!ctx || !cand || !cand_rt || !n_cand || !rec || !tracks || !frames)
+        return fail(M3E_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    KArgs a{};
+    a.s_cand = const_cast<uint32_t*>(cand);
+    a.s_rt = const_cast<float*>(cand_rt);
+    a.s_ncand = n_cand;
+    a.s_rec = rec;
+    a.s_trk = tracks;
+    a.out.frames = frames;
+    return run_mode(ctx, ctx->ws[0], kModeFit, p, x, y, z, offsets, F, H, a, s);
+}
+
+int m3e_vertex_select(m3e_context* ctx, const m3e_params* p, const float* x, const float* y, const float* z,
+                      const uint32_t* offsets, uint64_t F, uint64_t H, const m3e_track* tracks, const uint16_t* n_tracks,
+                      m3e_frame_out* frames, m3e_vertex* vertices, void* stream) {
+    if (!ctx || !tracks || !n_tracks || !frames) return fail(M3E_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    KArgs a{};
+    a.s_trk = const_cast<m3e_track*>(tracks);
+    a.s_ntrk = n_tracks;
+    a.s_vtx = vertices;
+    a.out.frames = frames;
+    return run_mode(ctx, ctx->ws[0], kModeVertex, p, x, y, z, offsets, F, H, a, s);
+}
+
+int m3e_pack_frames(m3e_context* ctx, const float* x, const float* y, const float* z, const uint32_t* offsets,
+                    uint64_t F, uint64_t H, const uint8_t* reason, const m3e_outputs* out, void* stream) {
+    if (!ctx || !reason || !out) return fail(M3E_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    // the packer needs no cut parameters; run with a valid default set
+    m3e_params p{};
+    const double R[4] = {23.3, 29.8, 73.9, 86.3};
+    for (int l = 0; l < 4; ++l) p.layer_r[l] = R[l];
+    p.b_field = 1.0; p.target_r = 19.0; p.target_half = 50.0; p.cuts_max = 768; p.max_tracks = 64;
+    p.max_combs = 64; p.x_over_x0 = 1e-3;
+    KArgs a{};
+    a.s_reason = reason;
+    a.out = *out;
+    a.out.tracks = nullptr;
+    if (F == 0) {
+        if (out->summary) CK(cudaMemsetAsync(out->summary, 0, sizeof(m3e_summary), s));
+        return M3E_OK;
+    }
+    return run_mode(ctx, ctx->ws[0], kModePack, &p, x, y, z, offsets, F, H, a, s);
+}
+
+// ------------------------------------------------------------ host path ----
+static int ensure_chunk(Chunk& c, uint64_t frames, uint64_t hits, bool want_tracks, uint64_t max_tracks) {
+    if (c.cap_frames >= frames && c.cap_hits >= hits && (!want_tracks || c.cap_tracks >= frames * max_tracks))
+        return M3E_OK;
+    free_chunk(c);
+    c.cap_frames = frames;
+    c.cap_hits = hits;
+    const size_t hb = (hits + 8) * sizeof(float);
+    CK(cudaMalloc(&c.x, hb)); CK(cudaMalloc(&c.y, hb)); CK(cudaMalloc(&c.z, hb));
+    CK(cudaMalloc(&c.offsets, (4 * frames + 4) * sizeof(uint32_t)));
+    CK(cudaMalloc(&c.reason, frames));
+    CK(cudaMalloc(&c.frames, frames * sizeof(m3e_frame_out)));
+    CK(cudaMalloc(&c.vertices, frames * sizeof(m3e_vertex)));
+    CK(cudaMalloc(&c.kept_frame, frames * sizeof(uint32_t)));
+    CK(cudaMalloc(&c.kept_offsets, (4 * frames + 1) * sizeof(uint32_t)));
+    CK(cudaMalloc(&c.kx, hb)); CK(cudaMalloc(&c.ky, hb)); CK(cudaMalloc(&c.kz, hb));
+    CK(cudaMalloc(&c.summary, sizeof(m3e_summary)));
+    CK(cudaMallocHost(&c.h_summary, sizeof(m3e_summary)));
+    if (want_tracks) {
+        c.cap_tracks = frames * max_tracks;
+        CK(cudaMalloc(&c.tracks, c.cap_tracks * sizeof(m3e_track)));
+    }
+    CK(cudaEventCreateWithFlags(&c.ev_summary, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c.ev_free, cudaEventDisableTiming));
+    return M3E_OK;
+}
+
+int m3e_filter_host(m3e_context* ctx, const m3e_params* p, const float* x, const float* y, const float* z,
+                    const uint32_t* offsets, uint64_t F, const m3e_outputs* out) {
+    if (!ctx || !out) return fail(M3E_ERR_INVALID_ARGUMENT, "ctx/out is NULL");
+    int rc = validate(p);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device));
+    m3e_summary total{};
+    if (F == 0) {
+        if (out->summary) *out->summary = total;
+        return M3E_OK;
+    }
+    if (!x || !y || !z || !offsets) return fail(M3E_ERR_INVALID_ARGUMENT, "input pointer is NULL");
+    // chunk size: bounded by the context limits, at most 2^20 frames per chunk
+    const uint64_t cf = std::max<uint64_t>(1, std::min<uint64_t>({F, ctx->max_frames ? ctx->max_frames : F,
+                                                                   (uint64_t)1 << 20}));
+    uint64_t max_chunk_hits = 0;
+    for (uint64_t a = 0; a < F; a += cf) {
+        const uint64_t b = std::min(F, a + cf);
+        max_chunk_hits = std::max<uint64_t>(max_chunk_hits, offsets[4 * b] - offsets[4 * a] + 8);
+    }
+    const bool want_tracks = out->tracks != nullptr || out->frames != nullptr;
+    for (int i = 0; i < 2; ++i) {
+        rc = ensure_chunk(ctx->ch[i], cf, max_chunk_hits, want_tracks, (uint64_t)p->max_tracks);
+        if (rc) return rc;
+        ctx->ch[i].used = false;
+    }
+    struct Done {
+        uint64_t a, b;
+        int set;
+    };
+    std::vector<Done> pending;
+    uint64_t base_trk = 0, base_kept = 0, base_hits = 0;
+    auto finish = [&](const Done& d) -> int {
+        Chunk& c = ctx->ch[d.set];
+        cudaStream_t s = ctx->st[d.set];
+        CK(cudaEventSynchronize(c.ev_summary));
+        const m3e_summary sm = *c.h_summary;
+        uint64_t K = 0;
+        for (int r = 1; r < 6; ++r) K += sm.kept_by_reason[r];
+        const uint64_t Hk = sm.kept_hits, T = sm.tracks;
+        if (sm.overflow) return fail(M3E_ERR_CAPACITY, "device chunk capacity exceeded");
+        if ((out->kept_frame || out->vertices || out->kept_offsets) && base_kept + K > out->kept_capacity)
+            return fail(M3E_ERR_CAPACITY, "kept_capacity too small");
+        if (out->kept_x && base_hits + Hk > out->kept_hit_capacity)
+            return fail(M3E_ERR_CAPACITY, "kept_hit_capacity too small");
+        if (out->tracks && base_trk + T > out->track_capacity)
+            return fail(M3E_ERR_CAPACITY, "track_capacity too small");
+        const uint64_t nfr = d.b - d.a;
+        if (out->reason) CK(cudaMemcpyAsync(out->reason + d.a, c.reason, nfr, cudaMemcpyDeviceToHost, s));
+        if (out->frames)
+            CK(cudaMemcpyAsync(out->frames + d.a, c.frames, nfr * sizeof(m3e_frame_out), cudaMemcpyDeviceToHost, s));
+        if (out->tracks && T)
+            CK(cudaMemcpyAsync(out->tracks + base_trk, c.tracks, T * sizeof(m3e_track), cudaMemcpyDeviceToHost, s));
+        if (K) {
+            if (out->kept_frame)
+                CK(cudaMemcpyAsync(out->kept_frame + base_kept, c.kept_frame, K * 4, cudaMemcpyDeviceToHost, s));
+            if (out->kept_offsets)
+                CK(cudaMemcpyAsync(out->kept_offsets + 4 * base_kept, c.kept_offsets, 4 * K * 4,
+                                   cudaMemcpyDeviceToHost, s));
+            if (out->vertices)
+                CK(cudaMemcpyAsync(out->vertices + base_kept, c.vertices, K * sizeof(m3e_vertex),
+                                   cudaMemcpyDeviceToHost, s));
+        }
+        if (Hk && out->kept_x) {
+            CK(cudaMemcpyAsync(out->kept_x + base_hits, c.kx, Hk * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(out->kept_y + base_hits, c.ky, Hk * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(out->kept_z + base_hits, c.kz, Hk * 4, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaEventRecord(c.ev_free, s));
+        CK(cudaEventSynchronize(c.ev_free));
+        // chunk-local indices -> call-global indices
+        if (out->frames)
+            for (uint64_t f = 0; f < nfr; ++f) {
+                m3e_frame_out& fo = out->frames[d.a + f];
+                fo.track_first += (uint32_t)base_trk;
+                if (fo.kept_index != 0xFFFFFFFFu) fo.kept_index += (uint32_t)base_kept;
+            }
+        if (out->tracks)
+            for (uint64_t t = 0; t < T; ++t) out->tracks[base_trk + t].frame += (uint32_t)d.a;
+        for (uint64_t k = 0; k < K; ++k) {
+            if (out->kept_frame) out->kept_frame[base_kept + k] += (uint32_t)d.a;
+            if (out->kept_offsets)
+                for (int l = 0; l < 4; ++l) out->kept_offsets[4 * (base_kept + k) + l] += (uint32_t)base_hits;
+            if (out->vertices && out->vertices[base_kept + k].frame != 0xFFFFFFFFu)
+                out->vertices[base_kept + k].frame += (uint32_t)d.a;
+        }
+        total.frames += sm.frames;
+        for (int r = 0; r < 6; ++r) total.kept_by_reason[r] += sm.kept_by_reason[r];
+        total.candidates += sm.candidates;
+        total.tracks += sm.tracks;
+        total.kept_hits += sm.kept_hits;
+        total.vertices += sm.vertices;
+        base_trk += T;
+        base_kept += K;
+        base_hits += Hk;
+        return M3E_OK;
+    };
+    int ci = 0;
+    for (uint64_t a = 0; a < F; a += cf, ++ci) {
+        const uint64_t b = std::min(F, a + cf);
+        const int set = ci & 1;
+        Chunk& c = ctx->ch[set];
+        cudaStream_t s = ctx->st[set];
+        // the previous user of this set must have been drained (finish() syncs ev_free)
+        if (pending.size() >= 2) {
+            rc = finish(pending.front());
+            if (rc) return rc;
+            pending.erase(pending.begin());
+        }
+        const uint64_t h0 = offsets[4 * a], h1 = offsets[4 * b];
+        const uint64_t h0a = h0 & ~3ull;           // keep 16 B alignment of the bulk copies
+        const uint64_t nh = h1 - h0a;
+        if (nh) {
+            CK(cudaMemcpyAsync(c.x, x + h0a, nh * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(c.y, y + h0a, nh * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(c.z, z + h0a, nh * 4, cudaMemcpyHostToDevice, s));
+        }
+        CK(cudaMemcpyAsync(c.offsets, offsets + 4 * a, (4 * (b - a) + 1) * 4, cudaMemcpyHostToDevice, s));
+        m3e_outputs o{};
+        o.reason = c.reason;
+        o.frames = c.frames;
+        o.tracks = want_tracks ? c.tracks : nullptr;
+        o.track_capacity = c.cap_tracks;
+        o.vertices = c.vertices;
+        o.kept_frame = c.kept_frame;
+        o.kept_offsets = c.kept_offsets;
+        o.kept_capacity = c.cap_frames;
+        o.kept_x = c.kx; o.kept_y = c.ky; o.kept_z = c.kz;
+        o.kept_hit_capacity = c.cap_hits;
+        o.summary = c.summary;
+        KArgs ka{};
+        ka.out = o;
+        // hit pointers shifted so that the (global) offsets index the chunk's copy
+        rc = run_mode(ctx, ctx->ws[set], kModeFull, p, c.x - h0a, c.y - h0a, c.z - h0a, c.offsets, b - a,
+                      h1 - h0, ka, s);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(c.h_summary, c.summary, sizeof(m3e_summary), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(c.ev_summary, s));
+        pending.push_back({a, b, set});
+    }
+    for (const Done& d : pending) {
+        rc = finish(d);
+        if (rc) return rc;
+    }
+    if (out->kept_offsets) out->kept_offsets[4 * base_kept] = (uint32_t)base_hits;
+    if (out->summary) *out->summary = total;
+    return M3E_OK;
+}
+
+}  // extern "C"
+
+static_assert(sizeof(m3e_frame_out) == 16, "m3e_frame_out layout");
+static_assert(sizeof(m3e_track) == 32, "m3e_track layout");
+static_assert(sizeof(m3e_vertex) == 56, "m3e_vertex layout");
+static_assert(sizeof(m3e_fit_record) == 40, "m3e_fit_record layout");
+static_assert(sizeof(m3e_summary) == 96, "m3e_summary layout");
