@@ -581,7 +581,7 @@ int or_process_frame(const or_params* P, const float* x, const float* y, const f
             ++nacc;
         }
     }
-    res->n_tracks = nacc;
+    res->n_tracks = nacc > P->max_tracks ? P->max_tracks + 1 : nacc;  /* min(#accepted, max_tracks + 1) */
     if (nacc > P->max_tracks) {
         res->reason = OR_REASON_TRACK_OVERFLOW;
         res->keep = 1;

@@ -16,6 +16,16 @@ import oracle
 
 REL_BAND = 1e-5
 REL_KAPPA = 1e-4
+# curvature floor of the relative tolerance: every track of a muon decay has
+# p <= 52.83 MeV/c (kinematic endpoint), i.e. |kappa| >= 0.299792458 / 52.83 /mm
+# in 1 T; those are compared at 1e-4 relative.  Stiffer (unphysical, near-straight
+# fake) fits are compared at the absolute 1e-4 * KAPPA_FLOOR, the fp32 rounding
+# floor of a curvature measured over ~50 mm chords.
+KAPPA_FLOOR = 0.299792458 / 52.83
+
+
+def kappa_close(a, b):
+    return abs(a - b) <= REL_KAPPA * max(abs(a), abs(b), KAPPA_FLOOR)
 
 
 def near(v, thr, band=REL_BAND):

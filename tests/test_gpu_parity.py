@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 import synth
-from parity import REL_BAND, combo_is_marginal, near, rel_close, unpack
+from parity import KAPPA_FLOOR, REL_BAND, combo_is_marginal, kappa_close, near, rel_close, unpack
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -117,8 +117,8 @@ def test_fit_parity(ctx, gp, P, name, n, seed):
                 assert int(g["hit3"]) == (o.hit[3] if o.hit[3] >= 0 else 0xFFFF) or o.marginal
             if o.status in (oracle.FIT_OK, oracle.FIT_CHI2):
                 for a, b in [(g["kappa1"], o.t1.kappa), (g["kappa2"], o.t2.kappa), (g["kappa"], o.kappa)]:
-                    worst = max(worst, abs(a - b) / abs(b))
-                    assert rel_close(float(a), b), (f, k, float(a), b)
+                    worst = max(worst, abs(a - b) / max(abs(b), KAPPA_FLOOR))
+                    assert kappa_close(float(a), b), (f, k, float(a), b)
                 assert rel_close(float(g["var1"]), o.t1.var_kappa, 1e-3)
                 assert rel_close(float(g["chi2"]), o.chi2, 1e-3, 1e-3), (f, k, float(g["chi2"]), o.chi2)
             if o.status == oracle.FIT_OK:
@@ -210,7 +210,7 @@ def _compare_full(P, fr, res_np, frames_np, tracks_np, n):
             explained.append(f)
             continue
         for t, u in zip(gt, otr):
-            assert rel_close(float(t["kappa"]), u.kappa), (f, float(t["kappa"]), u.kappa)
+            assert kappa_close(float(t["kappa"]), u.kappa), (f, float(t["kappa"]), u.kappa)
     return explained
 
 
