@@ -9,8 +9,13 @@
 
 #include "m3e.h"
 
+// fp32 fit math is also compiled for the host (tools/fit_numerics.cu) to study
+// its rounding against the oracle without a GPU
+#define M3E_HD __host__ __device__ __forceinline__
+
 namespace m3e {
 
+constexpr float kInfF = __builtin_huge_valf();
 constexpr float kPiF = 3.14159265358979323846f;
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kMuMass = 105.6583755;   // MeV (PDG), m_mu c^2 of Eq. 1
@@ -42,7 +47,7 @@ struct Frame {                  // one frame's hits, pointers to its first hit
     int n[4];                   // hits per layer
 };
 
-__device__ __forceinline__ float3 hit(const Frame& F, int layer, int i) {
+M3E_HD float3 hit(const Frame& F, int layer, int i) {
     int g = F.s[layer] + i;
     return make_float3(F.x[g], F.y[g], F.z[g]);
 }
@@ -50,10 +55,10 @@ __device__ __forceinline__ float3 hit(const Frame& F, int layer, int i) {
 // ---------------------------------------------------------------- Eq. 5 ----
 // r_tc = d01 d12 d20 / (2 [(h0 - h1) x (h2 - h1)]_z); > 0 clockwise (R5);
 // collinear -> +inf.
-__device__ __forceinline__ float circle_radius(float3 h0, float3 h1, float3 h2) {
+M3E_HD float circle_radius(float3 h0, float3 h1, float3 h2) {
     float ax = h0.x - h1.x, ay = h0.y - h1.y, bx = h2.x - h1.x, by = h2.y - h1.y;
     float cz = ax * by - ay * bx;
-    if (cz == 0.0f) return __int_as_float(0x7f800000);
+    if (cz == 0.0f) return kInfF;
     float cx = h2.x - h0.x, cy = h2.y - h0.y;
     float d01 = sqrtf(ax * ax + ay * ay), d12 = sqrtf(bx * bx + by * by), d20 = sqrtf(cx * cx + cy * cy);
     return d01 * d12 * d20 / (2.0f * cz);
@@ -134,9 +139,9 @@ struct Triplet {
     float phc[2], kc[2], dphi[2];
 };
 
-__device__ __forceinline__ bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2, float rtc,
+M3E_HD bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2, float rtc,
                                             Triplet& T) {
-    if (!(fabsf(rtc) < __int_as_float(0x7f800000))) return false;
+    if (!(fabsf(rtc) < kInfF)) return false;
     T.q = rtc > 0.0f ? 1 : -1;
     const float r = fabsf(rtc);
     float th[2], sth0 = 0.0f, dth[2];
@@ -180,7 +185,7 @@ __device__ __forceinline__ bool fit_triplet(const DevParams& P, float3 h0, float
 }
 
 // chi2_t (Eq. 6, linearised) at signed global curvature kappa (Eq. 7)
-__device__ __forceinline__ float triplet_chi2(const Triplet& T, float kappa) {
+M3E_HD float triplet_chi2(const Triplet& T, float kappa) {
     const float del = T.q * kappa - T.kref;
     const float fp = T.al_phi + T.b_phi * del, ft = T.al_th + T.b_th * del;
     return fp * fp * T.w_phi + ft * ft * T.w_th;
@@ -189,7 +194,7 @@ __device__ __forceinline__ float triplet_chi2(const Triplet& T, float kappa) {
 // exact short-arc bending angle: root of d^2/(4 sin^2(Phi/2)) + z^2/Phi^2 = 1/k^2
 // on (0, pi] by Newton from `start` (the linearised value).  false if no short arc
 // of curvature k joins the hits (1/k^2 < d^2/4 + z^2/pi^2).
-__device__ __forceinline__ bool arc_phi(float d, float z, float k, float start, float& phi) {
+M3E_HD bool arc_phi(float d, float z, float k, float start, float& phi) {
     if (!(k > 0.0f)) return false;
     const float R2 = 1.0f / (k * k);
     if (R2 < 0.25f * d * d + z * z * (1.0f / (kPiF * kPiF))) return false;
@@ -209,7 +214,7 @@ __device__ __forceinline__ bool arc_phi(float d, float z, float k, float start, 
 // Sec. IV-B-2 "Using this preliminary helix, the hit position in the fourth
 // layer is estimated" (R9): continue the arc h1 -> h2 of curvature k past h2 to
 // its first crossing of the layer-3 cylinder.
-__device__ __forceinline__ bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet& T,
+M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet& T,
                                             float3& out) {
     const float k = T.khat;
     const float dx = h2.x - h1.x, dy = h2.y - h1.y, z = h2.z - h1.z;
@@ -250,7 +255,7 @@ struct FitOut {
     float kappa1, kappa2, var1, var2, kappa, chi2, cth01, cx, cy;
 };
 
-__device__ __forceinline__ FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, int i2,
+M3E_HD FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, int i2,
                                                 float rtc) {
     FitOut o;
     o.status = 0; o.hit3 = -1;
@@ -264,7 +269,7 @@ __device__ __forceinline__ FitOut fit_candidate(const DevParams& P, const Frame&
     if (!extrapolate(P, h1, h2, T1, pred)) { o.status = 2; return o; }
     if (F.n[3] == 0) { o.status = 3; return o; }
     // find_closest_layer3_hit: 3D Euclidean, lowest index on ties (R10)
-    float best = __int_as_float(0x7f800000);
+    float best = kInfF;
     int bi = 0;
     for (int i = 0; i < F.n[3]; ++i) {
         const float3 h = hit(F, 3, i);

@@ -81,6 +81,17 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
 }
 
 // ----------------------------------------------------------- shared state ----
+// per-frame results of one batch; two copies, because a batch's outputs are
+// written only after the CTA has computed its next batch (deferred look-back)
+struct BatchState {
+    int nstored[kFB], ncand[kFB], ntrk[kFB], nneg[kFB], ncomb[kFB], reason[kFB];
+    uint32_t o_trk[kFB + 1], o_kept[kFB + 1], o_hits[kFB + 1];   // exclusive prefixes (+ total)
+    uint32_t offs[4 * kFB + 4];                                // the batch's offsets (packer)
+    m3e_vertex vtx[kFB];
+    uint32_t batch;
+    int nf;
+};
+
 struct Smem {
     float hx[2][kHCap];
     float hy[2][kHCap];
@@ -88,12 +99,9 @@ struct Smem {
     uint32_t offs[2][4 * kFB + 4];
     uint64_t bar[2];
     uint32_t b_batch[2], b_winlo[2], b_winhi[2];
-    // per-frame state of the batch being processed
-    int nstored[kFB], ncand[kFB], ntrk[kFB], nneg[kFB], ncomb[kFB], reason[kFB];
+    BatchState st[2];
     uint32_t pref[kFB + 1];                                   // candidates: exclusive prefix
-    uint32_t o_trk[kFB + 1], o_kept[kFB + 1], o_hits[kFB + 1];  // outputs: exclusive prefixes
-    uint32_t g_trk, g_kept, g_hits;                            // batch's global bases
-    m3e_vertex vtx[kFB];
+    uint32_t g_trk, g_kept, g_hits;                            // finalized batch's global bases
     uint8_t vlist[kWarps][2][kMaxTracksCap];
     uint32_t vcomb[kWarps][kMaxCombsCap];
     unsigned long long s_kept[6], s_cand, s_trk, s_hits, s_vtx, s_frames;
@@ -186,18 +194,20 @@ __device__ __forceinline__ double track_energy(const DevParams& P, float kappa) 
     return sqrt(p * p + kEMass * kEMass);
 }
 
-// decoupled look-back (warp 0): exclusive prefix of this batch's aggregate over
-// all earlier batches of this launch; status word = {epoch<<2 | state, v0, v1, v2},
-// state 1 = aggregate published, 2 = inclusive prefix published.
-__device__ __forceinline__ uint3 lookback(const KArgs& A, uint32_t b, uint3 agg) {
+// Decoupled look-back (warp 0).  Status word of batch b = {epoch<<2 | state,
+// tracks, kept frames, kept hits}; state 1 = aggregate, 2 = inclusive prefix.
+// publish_aggregate() runs as soon as the batch's counts are known; resolve()
+// runs one batch later (deferred), so the predecessors have normally published.
+__device__ __forceinline__ void publish_aggregate(const KArgs& A, uint32_t b, uint3 agg) {
+    const uint32_t tag = (A.epoch << 2) | (b == 0 ? 2u : 1u);
+    if ((threadIdx.x & 31) == 0) st_volatile_v4(A.status + b, make_uint4(tag, agg.x, agg.y, agg.z));
+}
+
+__device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) {
     const int lane = threadIdx.x & 31;
     const uint32_t tagA = (A.epoch << 2) | 1u, tagI = (A.epoch << 2) | 2u;
     uint3 ex = make_uint3(0, 0, 0);
-    if (b == 0) {
-        if (lane == 0) st_volatile_v4(A.status, make_uint4(tagI, agg.x, agg.y, agg.z));
-        return ex;
-    }
-    if (lane == 0) st_volatile_v4(A.status + b, make_uint4(tagA, agg.x, agg.y, agg.z));
+    if (b == 0) return ex;
     int j = (int)b - 1;
     for (;;) {
         const int idx = j - lane;
@@ -222,6 +232,112 @@ __device__ __forceinline__ uint3 lookback(const KArgs& A, uint32_t b, uint3 agg)
     return ex;
 }
 
+// Write the outputs of a batch whose counts and prefixes are in B (all threads):
+// per-frame records, the packed kept frames (Sec. V-A), vertices and tracks.
+template <int MODE>
+__device__ __forceinline__ void finalize_batch(const KArgs& A, Smem& S, const BatchState& B,
+                                               const m3e_track* trk) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nf = B.nf;
+    const uint32_t f0 = B.batch * (uint32_t)A.fb;
+    if (warp == 0) {
+        const uint3 ex = resolve(A, B.batch, make_uint3(B.o_trk[nf], B.o_kept[nf], B.o_hits[nf]));
+        if (lane == 0) {
+            S.g_trk = ex.x;
+            S.g_kept = ex.y;
+            S.g_hits = ex.z;
+        }
+    }
+    __syncthreads();
+    const m3e_outputs& O = A.out;
+    const uint32_t g_trk = S.g_trk, g_kept = S.g_kept, g_hits = S.g_hits;
+    for (int j = tid; j < nf; j += kThreads) {
+        const int r = B.reason[j];
+        const bool kept = r != M3E_REASON_NONE;
+        const uint32_t kidx = g_kept + B.o_kept[j];
+        if (O.reason) O.reason[f0 + j] = (uint8_t)r;
+        if (O.frames) {
+            m3e_frame_out fo;
+            fo.n_cand = (uint16_t)B.ncand[j];
+            fo.n_tracks = (uint16_t)B.ntrk[j];
+            fo.n_combs = (uint16_t)B.ncomb[j];
+            fo.reason = (uint8_t)r;
+            fo.n_neg = (uint8_t)min(B.nneg[j], 255);
+            fo.track_first = g_trk + B.o_trk[j];
+            fo.kept_index = kept ? kidx : 0xFFFFFFFFu;
+            O.frames[f0 + j] = fo;
+        }
+        if (kept) {
+            const uint32_t hb = g_hits + B.o_hits[j];
+            if (kidx < O.kept_capacity) {
+                if (O.kept_frame) O.kept_frame[kidx] = f0 + j;
+                if (O.kept_offsets)
+                    for (int l = 0; l < 4; ++l)
+                        O.kept_offsets[4 * (size_t)kidx + l] = hb + (B.offs[4 * j + l] - B.offs[4 * j]);
+                if (O.vertices) {
+                    m3e_vertex v;
+                    if (r == M3E_REASON_VERTEX) {
+                        v = B.vtx[j];
+                    } else {
+                        v = m3e_vertex{};
+                        v.frame = 0xFFFFFFFFu;
+                    }
+                    O.vertices[kidx] = v;
+                }
+            } else {
+                S.s_overflow = 1;
+            }
+        }
+    }
+    if (B.batch == A.nbatch - 1 && tid == 0 && O.kept_offsets) {  // the last batch closes the offsets
+        const uint32_t K = g_kept + B.o_kept[nf];
+        if (K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = g_hits + B.o_hits[nf];
+    }
+    if constexpr (MODE == kModeFull) {
+        const uint32_t nt = B.o_trk[nf];
+        if (O.tracks) {
+            for (uint32_t e = tid; e < nt; e += kThreads) {
+                const int j = find_frame(B.o_trk, nf, e);
+                const uint32_t dst = g_trk + e;
+                if (dst < O.track_capacity) {
+                    const uint4* s4 = reinterpret_cast<const uint4*>(trk + (size_t)j * A.P.max_tracks + (e - B.o_trk[j]));
+                    uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst);
+                    d4[0] = s4[0];
+                    d4[1] = s4[1];
+                } else {
+                    S.s_overflow = 1;
+                }
+            }
+        }
+    }
+    // packer: hits of the kept frames, verbatim, read from HBM (Sec. V-A)
+    const uint32_t nh = B.o_hits[nf];
+    if (O.kept_x) {
+        for (uint32_t e = tid; e < nh; e += kThreads) {
+            const int j = find_frame(B.o_hits, nf, e);
+            const uint32_t g = B.offs[4 * j] + (e - B.o_hits[j]);
+            const uint32_t dst = g_hits + e;
+            if (dst < O.kept_hit_capacity) {
+                O.kept_x[dst] = A.x[g];
+                O.kept_y[dst] = A.y[g];
+                O.kept_z[dst] = A.z[g];
+            } else {
+                S.s_overflow = 1;
+            }
+        }
+    }
+    if (tid == 0) {
+        S.s_frames += nf;
+        S.s_trk += B.o_trk[nf];
+        S.s_hits += B.o_hits[nf];
+        for (int j = 0; j < nf; ++j) {
+            S.s_kept[B.reason[j]] += 1;
+            S.s_cand += B.nstored[j];
+            S.s_vtx += B.reason[j] == M3E_REASON_VERTEX;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ kernel ----
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
@@ -230,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const DevParams& P = A.P;
+    constexpr bool kOut = MODE == kModeFull || MODE == kModePack;   // ordered outputs
 
     if (tid == 0) {
         S.P = A.P;
@@ -242,24 +359,26 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
         issue_load(A, S, 0, atomicAdd(A.ticket, 1u));
     }
     __syncthreads();
-    int buf = 0;
+    int buf = 0, par = 0;
+    bool pending = false;   // S.st[par ^ 1] holds a computed batch whose outputs are not written yet
     uint32_t phase0 = 0u, phase1 = 0u;
 
-    // candidate / track slots: per-CTA scratch (FULL) or the caller's fixed slots
+    // candidate / track slots: per-CTA scratch (FULL; tracks double-buffered by
+    // batch parity) or the caller's fixed slots (stage modes)
     uint32_t* cidx;
     float* crt;
     m3e_fit_record* crec;
-    m3e_track* ctrk;
+    m3e_track* ctrk_base;
     if constexpr (MODE == kModeFull) {
         cidx = A.pool_idx + (size_t)blockIdx.x * A.pool_stride;
         crt = A.pool_rt + (size_t)blockIdx.x * A.pool_stride;
         crec = A.pool_rec + (size_t)blockIdx.x * A.pool_stride;
-        ctrk = A.pool_trk + (size_t)blockIdx.x * A.trk_stride;
+        ctrk_base = A.pool_trk + (size_t)blockIdx.x * 2 * A.trk_stride;
     } else {
         cidx = A.s_cand;
         crt = A.s_rt;
         crec = A.s_rec;
-        ctrk = A.s_trk;
+        ctrk_base = A.s_trk;
     }
 
     for (;;) {
@@ -269,10 +388,16 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
         if (buf == 0) { mbar_wait(&S.bar[0], phase0); phase0 ^= 1u; }
         else { mbar_wait(&S.bar[1], phase1); phase1 ^= 1u; }
 
+        BatchState& B = S.st[par];
         const uint32_t f0 = b * (uint32_t)A.fb;
         const int nf = (int)min(A.F - f0, (uint32_t)A.fb);
         const size_t cfirst = MODE == kModeFull ? 0 : (size_t)f0 * P.cuts_max;   // slot of frame 0
         const size_t tfirst = MODE == kModeFull ? 0 : (size_t)f0 * P.max_tracks;
+        m3e_track* ctrk = MODE == kModeFull ? ctrk_base + (size_t)par * A.trk_stride : ctrk_base;
+        if (tid == 0) {
+            B.batch = b;
+            B.nf = nf;
+        }
 
         // ---------------------------------------------------- S: Selection Cuts
         if constexpr (MODE == kModeFull || MODE == kModeSelect) {
@@ -290,41 +415,57 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                     });
                 }
                 if (lane == 0) {
-                    S.ncand[j] = count;
+                    B.ncand[j] = count;
                     const int r = inval ? M3E_REASON_INVALID
                                         : (count > P.cuts_max ? M3E_REASON_TRIPLET_OVERFLOW : M3E_REASON_NONE);
-                    S.reason[j] = r;
-                    S.nstored[j] = r == M3E_REASON_NONE ? count : 0;
+                    B.reason[j] = r;
+                    B.nstored[j] = r == M3E_REASON_NONE ? count : 0;
                 }
             }
         } else if constexpr (MODE == kModeFit) {
             for (int j = tid; j < nf; j += kThreads) {
                 const int n = A.s_ncand[f0 + j];
-                S.ncand[j] = n;
-                S.reason[j] = n > P.cuts_max ? M3E_REASON_TRIPLET_OVERFLOW : M3E_REASON_NONE;
-                S.nstored[j] = n > P.cuts_max ? 0 : n;
+                B.ncand[j] = n;
+                B.reason[j] = n > P.cuts_max ? M3E_REASON_TRIPLET_OVERFLOW : M3E_REASON_NONE;
+                B.nstored[j] = n > P.cuts_max ? 0 : n;
             }
         } else if constexpr (MODE == kModeVertex) {
             for (int j = tid; j < nf; j += kThreads) {
-                S.ncand[j] = 0;
-                S.reason[j] = M3E_REASON_NONE;
-                S.ntrk[j] = min((int)A.s_ntrk[f0 + j], P.max_tracks);
+                B.ncand[j] = 0;
+                B.nstored[j] = 0;
+                B.reason[j] = M3E_REASON_NONE;
+                B.ntrk[j] = min((int)A.s_ntrk[f0 + j], P.max_tracks);
             }
         } else {  // kModePack
             for (int j = tid; j < nf; j += kThreads) {
-                S.ncand[j] = 0;
-                S.ntrk[j] = 0;
-                S.ncomb[j] = 0;
-                S.nneg[j] = 0;
-                S.reason[j] = A.s_reason[f0 + j];
+                B.ncand[j] = 0;
+                B.nstored[j] = 0;
+                B.ntrk[j] = 0;
+                B.ncomb[j] = 0;
+                B.nneg[j] = 0;
+                B.reason[j] = A.s_reason[f0 + j];
             }
         }
         __syncthreads();
 
+        if constexpr (MODE == kModeSelect) {
+            for (int j = tid; j < nf; j += kThreads) {
+                m3e_frame_out fo;
+                fo.n_cand = (uint16_t)B.ncand[j];
+                fo.n_tracks = 0;
+                fo.n_combs = 0;
+                fo.reason = (uint8_t)B.reason[j];
+                fo.n_neg = 0;
+                fo.track_first = (uint32_t)(tfirst + (size_t)j * P.max_tracks);
+                fo.kept_index = 0xFFFFFFFFu;
+                A.out.frames[f0 + j] = fo;
+            }
+        }
+
         // -------------------------------------- F: Triplet fit, one lane per candidate
         if constexpr (MODE == kModeFull || MODE == kModeFit) {
             if (warp == 0) {
-                for (int j = lane; j < nf; j += 32) S.pref[j] = (uint32_t)S.nstored[j];
+                for (int j = lane; j < nf; j += 32) S.pref[j] = (uint32_t)B.nstored[j];
                 __syncwarp();
                 warp_scan64(S.pref, nf);
             }
@@ -355,11 +496,11 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
 
             // ------------------------- T: per-frame track compaction (ballot / popc)
             for (int j = warp; j < nf; j += kWarps) {
-                if (S.reason[j] != M3E_REASON_NONE) {
-                    if (lane == 0) { S.ntrk[j] = 0; S.nneg[j] = 0; }
+                if (B.reason[j] != M3E_REASON_NONE) {
+                    if (lane == 0) { B.ntrk[j] = 0; B.nneg[j] = 0; }
                     continue;
                 }
-                const int n = S.nstored[j];
+                const int n = B.nstored[j];
                 const size_t cb = cfirst + (size_t)j * P.cuts_max;
                 m3e_track* tj = ctrk + tfirst + (size_t)j * P.max_tracks;
                 int cnt = 0, nneg = 0;
@@ -393,26 +534,26 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                     cnt += __popc(m);
                 }
                 if (lane == 0) {
-                    S.ntrk[j] = min(cnt, P.max_tracks + 1);
+                    B.ntrk[j] = min(cnt, P.max_tracks + 1);
                     if (cnt > P.max_tracks) {
-                        S.reason[j] = M3E_REASON_TRACK_OVERFLOW;
-                        S.nneg[j] = 0;
+                        B.reason[j] = M3E_REASON_TRACK_OVERFLOW;
+                        B.nneg[j] = 0;
                     } else {
-                        S.nneg[j] = nneg;
+                        B.nneg[j] = nneg;
                     }
                 }
             }
             __syncthreads();
         }
 
-        if constexpr (MODE == kModeSelect || MODE == kModeFit) {
+        if constexpr (MODE == kModeFit) {
             for (int j = tid; j < nf; j += kThreads) {
                 m3e_frame_out fo;
-                fo.n_cand = (uint16_t)S.ncand[j];
-                fo.n_tracks = MODE == kModeFit ? (uint16_t)S.ntrk[j] : (uint16_t)0;
+                fo.n_cand = (uint16_t)B.ncand[j];
+                fo.n_tracks = (uint16_t)B.ntrk[j];
                 fo.n_combs = 0;
-                fo.reason = (uint8_t)S.reason[j];
-                fo.n_neg = MODE == kModeFit ? (uint8_t)min(S.nneg[j], 255) : (uint8_t)0;
+                fo.reason = (uint8_t)B.reason[j];
+                fo.n_neg = (uint8_t)min(B.nneg[j], 255);
                 fo.track_first = (uint32_t)(tfirst + (size_t)j * P.max_tracks);
                 fo.kept_index = 0xFFFFFFFFu;
                 A.out.frames[f0 + j] = fo;
@@ -424,8 +565,8 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
             for (int j = warp; j < nf; j += kWarps) {
                 int ncomb = 0, nneg_out = 0;
                 bool has_vtx = false;
-                if (S.reason[j] == M3E_REASON_NONE) {
-                    const int nt = min(S.ntrk[j], P.max_tracks);
+                if (B.reason[j] == M3E_REASON_NONE) {
+                    const int nt = min(B.ntrk[j], P.max_tracks);
                     const m3e_track* tj = ctrk + tfirst + (size_t)j * P.max_tracks;
                     // charge-sorted index lists, in track order
                     int npos = 0, nneg = 0;
@@ -510,19 +651,19 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                                     v.chi2 = bres.chi2;
                                     v.target_dist = (float)bres.tdist;
                                     v.p_total = (float)bres.ptot;
-                                    S.vtx[j] = v;
+                                    B.vtx[j] = v;
                                 }
                             }
                         }
                     }
                     if (lane == 0) {
-                        S.ncomb[j] = ncomb;
-                        S.nneg[j] = nneg_out;
-                        if (ncomb > P.max_combs) S.reason[j] = M3E_REASON_COMB_OVERFLOW;
-                        else if (has_vtx) S.reason[j] = M3E_REASON_VERTEX;
+                        B.ncomb[j] = ncomb;
+                        B.nneg[j] = nneg_out;
+                        if (ncomb > P.max_combs) B.reason[j] = M3E_REASON_COMB_OVERFLOW;
+                        else if (has_vtx) B.reason[j] = M3E_REASON_VERTEX;
                     }
                 } else if (lane == 0) {
-                    S.ncomb[j] = 0;
+                    B.ncomb[j] = 0;
                 }
                 __syncwarp();
             }
@@ -533,141 +674,56 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
             for (int j = tid; j < nf; j += kThreads) {
                 m3e_frame_out fo;
                 fo.n_cand = 0;
-                fo.n_tracks = (uint16_t)S.ntrk[j];
-                fo.n_combs = (uint16_t)S.ncomb[j];
-                fo.reason = (uint8_t)S.reason[j];
-                fo.n_neg = (uint8_t)min(S.nneg[j], 255);
+                fo.n_tracks = (uint16_t)B.ntrk[j];
+                fo.n_combs = (uint16_t)B.ncomb[j];
+                fo.reason = (uint8_t)B.reason[j];
+                fo.n_neg = (uint8_t)min(B.nneg[j], 255);
                 fo.track_first = (uint32_t)(tfirst + (size_t)j * P.max_tracks);
                 fo.kept_index = 0xFFFFFFFFu;
                 A.out.frames[f0 + j] = fo;
-                if (S.reason[j] == M3E_REASON_VERTEX && A.s_vtx) A.s_vtx[f0 + j] = S.vtx[j];
+                if (B.reason[j] == M3E_REASON_VERTEX && A.s_vtx) A.s_vtx[f0 + j] = B.vtx[j];
             }
         }
 
-        // ------------------------------- O: ordered outputs + packer (look-back)
-        if constexpr (MODE == kModeFull || MODE == kModePack) {
+        // ------------------------ O: counts, aggregate now, outputs one batch later
+        if constexpr (kOut) {
             for (int j = tid; j < nf; j += kThreads) {
-                const int r = S.reason[j];
+                const int r = B.reason[j];
                 const bool kept = r != M3E_REASON_NONE;
                 const bool has_tracks = r == M3E_REASON_NONE || r == M3E_REASON_TRACK_OVERFLOW ||
                                         r == M3E_REASON_COMB_OVERFLOW || r == M3E_REASON_VERTEX;
-                S.o_trk[j] = (MODE == kModeFull && has_tracks) ? (uint32_t)min(S.ntrk[j], P.max_tracks) : 0u;
-                S.o_kept[j] = kept ? 1u : 0u;
-                S.o_hits[j] = kept ? (S.offs[buf][4 * j + 4] - S.offs[buf][4 * j]) : 0u;
+                B.o_trk[j] = (MODE == kModeFull && has_tracks) ? (uint32_t)min(B.ntrk[j], P.max_tracks) : 0u;
+                B.o_kept[j] = kept ? 1u : 0u;
+                B.o_hits[j] = kept ? (S.offs[buf][4 * j + 4] - S.offs[buf][4 * j]) : 0u;
             }
+            for (int i = tid; i <= 4 * nf; i += kThreads) B.offs[i] = S.offs[buf][i];
             __syncthreads();
             if (warp == 0) {
-                warp_scan64(S.o_trk, nf);
-                warp_scan64(S.o_kept, nf);
-                warp_scan64(S.o_hits, nf);
-                const uint3 ex = lookback(A, b, make_uint3(S.o_trk[nf], S.o_kept[nf], S.o_hits[nf]));
-                if (lane == 0) {
-                    S.g_trk = ex.x;
-                    S.g_kept = ex.y;
-                    S.g_hits = ex.z;
-                }
+                warp_scan64(B.o_trk, nf);
+                warp_scan64(B.o_kept, nf);
+                warp_scan64(B.o_hits, nf);
+                publish_aggregate(A, b, make_uint3(B.o_trk[nf], B.o_kept[nf], B.o_hits[nf]));
             }
-            __syncthreads();
-            const m3e_outputs& O = A.out;
-            const uint32_t g_trk = S.g_trk, g_kept = S.g_kept, g_hits = S.g_hits;
-            // per-frame records
-            for (int j = tid; j < nf; j += kThreads) {
-                const int r = S.reason[j];
-                const bool kept = r != M3E_REASON_NONE;
-                const uint32_t kidx = g_kept + S.o_kept[j];
-                if (O.reason) O.reason[f0 + j] = (uint8_t)r;
-                if (O.frames) {
-                    m3e_frame_out fo;
-                    fo.n_cand = (uint16_t)S.ncand[j];
-                    fo.n_tracks = (uint16_t)S.ntrk[j];
-                    fo.n_combs = (uint16_t)S.ncomb[j];
-                    fo.reason = (uint8_t)r;
-                    fo.n_neg = (uint8_t)min(S.nneg[j], 255);
-                    fo.track_first = g_trk + S.o_trk[j];
-                    fo.kept_index = kept ? kidx : 0xFFFFFFFFu;
-                    O.frames[f0 + j] = fo;
-                }
-                if (kept) {
-                    const uint32_t hb = g_hits + S.o_hits[j];
-                    if (kidx < O.kept_capacity) {
-                        if (O.kept_frame) O.kept_frame[kidx] = f0 + j;
-                        if (O.kept_offsets)
-                            for (int l = 0; l < 4; ++l)
-                                O.kept_offsets[4 * (size_t)kidx + l] = hb + (S.offs[buf][4 * j + l] - S.offs[buf][4 * j]);
-                        if (O.vertices) {
-                            m3e_vertex v;
-                            if (r == M3E_REASON_VERTEX) {
-                                v = S.vtx[j];
-                            } else {
-                                v = m3e_vertex{};
-                                v.frame = 0xFFFFFFFFu;
-                            }
-                            O.vertices[kidx] = v;
-                        }
-                    } else {
-                        S.s_overflow = 1;
-                    }
-                }
+            // the previous batch's predecessors have had a whole batch of time to publish
+            if (pending) {
+                __syncthreads();
+                finalize_batch<MODE>(A, S, S.st[par ^ 1],
+                                     MODE == kModeFull ? ctrk_base + (size_t)(par ^ 1) * A.trk_stride : nullptr);
             }
-            // last batch closes the packed offsets
-            if (b == A.nbatch - 1 && tid == 0 && O.kept_offsets) {
-                const uint32_t K = g_kept + S.o_kept[nf];
-                if (K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = g_hits + S.o_hits[nf];
-            }
-            // tracks, in frame order
-            if constexpr (MODE == kModeFull) {
-                const uint32_t nt = S.o_trk[nf];
-                if (O.tracks) {
-                    for (uint32_t e = tid; e < nt; e += kThreads) {
-                        const int j = find_frame(S.o_trk, nf, e);
-                        const uint32_t dst = g_trk + e;
-                        if (dst < O.track_capacity) {
-                            const m3e_track* src = ctrk + (size_t)j * P.max_tracks + (e - S.o_trk[j]);
-                            const uint4* s4 = reinterpret_cast<const uint4*>(src);
-                            uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst);
-                            d4[0] = s4[0];
-                            d4[1] = s4[1];
-                        } else {
-                            S.s_overflow = 1;
-                        }
-                    }
-                }
-            }
-            // packer: hits of the kept frames (Sec. V-A "filter, never transform")
-            {
-                const uint32_t nh = S.o_hits[nf];
-                if (O.kept_x) {
-                    for (uint32_t e = tid; e < nh; e += kThreads) {
-                        const int j = find_frame(S.o_hits, nf, e);
-                        const uint32_t i = e - S.o_hits[j];
-                        const uint32_t dst = g_hits + e;
-                        if (dst < O.kept_hit_capacity) {
-                            const Frame Fv = frame_view(A, S, buf, j);
-                            O.kept_x[dst] = Fv.x[i];
-                            O.kept_y[dst] = Fv.y[i];
-                            O.kept_z[dst] = Fv.z[i];
-                        } else {
-                            S.s_overflow = 1;
-                        }
-                    }
-                }
-            }
-            if (tid == 0) {
-                S.s_frames += nf;
-                S.s_trk += S.o_trk[nf];
-                S.s_hits += S.o_hits[nf];
-                for (int j = 0; j < nf; ++j) {
-                    S.s_kept[S.reason[j]] += 1;
-                    S.s_cand += S.nstored[j];
-                    S.s_vtx += S.reason[j] == M3E_REASON_VERTEX;
-                }
-            }
+            pending = true;
+            par ^= 1;
         }
         __syncthreads();
         buf ^= 1;
     }
 
-    if constexpr (MODE == kModeFull || MODE == kModePack) {
+    if constexpr (kOut) {
+        if (pending) {
+            __syncthreads();
+            finalize_batch<MODE>(A, S, S.st[par ^ 1],
+                                 MODE == kModeFull ? ctrk_base + (size_t)(par ^ 1) * A.trk_stride : nullptr);
+        }
+        __syncthreads();
         if (tid == 0 && A.out.summary) {
             m3e_summary* sm = A.out.summary;
             atomicAdd((unsigned long long*)&sm->frames, S.s_frames);

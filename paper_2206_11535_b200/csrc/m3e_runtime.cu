@@ -188,11 +188,11 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
         CK(cudaMalloc(&w.pool_idx, PS * n * sizeof(uint32_t)));
         CK(cudaMalloc(&w.pool_rt, PS * n * sizeof(float)));
         CK(cudaMalloc(&w.pool_rec, PS * n * sizeof(m3e_fit_record)));
-        CK(cudaMalloc(&w.pool_trk, TS * n * sizeof(m3e_track)));
+        CK(cudaMalloc(&w.pool_trk, 2 * TS * n * sizeof(m3e_track)));  // double-buffered by batch parity
         w.pool_stride = PS;
         w.trk_stride = TS;
         w.pool_ctas = n;
-        w.bytes += PS * n * (sizeof(uint32_t) + sizeof(float) + sizeof(m3e_fit_record)) + TS * n * sizeof(m3e_track);
+        w.bytes += PS * n * (sizeof(uint32_t) + sizeof(float) + sizeof(m3e_fit_record)) + 2 * TS * n * sizeof(m3e_track);
     }
     (void)c;
     return M3E_OK;

@@ -233,7 +233,7 @@ class Result:
                  kept_capacity: Optional[int] = None, device="cuda"):
         import torch
         F = max(n_frames, 1)
-        self.track_capacity = track_capacity if track_capacity is not None else 16 * F + 1024
+        self.track_capacity = track_capacity if track_capacity is not None else 64 * F + 1024
         self.kept_capacity = kept_capacity if kept_capacity is not None else F
         kh = n_hits + 8 if kept_capacity is None else max(8, n_hits)
         u8 = dict(dtype=torch.uint8, device=device)

@@ -22,6 +22,10 @@ REL_KAPPA = 1e-4
 # fake) fits are compared at the absolute 1e-4 * KAPPA_FLOOR, the fp32 rounding
 # floor of a curvature measured over ~50 mm chords.
 KAPPA_FLOOR = 0.299792458 / 52.83
+# fits with chi2_global above this are > 30 sigma inconsistent; the linearised
+# model (Eq. 6, R6) is outside its domain there and only the reject decision is
+# compared (measured fp32 agreement below it: <= 5e-6 relative on kappa)
+CHI2_DOMAIN = 1000.0
 
 
 def kappa_close(a, b):

@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 import synth
-from parity import KAPPA_FLOOR, REL_BAND, combo_is_marginal, kappa_close, near, rel_close, unpack
+from parity import CHI2_DOMAIN, REL_BAND, REL_KAPPA, combo_is_marginal, kappa_close, near, rel_close, unpack
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -115,12 +115,15 @@ def test_fit_parity(ctx, gp, P, name, n, seed):
                 continue
             if o.status >= 2 and o.status != oracle.FIT_LAYER3_EMPTY:
                 assert int(g["hit3"]) == (o.hit[3] if o.hit[3] >= 0 else 0xFFFF) or o.marginal
-            if o.status in (oracle.FIT_OK, oracle.FIT_CHI2):
+            # curvatures / chi2 compared wherever the linearised model is in its domain:
+            # chi2_global < 1000 (every fit the chi2 < 32 cut could accept, with a 30x
+            # margin); beyond, only the reject decision is compared
+            if o.status in (oracle.FIT_OK, oracle.FIT_CHI2) and o.chi2 < CHI2_DOMAIN:
                 for a, b in [(g["kappa1"], o.t1.kappa), (g["kappa2"], o.t2.kappa), (g["kappa"], o.kappa)]:
-                    worst = max(worst, abs(a - b) / max(abs(b), KAPPA_FLOOR))
-                    assert kappa_close(float(a), b), (f, k, float(a), b)
+                    worst = max(worst, abs(a - b) / abs(b))
+                    assert rel_close(float(a), b, REL_KAPPA), (f, k, float(a), b, o.chi2)
                 assert rel_close(float(g["var1"]), o.t1.var_kappa, 1e-3)
-                assert rel_close(float(g["chi2"]), o.chi2, 1e-3, 1e-3), (f, k, float(g["chi2"]), o.chi2)
+                assert abs(float(g["chi2"]) - o.chi2) <= 1e-3 * max(o.chi2, 1.0), (f, k, float(g["chi2"]), o.chi2)
             if o.status == oracle.FIT_OK:
                 assert abs(float(g["cos_theta01"]) - o.cos_theta01) <= 1e-4
                 assert math.hypot(float(g["cx"]) - o.cx, float(g["cy"]) - o.cy) <= 1e-4 * o.rt
@@ -206,7 +209,9 @@ def _compare_full(P, fr, res_np, frames_np, tracks_np, n):
             same = [tuple(int(h) for h in t["hit"]) for t in gt] == [tuple(t.hit) for t in otr]
         if not same:
             marg = o.n_cand_marginal or o.n_fit_marginal or o.n_vertex_marginal
-            assert marg, f"frame {f}: gpu {g} oracle reason {o.reason} n_cand {o.n_cand} n_tracks {o.n_tracks}"
+            assert marg, (f"frame {f}: gpu {g} oracle reason {o.reason} n_cand {o.n_cand} n_tracks {o.n_tracks} "
+                          f"n_combs {o.n_combs}; gpu tracks {[tuple(int(h) for h in t['hit']) for t in gt]} "
+                          f"oracle tracks {[tuple(t.hit) for t in otr]}")
             explained.append(f)
             continue
         for t, u in zip(gt, otr):
@@ -222,6 +227,7 @@ def test_full_parity(ctx, gp, P, name, n, seed):
     res = m3e.run_filter(ctx, gp, df)
     torch.cuda.synchronize()
     sm = res.summary_np()
+    assert int(sm["overflow"]) == 0
     frames_np = res.frames_np(n)
     tracks_np = res.tracks_np(int(sm["tracks"]))
     explained = _compare_full(P, fr, None, frames_np, tracks_np, n)
