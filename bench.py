@@ -213,14 +213,15 @@ def main():
     kept = int(sum(sm["kept_by_reason"][1:]))
     assert int(sm["frames"]) == F and not int(sm["overflow"]), "output capacity exceeded"
     out_bytes = (F * (1 + 16) + int(sm["tracks"]) * 32 + kept * (56 + 4 + 16) + int(sm["kept_hits"]) * 12)
-    counters = torch.tensor([F, H, kept, int(sm["tracks"]), int(sm["kept_hits"]), ms_step * 1e3] +
+    from paper_2206_11535_b200 import dist as m3dist
+    counters = torch.tensor([F, H, kept, int(sm["tracks"]), int(sm["kept_hits"]), 0.0] +
                             [int(v) for v in sm["kept_by_reason"]], dtype=torch.float64, device=dev)
-    if world > 1:
-        # the only collective: counters (sum) and the slowest rank's step time (max)
-        t_max = counters[5].clone()
-        dist.all_reduce(counters, op=dist.ReduceOp.SUM)
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        counters[5] = t_max
+    # the only collectives (after the timed region): counters (sum), slowest rank's
+    # step time (max), accepted global frame ids (gather)
+    counters, t_max = m3dist.reduce_counters(counters, ms_step / 1e3)
+    counters[5] = t_max * 1e6
+    kept_ids = m3dist.gather_kept(res.kept_frame[:kept], rank * F)
+    assert kept_ids.numel() == int(counters[2])
     tot_frames, tot_hits, tot_kept = float(counters[0]), float(counters[1]), float(counters[2])
     ms_max = float(counters[5]) / 1e3
     fps = tot_frames / (ms_max / 1e3)

@@ -12,6 +12,12 @@
 // fp32 fit math is also compiled for the host (tools/fit_numerics.cu) to study
 // its rounding against the oracle without a GPU
 #define M3E_HD __host__ __device__ __forceinline__
+// called at two sites: one out-of-line copy keeps the fit's code small
+#ifdef __CUDA_ARCH__
+#define M3E_HD_CALL __host__ __device__ __noinline__
+#else
+#define M3E_HD_CALL __host__ __device__ inline
+#endif
 
 namespace m3e {
 
@@ -22,6 +28,28 @@ constexpr double kMuMass = 105.6583755;   // MeV (PDG), m_mu c^2 of Eq. 1
 constexpr double kEMass = 0.51099895;     // MeV (PDG)
 constexpr double kPtConv = 0.299792458;   // MeV/c per (T mm)
 constexpr int kMaxLayerHits = 1024;       // 10-bit candidate index fields
+
+// Compact fp32 primitives for the fit (code size matters: every warp of an SM
+// can be in a different stage, so the hot code must stay in the I-cache).
+// rcp: one MUFU.RCP (rcp.approx.ftz, <= 1 ulp): the fit is compared at 1e-4.
+M3E_HD float rcp(float x) {
+#ifdef __CUDA_ARCH__
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+#else
+    return 1.0f / x;
+#endif
+}
+// sin / cos of 0 <= x <= pi/2 by Taylor polynomials of degree 11 / 12
+// (truncation < 6e-8 absolute on the interval; no range reduction needed).
+M3E_HD void sincos_half(float x, float& s, float& c) {
+    const float x2 = x * x;
+    s = x * (1.0f + x2 * (-1.6666667e-1f + x2 * (8.3333333e-3f + x2 * (-1.9841270e-4f +
+                                                                           x2 * (2.7557319e-6f + x2 * -2.5052108e-8f)))));
+    c = 1.0f + x2 * (-0.5f + x2 * (4.1666667e-2f + x2 * (-1.3888889e-3f + x2 * (2.4801587e-5f +
+                                                                              x2 * (-2.7557319e-7f + x2 * 2.0876757e-9f)))));
+}
 
 // Kernel-side parameters, derived once on the host from m3e_params.
 struct DevParams {
@@ -61,35 +89,41 @@ M3E_HD float circle_radius(float3 h0, float3 h1, float3 h2) {
     if (cz == 0.0f) return kInfF;
     float cx = h2.x - h0.x, cy = h2.y - h0.y;
     float d01 = sqrtf(ax * ax + ay * ay), d12 = sqrtf(bx * bx + by * by), d20 = sqrtf(cx * cx + cy * cy);
-    return d01 * d12 * d20 / (2.0f * cz);
+    return d01 * d12 * d20 * rcp(2.0f * cz);
 }
 
 // ------------------------------------------------------- Selection Cuts ----
-// Tests of Alg. 2 in order: Delta-lambda (Eq. 2-3), Phi_01, Phi_12 (Eq. 4), r_tc
-// (Eq. 5).  Returns true if the combination survives; rt = Eq. 5 radius.
-__device__ __forceinline__ bool pass_cuts(const DevParams& P, const Frame& F, int i0, int i1, int i2,
-                                          float& rt) {
-    const int g0 = F.s[0] + i0, g1 = F.s[1] + i1, g2 = F.s[2] + i2;
-    const float z0 = F.z[g0], z1 = F.z[g1], z2 = F.z[g2];
+// Alg. 2 tests: Delta-lambda (Eq. 2-3) first, then Phi_01, Phi_12 (Eq. 4) and
+// r_tc (Eq. 5).  The survivor set is the AND of the four tests, so evaluating
+// them in two passes (below) does not change it.
+__device__ __forceinline__ bool pass_dlambda(const DevParams& P, const Frame& F, int i0, int i1, int i2) {
+    const float z0 = F.z[F.s[0] + i0], z1 = F.z[F.s[1] + i1], z2 = F.z[F.s[2] + i2];
     const float dl = (z2 - z1) * P.inv_dr12 - (z1 - z0) * P.inv_dr01;
-    if (!(fabsf(dl) <= P.dl_max)) return false;
+    return fabsf(dl) <= P.dl_max;
+}
+__device__ __forceinline__ bool pass_rest(const DevParams& P, const Frame& F, int i0, int i1, int i2, float& rt) {
+    const int g0 = F.s[0] + i0, g1 = F.s[1] + i1, g2 = F.s[2] + i2;
     const float x0 = F.x[g0], y0 = F.y[g0], x1 = F.x[g1], y1 = F.y[g1];
     if (!((x0 * x1 + y0 * y1) * P.inv_r0r1 >= P.c01_min)) return false;
     const float x2 = F.x[g2], y2 = F.y[g2];
     if (!((x1 * x2 + y1 * y2) * P.inv_r1r2 >= P.c12_min)) return false;
-    rt = circle_radius(make_float3(x0, y0, z0), make_float3(x1, y1, z1), make_float3(x2, y2, z2));
+    rt = circle_radius(make_float3(x0, y0, 0.0f), make_float3(x1, y1, 0.0f), make_float3(x2, y2, 0.0f));
     const float ar = fabsf(rt);
     return ar >= P.rt_min && ar <= P.rt_max;
 }
 
 // Warp-cooperative enumeration of all n0 n1 n2 combinations of one frame in the
 // row-major order of Alg. 2 (i0 outer, i2 inner), 32 consecutive combinations per
-// step; survivors are compacted with a ballot + popc prefix so that stored
-// candidates keep the enumeration order.  Stops once more than cuts_max survive
-// (the frame then overflows, R3).  emit(pos, packed, rt) is called for pos <
-// cuts_max.  Returns min(#survivors, cuts_max + 1) (warp-uniform).
+// step.  Two-level compaction: the Delta-lambda survivors (~7 % of combinations,
+// the cut that removes > 80 %, Fig. 4) are appended with ballot + popc to a
+// per-warp FIFO `q` (64 entries, shared memory); each full 32 of them is tested
+// for Phi_01, Phi_12, r_tc on all 32 lanes (no divergent tail) and the final
+// survivors are compacted again with ballot + popc, so stored candidates keep
+// the enumeration order.  Stops once more than cuts_max survive (R3).
+// emit(pos, packed, rt) is called for pos < cuts_max.  Returns min(#survivors,
+// cuts_max + 1) (warp-uniform).
 template <class Emit>
-__device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame& F, Emit emit) {
+__device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame& F, uint32_t* q, Emit emit) {
     const int lane = threadIdx.x & 31;
     const int n0 = F.n[0], n1 = F.n[1], n2 = F.n[2];
     const long long total = (long long)n0 * n1 * n2;
@@ -100,18 +134,36 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
     int i0 = lane / n12, rem = lane - i0 * n12;
     int i1 = rem / n2, i2 = rem - i1 * n2;
     const int a = 32 / n12, r32 = 32 - a * n12, b = r32 / n2, c = r32 - b * n2;
-    int count = 0;
-    for (long long base = 0; base < total; base += 32) {
-        const bool valid = i0 < n0;
+    int count = 0, qn = 0;
+    // test q[0..n) (n <= 32) for the remaining cuts; true once the frame overflows
+    auto drain = [&](int n) -> bool {
         float rt = 0.0f;
-        const bool pass = valid && pass_cuts(P, F, i0, i1, i2, rt);
-        const unsigned m = __ballot_sync(0xffffffffu, pass);
-        if (pass) {
-            const int pos = count + __popc(m & lt_mask);
-            if (pos < P.cuts_max) emit(pos, (uint32_t)i0 | ((uint32_t)i1 << 10) | ((uint32_t)i2 << 20), rt);
+        uint32_t pk = 0;
+        bool pass = false;
+        if (lane < n) {
+            pk = q[lane];
+            pass = pass_rest(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
         }
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        const int pos = count + __popc(m & lt_mask);
+        if (pass && pos < P.cuts_max) emit(pos, pk, rt);
         count += __popc(m);
-        if (count > P.cuts_max) return P.cuts_max + 1;
+        return count > P.cuts_max;
+    };
+    for (long long base = 0; base < total; base += 32) {
+        const bool pass = i0 < n0 && pass_dlambda(P, F, i0, i1, i2);
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (pass) q[qn + __popc(m & lt_mask)] = (uint32_t)i0 | ((uint32_t)i1 << 10) | ((uint32_t)i2 << 20);
+        qn += __popc(m);
+        if (qn >= 32) {
+            __syncwarp();
+            if (drain(32)) return P.cuts_max + 1;
+            const uint32_t v = lane < qn - 32 ? q[32 + lane] : 0u;
+            __syncwarp();
+            if (lane < qn - 32) q[lane] = v;
+            qn -= 32;
+            __syncwarp();
+        }
         // advance (i0, i1, i2) by 32 in radix (n0, n1, n2)
         i2 += c;
         if (i2 >= n2) { i2 -= n2; ++i1; }
@@ -119,6 +171,8 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
         if (i1 >= n1) { i1 -= n1; ++i0; }
         i0 += a;
     }
+    __syncwarp();
+    if (qn > 0 && drain(qn)) return P.cuts_max + 1;
     return count;
 }
 
@@ -139,28 +193,31 @@ struct Triplet {
     float phc[2], kc[2], dphi[2];
 };
 
-M3E_HD bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2, float rtc,
+M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2, float rtc,
                                             Triplet& T) {
     if (!(fabsf(rtc) < kInfF)) return false;
     T.q = rtc > 0.0f ? 1 : -1;
     const float r = fabsf(rtc);
+    const float ir = rcp(r);
     float th[2], sth0 = 0.0f, dth[2];
     const float3 H[3] = {h0, h1, h2};
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
         const float dx = H[a + 1].x - H[a].x, dy = H[a + 1].y - H[a].y, z = H[a + 1].z - H[a].z;
         const float d = sqrtf(dx * dx + dy * dy);
-        float s = d / (2.0f * r);
+        float s = d * (0.5f * ir);
         s = fminf(s, 1.0f);
         const float phc = 2.0f * asinf(s);
         const float den = sqrtf(r * r * phc * phc + z * z);
-        const float kc = phc / den;
-        const float cth = z / den, sth = r * phc / den;
+        const float iden = rcp(den);
+        const float kc = phc * iden;
+        const float cth = z * iden, sth = r * phc * iden;
         const float ch = sqrtf(fmaxf(0.0f, 1.0f - s * s));     // cos(Phi_C / 2)
         // dPhi/dk = (2/k^3) / (d^2 cos(Phi/2) / (4 sin^3(Phi/2)) + 2 z^2/Phi^3), sin(Phi_C/2) = d/(2r)
-        const float dphi = (2.0f / (kc * kc * kc)) / (r * r * ch / s + 2.0f * z * z / (phc * phc * phc));
+        const float iphc = rcp(phc), ikc = rcp(kc);
+        const float dphi = 2.0f * ikc * ikc * ikc * rcp(r * r * ch * rcp(s) + 2.0f * z * z * iphc * iphc * iphc);
         // dtheta/dk = -z (Phi - k Phi') / (Phi^2 sin theta)
-        dth[a] = -z * (phc - kc * dphi) / (phc * phc * sth);
+        dth[a] = -z * (phc - kc * dphi) * iphc * iphc * rcp(sth);
         th[a] = atan2f(sth, cth);
         if (a == 0) sth0 = sth;
         T.phc[a] = phc;
@@ -174,13 +231,13 @@ M3E_HD bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2, flo
     T.b_th = dth[1] - dth[0];
     T.al_th = (th[1] - th[0]) - 0.5f * dk * (dth[1] + dth[0]);
     const float sig = P.chl * T.kref;
-    T.w_th = 1.0f / (sig * sig);
+    T.w_th = rcp(sig * sig);
     T.w_phi = sth0 * sth0 * T.w_th;
     const float A = T.b_phi * T.b_phi * T.w_phi + T.b_th * T.b_th * T.w_th;
     if (!(A > 0.0f)) return false;
     const float B = T.al_phi * T.b_phi * T.w_phi + T.al_th * T.b_th * T.w_th;
-    T.khat = T.kref - B / A;
-    T.var = 1.0f / A;
+    T.var = rcp(A);
+    T.khat = T.kref - B * T.var;
     return true;
 }
 
@@ -194,18 +251,22 @@ M3E_HD float triplet_chi2(const Triplet& T, float kappa) {
 // exact short-arc bending angle: root of d^2/(4 sin^2(Phi/2)) + z^2/Phi^2 = 1/k^2
 // on (0, pi] by Newton from `start` (the linearised value).  false if no short arc
 // of curvature k joins the hits (1/k^2 < d^2/4 + z^2/pi^2).
-M3E_HD bool arc_phi(float d, float z, float k, float start, float& phi) {
+M3E_HD_CALL bool arc_phi(float d, float z, float k, float start, float& phi) {
     if (!(k > 0.0f)) return false;
-    const float R2 = 1.0f / (k * k);
-    if (R2 < 0.25f * d * d + z * z * (1.0f / (kPiF * kPiF))) return false;
+    const float ik = rcp(k);
+    const float R2 = ik * ik;
+    const float d2 = 0.25f * d * d, z2 = z * z;
+    if (R2 < d2 + z2 * (1.0f / (kPiF * kPiF))) return false;
     float p = fminf(fmaxf(start, 1e-6f), kPiF);
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-        float s, c;
-        sincosf(0.5f * p, &s, &c);
-        const float f = d * d / (4.0f * s * s) + z * z / (p * p) - R2;
-        const float fp = -d * d * c / (4.0f * s * s * s) - 2.0f * z * z / (p * p * p);
-        p = fminf(fmaxf(p - f / fp, 1e-7f), kPiF);
+#pragma unroll 1
+    for (int it = 0; it < 3; ++it) {   // quadratic convergence from the linearised start
+        float sh, ch;
+        sincos_half(0.5f * p, sh, ch);
+        const float is = rcp(sh), ip = rcp(p);
+        const float is2 = is * is, ip2 = ip * ip;
+        const float f = d2 * is2 + z2 * ip2 - R2;
+        const float fp = -d2 * ch * is2 * is - 2.0f * z2 * ip2 * ip;
+        p = fminf(fmaxf(p - f * rcp(fp), 1e-7f), kPiF);
     }
     phi = p;
     return true;
@@ -221,30 +282,31 @@ M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet&
     const float d = sqrtf(dx * dx + dy * dy);
     float phi;
     if (!arc_phi(d, z, k, T.phc[1] + T.dphi[1] * (k - T.kc[1]), phi)) return false;
-    const float cth = fminf(fmaxf(z * k / phi, -1.0f), 1.0f);
+    const float ik = rcp(k);
+    const float cth = fminf(fmaxf(z * k * rcp(phi), -1.0f), 1.0f);
     const float sth = sqrtf(1.0f - cth * cth);
     const float psi = atan2f(dy, dx) - T.q * 0.5f * phi;     // heading at h2
-    const float rt = sth / k;
+    const float rt = sth * ik;
     float sp, cp;
     sincosf(psi, &sp, &cp);
     const float cx = h2.x + T.q * rt * sp, cy = h2.y - T.q * rt * cp;
     const float C = sqrtf(cx * cx + cy * cy);
     if (C == 0.0f) return false;
-    const float arg = (P.R3sq - C * C - rt * rt) / (2.0f * rt * C);
+    const float arg = (P.R3sq - C * C - rt * rt) * rcp(2.0f * rt * C);
     if (arg > 1.0f || arg < -1.0f) return false;
     const float phic = atan2f(cy, cx), da = acosf(arg);
     const float phi0 = atan2f(h2.y - cy, h2.x - cx);
     float best = 1e30f;
 #pragma unroll
     for (int s = -1; s <= 1; s += 2) {
-        float t = fmodf(T.q * (phi0 - (phic + s * da)), 2.0f * kPiF);
-        if (t < 0.0f) t += 2.0f * kPiF;
+        float t = T.q * (phi0 - (phic + s * da));
+        t -= 2.0f * kPiF * floorf(t * (0.5f / kPiF));   // to [0, 2 pi)
         if (t > 0.0f && t < best) best = t;
     }
     const float ph = phi0 - T.q * best;
     float s2, c2;
     sincosf(ph, &s2, &c2);
-    out = make_float3(cx + rt * c2, cy + rt * s2, h2.z + cth / k * best);
+    out = make_float3(cx + rt * c2, cy + rt * s2, h2.z + cth * ik * best);
     return true;
 }
 
@@ -283,8 +345,8 @@ M3E_HD FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, 
     o.kappa2 = T2.q * T2.khat;
     o.var2 = T2.var;
     // Eq. 8 weighted mean, Eq. 7 global chi2
-    const float w1 = 1.0f / T1.var, w2 = 1.0f / T2.var;
-    const float kb = (o.kappa1 * w1 + o.kappa2 * w2) / (w1 + w2);
+    const float w1 = rcp(T1.var), w2 = rcp(T2.var);
+    const float kb = (o.kappa1 * w1 + o.kappa2 * w2) * rcp(w1 + w2);
     o.kappa = kb;
     o.chi2 = triplet_chi2(T1, kb) + triplet_chi2(T2, kb);
     if (!(o.chi2 < P.chi2_max)) { o.status = 5; return o; }
@@ -295,10 +357,11 @@ M3E_HD FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, 
     const float d01 = sqrtf(dx * dx + dy * dy);
     float phi01;
     if (!arc_phi(d01, z01, k, T1.phc[0] + T1.dphi[0] * (k - T1.kc[0]), phi01)) { o.status = 6; return o; }
-    const float cth = fminf(fmaxf(z01 * k / phi01, -1.0f), 1.0f);
-    const float rt = sqrtf(1.0f - cth * cth) / k;
+    const float cth = fminf(fmaxf(z01 * k * rcp(phi01), -1.0f), 1.0f);
+    const float rt = sqrtf(1.0f - cth * cth) * rcp(k);
     const float off = sqrtf(fmaxf(0.0f, rt * rt - 0.25f * d01 * d01));
-    const float ux = dx / d01, uy = dy / d01;
+    const float id01 = rcp(d01);
+    const float ux = dx * id01, uy = dy * id01;
     o.cth01 = cth;
     o.cx = 0.5f * (h0.x + h1.x) + q * off * uy;   // clockwise: centre right of the chord
     o.cy = 0.5f * (h0.y + h1.y) - q * off * ux;
@@ -331,21 +394,18 @@ __device__ __forceinline__ VTrk make_vtrk(const DevParams& P, const m3e_track& t
     return v;
 }
 
-__device__ __forceinline__ double wrap_pi(double a) {
-    while (a > kPi) a -= 2.0 * kPi;
-    while (a <= -kPi) a += 2.0 * kPi;
-    return a;
-}
-
 // signed turning angle from point (px,py) on the track circle to the layer-0 hit,
 // in the direction of motion, wrapped to (-pi, pi] (R12)
-__device__ __forceinline__ double turn_to_h0(const VTrk& t, double px, double py) {
-    return wrap_pi(t.q * (atan2(py - t.cy, px - t.cx) - atan2(t.h0y - t.cy, t.h0x - t.cx)));
+// (one atan2 of the cross and dot products of the two radii; out of line to keep
+// the code small)
+static __device__ __noinline__ double turn_to_h0(const VTrk& t, double px, double py) {
+    const double ax = t.h0x - t.cx, ay = t.h0y - t.cy, bx = px - t.cx, by = py - t.cy;
+    return t.q * atan2(ax * by - ay * bx, ax * bx + ay * by);
 }
 
 // circle-circle intersections; 0 or 2 points {x0,y0,x1,y1}
 __device__ __forceinline__ int intersect(const VTrk& A, const VTrk& B, double o[4]) {
-    const double dx = B.cx - A.cx, dy = B.cy - A.cy, D = hypot(dx, dy);
+    const double dx = B.cx - A.cx, dy = B.cy - A.cy, D = sqrt(dx * dx + dy * dy);
     if (D == 0.0 || D > A.rt + B.rt || D < fabs(A.rt - B.rt)) return 0;
     const double a = (A.rt * A.rt - B.rt * B.rt + D * D) / (2.0 * D);
     const double h = sqrt(fmax(0.0, A.rt * A.rt - a * a));
@@ -359,12 +419,13 @@ __device__ __forceinline__ double seg_dist(double px, double py, double ax, doub
     const double vx = bx - ax, vy = by - ay;
     double t = ((px - ax) * vx + (py - ay) * vy) / (vx * vx + vy * vy);
     t = fmin(fmax(t, 0.0), 1.0);
-    return hypot(px - ax - t * vx, py - ay - t * vy);
+    const double ex = px - ax - t * vx, ey = py - ay - t * vy;
+    return sqrt(ex * ex + ey * ey);
 }
 
 // distance to the double hollow-cone target surface (R14)
 __device__ __forceinline__ double target_distance(const DevParams& P, double x, double y, double z) {
-    const double rho = hypot(x, y), R = P.target_r, L = P.target_half;
+    const double rho = sqrt(x * x + y * y), R = P.target_r, L = P.target_half;
     return fmin(seg_dist(rho, z, 0.0, -L, R, 0.0), seg_dist(rho, z, R, 0.0, 0.0, L));
 }
 
@@ -388,7 +449,7 @@ static __device__ __noinline__ VResult vertex_triple(const DevParams* __restrict
         if (intersect(T[pr[pi][0]], T[pr[pi][1]], o) == 0) return best;   // "the track triplet is skipped"
         npt[pi] = 0;
         for (int s = 0; s < 2; ++s) {
-            if (hypot(o[2 * s], o[2 * s + 1]) <= P.rlim) {
+            if (sqrt(o[2 * s] * o[2 * s] + o[2 * s + 1] * o[2 * s + 1]) <= P.rlim) {
                 pts[pi][npt[pi]][0] = o[2 * s];
                 pts[pi][npt[pi]][1] = o[2 * s + 1];
                 ++npt[pi];
@@ -415,7 +476,7 @@ static __device__ __noinline__ VResult vertex_triple(const DevParams* __restrict
                 bool bad = false;
                 for (int t = 0; t < 3; ++t) {                              // Fig. 6, Eq. 11
                     const VTrk& A = T[t];
-                    const double dx = mx - A.cx, dy = my - A.cy, dn = hypot(dx, dy);
+                    const double dx = mx - A.cx, dy = my - A.cy, dn = sqrt(dx * dx + dy * dy);
                     if (dn == 0.0) { bad = true; break; }
                     pcx[t] = A.cx + A.rt * dx / dn;
                     pcy[t] = A.cy + A.rt * dy / dn;
@@ -439,9 +500,10 @@ static __device__ __noinline__ VResult vertex_triple(const DevParams* __restrict
                     double px = 0.0, py = 0.0, pz = 0.0;
                     for (int t = 0; t < 3; ++t) {
                         const VTrk& A = T[t];
-                        const double ph = atan2(pcy[t] - A.cy, pcx[t] - A.cx);
-                        px += A.p * A.sth * A.q * sin(ph);
-                        py += A.p * A.sth * (-A.q * cos(ph));
+                        // direction of motion at the pca: q (sin ph, -cos ph), ph = angle of pca - c
+                        const double irt = 1.0 / A.rt;
+                        px += A.p * A.sth * A.q * (pcy[t] - A.cy) * irt;
+                        py += A.p * A.sth * (-A.q) * (pcx[t] - A.cx) * irt;
                         pz += A.p * A.cth;
                     }
                     best.ptot = sqrt(px * px + py * py + pz * pz);

@@ -1,24 +1,26 @@
 // m3e_kernels.cu -- the persistent filter kernel of the Mu3e online event selection.
 //
-// One CTA (256 threads, 8 warps) processes a batch of consecutive frames at a
-// time (Alg. 1 "Distribute frames over CUDA blocks", re-blocked for
-// B200: a batch instead of one frame, so the fit stage runs one lane per
-// candidate over the whole batch instead of one thread per candidate of one
-// frame).  Per batch:
-//   load   the batch's offsets and hits (SoA x/y/z) into shared memory with
-//          cp.async.bulk (TMA bulk copies) completing on an mbarrier,
-//          double-buffered: the next batch's copies are in flight while this
-//          batch computes;
-//   S      Selection Cuts, one warp per frame, ballot/popc compaction (Alg. 2);
-//   F      triplet fit + layer-3 extension, one lane per candidate (Alg. 3);
+// Every warp is an independent pipeline (no CTA-wide barriers): it claims a
+// warp-batch of consecutive frames with an atomic ticket (Alg. 1
+// "Distribute frames over CUDA blocks", re-blocked to warps so that uneven
+// frames never stall other warps at a barrier) and, per warp-batch:
+//   load   offsets + hits (SoA x/y/z) -> shared memory with cp.async.bulk (TMA
+//          bulk copies) on the warp's mbarrier, double-buffered: the next
+//          warp-batch is in flight while this one computes;
+//   S      Selection Cuts per frame (Alg. 2), two-level ballot/popc compaction;
+//   F      triplet fit + layer-3 extension (Alg. 3), one lane per candidate
+//          across all frames of the warp-batch;
 //   T      per-frame track compaction (ballot/popc), charge split;
-//   V      vertex selection in fp64, one warp per frame with e+e+e- (Alg. 4);
-//   O      decoupled look-back prefix over (tracks, kept frames, kept hits) so
-//          every output is written in frame order; the packer copies the kept
-//          frames' hits (Sec. V-A), tracks and vertices out.
-// Batches are handed out by an atomic ticket, so the look-back only ever waits
-// on batches held by running CTAs.  The same kernel with a compile-time MODE
-// runs one stage on fixed per-frame slots (stage-isolated parity tests).
+//   V      vertex selection in fp64 (Alg. 4) for frames with e+ e+ e-;
+//   O      per-frame records are written in place; the warp-batch's tracks and
+//          kept-frame records are staged at offsets reserved with one atomic
+//          per warp-batch, so no warp ever waits for another.
+// The pack kernel (second launch) then scans the per-warp-batch counts with a
+// decoupled look-back over tiles (all counts final, so it never waits on
+// compute) and scatters tracks, vertices and the kept frames' hits into frame
+// order (Sec. V-A: kept frames are stored).
+// The filter kernel with a compile-time MODE runs one stage on fixed per-frame
+// slots (stage-isolated parity tests).
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -81,53 +83,53 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
 }
 
 // ----------------------------------------------------------- shared state ----
-// per-frame results of one batch; two copies, because a batch's outputs are
-// written only after the CTA has computed its next batch (deferred look-back)
+// per-frame results of the warp-batch being processed
 struct BatchState {
     int nstored[kFB], ncand[kFB], ntrk[kFB], nneg[kFB], ncomb[kFB], reason[kFB];
     uint32_t o_trk[kFB + 1], o_kept[kFB + 1], o_hits[kFB + 1];   // exclusive prefixes (+ total)
-    uint32_t offs[4 * kFB + 4];                                // the batch's offsets (packer)
     m3e_vertex vtx[kFB];
-    uint32_t batch;
-    int nf;
 };
 
-struct Smem {
+struct __align__(16) WarpSmem {
     float hx[2][kHCap];
     float hy[2][kHCap];
     float hz[2][kHCap];
     uint32_t offs[2][4 * kFB + 4];
     uint64_t bar[2];
     uint32_t b_batch[2], b_winlo[2], b_winhi[2];
-    BatchState st[2];
-    uint32_t pref[kFB + 1];                                   // candidates: exclusive prefix
-    uint32_t g_trk, g_kept, g_hits;                            // finalized batch's global bases
-    uint8_t vlist[kWarps][2][kMaxTracksCap];
-    uint32_t vcomb[kWarps][kMaxCombsCap];
+    BatchState st;
+    uint32_t pref[kFB + 1];          // candidates: exclusive prefix
+    uint32_t q[64];                  // Delta-lambda survivors (selection FIFO)
+    uint8_t vlist[2][kMaxTracksCap];
+    uint32_t vcomb[kMaxCombsCap];
+};
+
+struct Smem {
+    WarpSmem w[kWarps];
+    DevParams P;   // copy for the out-of-line vertex routine (no address of a kernel parameter is taken)
     unsigned long long s_kept[6], s_cand, s_trk, s_hits, s_vtx, s_frames;
     int s_overflow;
-    DevParams P;   // copy for the out-of-line vertex routine (no address of a kernel parameter is taken)
 };
 
 size_t smem_bytes() { return sizeof(Smem); }
 
-// view of frame j of the batch in buffer `buf`
-__device__ __forceinline__ Frame frame_view(const KArgs& A, const Smem& S, int buf, int j) {
+// view of frame j of the warp-batch in buffer `buf`
+__device__ __forceinline__ Frame frame_view(const KArgs& A, const WarpSmem& W, int buf, int j) {
     Frame F;
-    const uint32_t* o = S.offs[buf] + 4 * j;
+    const uint32_t* o = W.offs[buf] + 4 * j;
     const uint32_t g = o[0];
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
         F.s[l] = (int)(o[l] - g);
         F.n[l] = (int)(o[l + 1] - o[l]);
     }
-    const bool inwin = g >= S.b_winlo[buf] && o[4] <= S.b_winhi[buf];
+    const bool inwin = g >= W.b_winlo[buf] && o[4] <= W.b_winhi[buf];
     if (inwin) {
-        const uint32_t d = g - S.b_winlo[buf];
-        F.x = S.hx[buf] + d;
-        F.y = S.hy[buf] + d;
-        F.z = S.hz[buf] + d;
-    } else {  // batch larger than the staging window: read this frame from HBM
+        const uint32_t d = g - W.b_winlo[buf];
+        F.x = W.hx[buf] + d;
+        F.y = W.hy[buf] + d;
+        F.z = W.hz[buf] + d;
+    } else {  // warp-batch larger than the staging window: read this frame from HBM
         F.x = A.x + g;
         F.y = A.y + g;
         F.z = A.z + g;
@@ -135,46 +137,42 @@ __device__ __forceinline__ Frame frame_view(const KArgs& A, const Smem& S, int b
     return F;
 }
 
-// thread 0: claim batch b into buffer buf and start its bulk copies
-__device__ __forceinline__ void issue_load(const KArgs& A, Smem& S, int buf, uint32_t b) {
-    S.b_batch[buf] = b;
+// lane 0: claim warp-batch b into buffer buf and start its bulk copies
+__device__ __forceinline__ void issue_load(const KArgs& A, WarpSmem& W, int buf, uint32_t b) {
+    W.b_batch[buf] = b;
     if (b >= A.nbatch) return;
     const uint32_t f0 = b * (uint32_t)A.fb;
     const uint32_t nf = min(A.F - f0, (uint32_t)A.fb);
     const uint32_t lo = A.offsets[4 * f0], hi = A.offsets[4 * (f0 + nf)];
     const uint32_t wlo = lo & ~3u;
     const uint32_t whi = min((hi + 3u) & ~3u, wlo + (uint32_t)kHCap);
-    S.b_winlo[buf] = wlo;
-    S.b_winhi[buf] = whi;
-    S.offs[buf][4 * nf] = hi;
+    W.b_winlo[buf] = wlo;
+    W.b_winhi[buf] = whi;
+    W.offs[buf][4 * nf] = hi;
     const uint32_t hb = (whi - wlo) * 4u, ob = nf * 16u;
     fence_proxy_async();
-    mbar_arrive_expect_tx(&S.bar[buf], 3u * hb + ob);
-    bulk_g2s(S.offs[buf], A.offsets + 4 * (size_t)f0, ob, &S.bar[buf]);
+    mbar_arrive_expect_tx(&W.bar[buf], 3u * hb + ob);
+    bulk_g2s(W.offs[buf], A.offsets + 4 * (size_t)f0, ob, &W.bar[buf]);
     if (hb) {
-        bulk_g2s(S.hx[buf], A.x + wlo, hb, &S.bar[buf]);
-        bulk_g2s(S.hy[buf], A.y + wlo, hb, &S.bar[buf]);
-        bulk_g2s(S.hz[buf], A.z + wlo, hb, &S.bar[buf]);
+        bulk_g2s(W.hx[buf], A.x + wlo, hb, &W.bar[buf]);
+        bulk_g2s(W.hy[buf], A.y + wlo, hb, &W.bar[buf]);
+        bulk_g2s(W.hz[buf], A.z + wlo, hb, &W.bar[buf]);
     }
 }
 
-// exclusive scan of v[0..n) (n <= 64) in place by one warp, v[n] = total
-__device__ __forceinline__ void warp_scan64(uint32_t* v, int n) {
+// exclusive scan of v[0..n) (n <= 32) in place by the warp, v[n] = total
+__device__ __forceinline__ void warp_scan(uint32_t* v, int n) {
     const int lane = threadIdx.x & 31;
-    const uint32_t a = (2 * lane < n) ? v[2 * lane] : 0u;
-    const uint32_t b = (2 * lane + 1 < n) ? v[2 * lane + 1] : 0u;
-    const uint32_t s = a + b;
-    uint32_t inc = s;
+    const uint32_t a = lane < n ? v[lane] : 0u;
+    uint32_t inc = a;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += t;
     }
-    const uint32_t ex = inc - s;
     const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
     __syncwarp();
-    if (2 * lane < n) v[2 * lane] = ex;
-    if (2 * lane + 1 < n) v[2 * lane + 1] = ex + a;
+    if (lane < n) v[lane] = inc - a;
     if (lane == 0) v[n] = tot;
     __syncwarp();
 }
@@ -194,13 +192,11 @@ __device__ __forceinline__ double track_energy(const DevParams& P, float kappa) 
     return sqrt(p * p + kEMass * kEMass);
 }
 
-// Decoupled look-back (warp 0).  Status word of batch b = {epoch<<2 | state,
-// tracks, kept frames, kept hits}; state 1 = aggregate, 2 = inclusive prefix.
-// publish_aggregate() runs as soon as the batch's counts are known; resolve()
-// runs one batch later (deferred), so the predecessors have normally published.
-__device__ __forceinline__ void publish_aggregate(const KArgs& A, uint32_t b, uint3 agg) {
-    const uint32_t tag = (A.epoch << 2) | (b == 0 ? 2u : 1u);
-    if ((threadIdx.x & 31) == 0) st_volatile_v4(A.status + b, make_uint4(tag, agg.x, agg.y, agg.z));
+// Decoupled look-back of the pack kernel.  Status word of tile t = {epoch<<2 |
+// state, tracks, kept frames, kept hits}; state 1 = aggregate, 2 = inclusive.
+__device__ __forceinline__ void publish_aggregate(const KArgs& A, uint32_t t, uint3 agg) {
+    const uint32_t tag = (A.epoch << 2) | (t == 0 ? 2u : 1u);
+    if ((threadIdx.x & 31) == 0) st_volatile_v4(A.status + t, make_uint4(tag, agg.x, agg.y, agg.z));
 }
 
 __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) {
@@ -217,7 +213,7 @@ __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) 
                 st = ld_volatile_v4(A.status + idx);
             } while (st.x != tagA && st.x != tagI);
         } else {
-            st = make_uint4(tagI, 0u, 0u, 0u);  // virtual inclusive zero before batch 0
+            st = make_uint4(tagI, 0u, 0u, 0u);  // virtual inclusive zero before warp-batch 0
         }
         const unsigned m = __ballot_sync(0xffffffffu, st.x == tagI);
         const int k = m ? __ffs(m) - 1 : 32;  // nearest predecessor with an inclusive prefix
@@ -232,112 +228,6 @@ __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) 
     return ex;
 }
 
-// Write the outputs of a batch whose counts and prefixes are in B (all threads):
-// per-frame records, the packed kept frames (Sec. V-A), vertices and tracks.
-template <int MODE>
-__device__ __forceinline__ void finalize_batch(const KArgs& A, Smem& S, const BatchState& B,
-                                               const m3e_track* trk) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nf = B.nf;
-    const uint32_t f0 = B.batch * (uint32_t)A.fb;
-    if (warp == 0) {
-        const uint3 ex = resolve(A, B.batch, make_uint3(B.o_trk[nf], B.o_kept[nf], B.o_hits[nf]));
-        if (lane == 0) {
-            S.g_trk = ex.x;
-            S.g_kept = ex.y;
-            S.g_hits = ex.z;
-        }
-    }
-    __syncthreads();
-    const m3e_outputs& O = A.out;
-    const uint32_t g_trk = S.g_trk, g_kept = S.g_kept, g_hits = S.g_hits;
-    for (int j = tid; j < nf; j += kThreads) {
-        const int r = B.reason[j];
-        const bool kept = r != M3E_REASON_NONE;
-        const uint32_t kidx = g_kept + B.o_kept[j];
-        if (O.reason) O.reason[f0 + j] = (uint8_t)r;
-        if (O.frames) {
-            m3e_frame_out fo;
-            fo.n_cand = (uint16_t)B.ncand[j];
-            fo.n_tracks = (uint16_t)B.ntrk[j];
-            fo.n_combs = (uint16_t)B.ncomb[j];
-            fo.reason = (uint8_t)r;
-            fo.n_neg = (uint8_t)min(B.nneg[j], 255);
-            fo.track_first = g_trk + B.o_trk[j];
-            fo.kept_index = kept ? kidx : 0xFFFFFFFFu;
-            O.frames[f0 + j] = fo;
-        }
-        if (kept) {
-            const uint32_t hb = g_hits + B.o_hits[j];
-            if (kidx < O.kept_capacity) {
-                if (O.kept_frame) O.kept_frame[kidx] = f0 + j;
-                if (O.kept_offsets)
-                    for (int l = 0; l < 4; ++l)
-                        O.kept_offsets[4 * (size_t)kidx + l] = hb + (B.offs[4 * j + l] - B.offs[4 * j]);
-                if (O.vertices) {
-                    m3e_vertex v;
-                    if (r == M3E_REASON_VERTEX) {
-                        v = B.vtx[j];
-                    } else {
-                        v = m3e_vertex{};
-                        v.frame = 0xFFFFFFFFu;
-                    }
-                    O.vertices[kidx] = v;
-                }
-            } else {
-                S.s_overflow = 1;
-            }
-        }
-    }
-    if (B.batch == A.nbatch - 1 && tid == 0 && O.kept_offsets) {  // the last batch closes the offsets
-        const uint32_t K = g_kept + B.o_kept[nf];
-        if (K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = g_hits + B.o_hits[nf];
-    }
-    if constexpr (MODE == kModeFull) {
-        const uint32_t nt = B.o_trk[nf];
-        if (O.tracks) {
-            for (uint32_t e = tid; e < nt; e += kThreads) {
-                const int j = find_frame(B.o_trk, nf, e);
-                const uint32_t dst = g_trk + e;
-                if (dst < O.track_capacity) {
-                    const uint4* s4 = reinterpret_cast<const uint4*>(trk + (size_t)j * A.P.max_tracks + (e - B.o_trk[j]));
-                    uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst);
-                    d4[0] = s4[0];
-                    d4[1] = s4[1];
-                } else {
-                    S.s_overflow = 1;
-                }
-            }
-        }
-    }
-    // packer: hits of the kept frames, verbatim, read from HBM (Sec. V-A)
-    const uint32_t nh = B.o_hits[nf];
-    if (O.kept_x) {
-        for (uint32_t e = tid; e < nh; e += kThreads) {
-            const int j = find_frame(B.o_hits, nf, e);
-            const uint32_t g = B.offs[4 * j] + (e - B.o_hits[j]);
-            const uint32_t dst = g_hits + e;
-            if (dst < O.kept_hit_capacity) {
-                O.kept_x[dst] = A.x[g];
-                O.kept_y[dst] = A.y[g];
-                O.kept_z[dst] = A.z[g];
-            } else {
-                S.s_overflow = 1;
-            }
-        }
-    }
-    if (tid == 0) {
-        S.s_frames += nf;
-        S.s_trk += B.o_trk[nf];
-        S.s_hits += B.o_hits[nf];
-        for (int j = 0; j < nf; ++j) {
-            S.s_kept[B.reason[j]] += 1;
-            S.s_cand += B.nstored[j];
-            S.s_vtx += B.reason[j] == M3E_REASON_VERTEX;
-        }
-    }
-}
-
 // ------------------------------------------------------------------ kernel ----
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
@@ -347,33 +237,37 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
     const unsigned lt_mask = (1u << lane) - 1u;
     const DevParams& P = A.P;
     constexpr bool kOut = MODE == kModeFull || MODE == kModePack;   // ordered outputs
+    WarpSmem& W = S.w[warp];
+    const size_t gwarp = (size_t)blockIdx.x * kWarps + warp;
 
     if (tid == 0) {
         S.P = A.P;
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
-        fence_mbar_init();
         for (int i = 0; i < 6; ++i) S.s_kept[i] = 0;
         S.s_cand = S.s_trk = S.s_hits = S.s_vtx = S.s_frames = 0;
         S.s_overflow = 0;
-        issue_load(A, S, 0, atomicAdd(A.ticket, 1u));
     }
-    __syncthreads();
-    int buf = 0, par = 0;
-    bool pending = false;   // S.st[par ^ 1] holds a computed batch whose outputs are not written yet
+    if (lane == 0) {
+        mbar_init(&W.bar[0], 1);
+        mbar_init(&W.bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();   // the only CTA barrier before the final summary flush
+    if (lane == 0) issue_load(A, W, 0, atomicAdd(A.ticket, 1u));
+    __syncwarp();
+    int buf = 0;
     uint32_t phase0 = 0u, phase1 = 0u;
 
-    // candidate / track slots: per-CTA scratch (FULL; tracks double-buffered by
-    // batch parity) or the caller's fixed slots (stage modes)
+    // candidate / track slots: per-warp scratch (FULL) or the caller's fixed slots
+    // (stage modes)
     uint32_t* cidx;
     float* crt;
     m3e_fit_record* crec;
     m3e_track* ctrk_base;
     if constexpr (MODE == kModeFull) {
-        cidx = A.pool_idx + (size_t)blockIdx.x * A.pool_stride;
-        crt = A.pool_rt + (size_t)blockIdx.x * A.pool_stride;
-        crec = A.pool_rec + (size_t)blockIdx.x * A.pool_stride;
-        ctrk_base = A.pool_trk + (size_t)blockIdx.x * 2 * A.trk_stride;
+        cidx = A.pool_idx + gwarp * A.pool_stride;
+        crt = A.pool_rt + gwarp * A.pool_stride;
+        crec = A.pool_rec + gwarp * A.pool_stride;
+        ctrk_base = A.pool_trk + gwarp * A.trk_stride;
     } else {
         cidx = A.s_cand;
         crt = A.s_rt;
@@ -382,34 +276,30 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
     }
 
     for (;;) {
-        const uint32_t b = S.b_batch[buf];
+        const uint32_t b = W.b_batch[buf];
         if (b >= A.nbatch) break;
-        if (tid == 0) issue_load(A, S, buf ^ 1, atomicAdd(A.ticket, 1u));
-        if (buf == 0) { mbar_wait(&S.bar[0], phase0); phase0 ^= 1u; }
-        else { mbar_wait(&S.bar[1], phase1); phase1 ^= 1u; }
+        if (lane == 0) issue_load(A, W, buf ^ 1, atomicAdd(A.ticket, 1u));
+        if (buf == 0) { mbar_wait(&W.bar[0], phase0); phase0 ^= 1u; }
+        else { mbar_wait(&W.bar[1], phase1); phase1 ^= 1u; }
 
-        BatchState& B = S.st[par];
+        BatchState& B = W.st;
         const uint32_t f0 = b * (uint32_t)A.fb;
         const int nf = (int)min(A.F - f0, (uint32_t)A.fb);
         const size_t cfirst = MODE == kModeFull ? 0 : (size_t)f0 * P.cuts_max;   // slot of frame 0
         const size_t tfirst = MODE == kModeFull ? 0 : (size_t)f0 * P.max_tracks;
-        m3e_track* ctrk = MODE == kModeFull ? ctrk_base + (size_t)par * A.trk_stride : ctrk_base;
-        if (tid == 0) {
-            B.batch = b;
-            B.nf = nf;
-        }
+        m3e_track* ctrk = ctrk_base;
 
         // ---------------------------------------------------- S: Selection Cuts
         if constexpr (MODE == kModeFull || MODE == kModeSelect) {
-            for (int j = warp; j < nf; j += kWarps) {
-                const Frame Fv = frame_view(A, S, buf, j);
+            for (int j = 0; j < nf; ++j) {
+                const Frame Fv = frame_view(A, W, buf, j);
                 const bool inval = Fv.n[0] > kMaxLayerHits || Fv.n[1] > kMaxLayerHits ||
                                    Fv.n[2] > kMaxLayerHits || Fv.n[3] > kMaxLayerHits;
                 int count = 0;
                 if (!inval) {
                     uint32_t* ci = cidx + cfirst + (size_t)j * P.cuts_max;
                     float* cr = crt + cfirst + (size_t)j * P.cuts_max;
-                    count = select_frame_warp(P, Fv, [&](int pos, uint32_t packed, float rt) {
+                    count = select_frame_warp(P, Fv, W.q, [&](int pos, uint32_t packed, float rt) {
                         ci[pos] = packed;
                         cr[pos] = rt;
                     });
@@ -423,21 +313,21 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                 }
             }
         } else if constexpr (MODE == kModeFit) {
-            for (int j = tid; j < nf; j += kThreads) {
+            for (int j = lane; j < nf; j += 32) {
                 const int n = A.s_ncand[f0 + j];
                 B.ncand[j] = n;
                 B.reason[j] = n > P.cuts_max ? M3E_REASON_TRIPLET_OVERFLOW : M3E_REASON_NONE;
                 B.nstored[j] = n > P.cuts_max ? 0 : n;
             }
         } else if constexpr (MODE == kModeVertex) {
-            for (int j = tid; j < nf; j += kThreads) {
+            for (int j = lane; j < nf; j += 32) {
                 B.ncand[j] = 0;
                 B.nstored[j] = 0;
                 B.reason[j] = M3E_REASON_NONE;
                 B.ntrk[j] = min((int)A.s_ntrk[f0 + j], P.max_tracks);
             }
         } else {  // kModePack
-            for (int j = tid; j < nf; j += kThreads) {
+            for (int j = lane; j < nf; j += 32) {
                 B.ncand[j] = 0;
                 B.nstored[j] = 0;
                 B.ntrk[j] = 0;
@@ -446,10 +336,10 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                 B.reason[j] = A.s_reason[f0 + j];
             }
         }
-        __syncthreads();
+        __syncwarp();
 
         if constexpr (MODE == kModeSelect) {
-            for (int j = tid; j < nf; j += kThreads) {
+            for (int j = lane; j < nf; j += 32) {
                 m3e_frame_out fo;
                 fo.n_cand = (uint16_t)B.ncand[j];
                 fo.n_tracks = 0;
@@ -464,18 +354,15 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
 
         // -------------------------------------- F: Triplet fit, one lane per candidate
         if constexpr (MODE == kModeFull || MODE == kModeFit) {
-            if (warp == 0) {
-                for (int j = lane; j < nf; j += 32) S.pref[j] = (uint32_t)B.nstored[j];
-                __syncwarp();
-                warp_scan64(S.pref, nf);
-            }
-            __syncthreads();
-            const int total = (int)S.pref[nf];
-            for (int e = tid; e < total; e += kThreads) {
-                const int j = find_frame(S.pref, nf, (uint32_t)e);
-                const size_t slot = cfirst + (size_t)j * P.cuts_max + (e - (int)S.pref[j]);
+            for (int j = lane; j < nf; j += 32) W.pref[j] = (uint32_t)B.nstored[j];
+            __syncwarp();
+            warp_scan(W.pref, nf);
+            const int total = (int)W.pref[nf];
+            for (int e = lane; e < total; e += 32) {
+                const int j = find_frame(W.pref, nf, (uint32_t)e);
+                const size_t slot = cfirst + (size_t)j * P.cuts_max + (e - (int)W.pref[j]);
                 const uint32_t pk = cidx[slot];
-                const Frame Fv = frame_view(A, S, buf, j);
+                const Frame Fv = frame_view(A, W, buf, j);
                 const FitOut o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, crt[slot]);
                 m3e_fit_record r;
                 r.status = (uint8_t)o.status;
@@ -492,10 +379,10 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                 r.cy = o.cy;
                 crec[slot] = r;
             }
-            __syncthreads();
+            __syncwarp();
 
             // ------------------------- T: per-frame track compaction (ballot / popc)
-            for (int j = warp; j < nf; j += kWarps) {
+            for (int j = 0; j < nf; ++j) {
                 if (B.reason[j] != M3E_REASON_NONE) {
                     if (lane == 0) { B.ntrk[j] = 0; B.nneg[j] = 0; }
                     continue;
@@ -543,11 +430,11 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                     }
                 }
             }
-            __syncthreads();
+            __syncwarp();
         }
 
         if constexpr (MODE == kModeFit) {
-            for (int j = tid; j < nf; j += kThreads) {
+            for (int j = lane; j < nf; j += 32) {
                 m3e_frame_out fo;
                 fo.n_cand = (uint16_t)B.ncand[j];
                 fo.n_tracks = (uint16_t)B.ntrk[j];
@@ -562,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
 
         // --------------------------------------------- V: vertex selection (fp64)
         if constexpr (MODE == kModeFull || MODE == kModeVertex) {
-            for (int j = warp; j < nf; j += kWarps) {
+            for (int j = 0; j < nf; ++j) {
                 int ncomb = 0, nneg_out = 0;
                 bool has_vtx = false;
                 if (B.reason[j] == M3E_REASON_NONE) {
@@ -576,15 +463,15 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                         const bool ispos = i < nt && kap > 0.0f, isneg = i < nt && kap < 0.0f;
                         const unsigned mp = __ballot_sync(0xffffffffu, ispos);
                         const unsigned mn = __ballot_sync(0xffffffffu, isneg);
-                        if (ispos) S.vlist[warp][0][npos + __popc(mp & lt_mask)] = (uint8_t)i;
-                        if (isneg) S.vlist[warp][1][nneg + __popc(mn & lt_mask)] = (uint8_t)i;
+                        if (ispos) W.vlist[0][npos + __popc(mp & lt_mask)] = (uint8_t)i;
+                        if (isneg) W.vlist[1][nneg + __popc(mn & lt_mask)] = (uint8_t)i;
                         npos += __popc(mp);
                         nneg += __popc(mn);
                     }
                     __syncwarp();
                     nneg_out = nneg;
                     if (npos >= 2 && nneg >= 1) {
-                        const Frame Fv = frame_view(A, S, buf, j);
+                        const Frame Fv = frame_view(A, W, buf, j);
                         // Alg. 4 phase 1: energy test over (a < b, e) in row-major order
                         const int tot = npos * npos * nneg;
                         for (int base = 0; base < tot; base += 32) {
@@ -595,8 +482,7 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                                 const int ia = t / (npos * nneg), rem = t - ia * npos * nneg;
                                 const int ib = rem / nneg, ie = rem - ib * nneg;
                                 if (ia < ib) {
-                                    const int a = S.vlist[warp][0][ia], bb = S.vlist[warp][0][ib],
-                                              e = S.vlist[warp][1][ie];
+                                    const int a = W.vlist[0][ia], bb = W.vlist[0][ib], e = W.vlist[1][ie];
                                     const double dE = track_energy(P, tj[a].kappa) + track_energy(P, tj[bb].kappa) +
                                                       track_energy(P, tj[e].kappa) - kMuMass;
                                     pass = fabs(dE) <= P.e_window;
@@ -605,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                             }
                             const unsigned m = __ballot_sync(0xffffffffu, pass);
                             const int pos = ncomb + __popc(m & lt_mask);
-                            if (pass && pos < P.max_combs) S.vcomb[warp][pos] = code;
+                            if (pass && pos < P.max_combs) W.vcomb[pos] = code;
                             ncomb += __popc(m);
                             if (ncomb > P.max_combs) break;
                         }
@@ -619,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                             VResult bres;
                             bres.pass = 0;
                             for (int c = lane; c < ncomb; c += 32) {
-                                const uint32_t code = S.vcomb[warp][c];
+                                const uint32_t code = W.vcomb[c];
                                 VTrk T[3];
                                 T[0] = make_vtrk(P, tj[code & 255u], Fv);
                                 T[1] = make_vtrk(P, tj[(code >> 8) & 255u], Fv);
@@ -639,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                             if (widx != 0x7fffffff) {
                                 has_vtx = true;
                                 if (bidx == widx) {
-                                    const uint32_t code = S.vcomb[warp][widx];
+                                    const uint32_t code = W.vcomb[widx];
                                     m3e_vertex v;
                                     v.frame = f0 + j;
                                     v.track[0] = (uint16_t)(code & 255u);
@@ -667,11 +553,10 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                 }
                 __syncwarp();
             }
-            __syncthreads();
         }
 
         if constexpr (MODE == kModeVertex) {
-            for (int j = tid; j < nf; j += kThreads) {
+            for (int j = lane; j < nf; j += 32) {
                 m3e_frame_out fo;
                 fo.n_cand = 0;
                 fo.n_tracks = (uint16_t)B.ntrk[j];
@@ -685,44 +570,116 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
             }
         }
 
-        // ------------------------ O: counts, aggregate now, outputs one batch later
+        // --------------------- O: records in place, tracks / kept frames staged
         if constexpr (kOut) {
-            for (int j = tid; j < nf; j += kThreads) {
+            for (int j = lane; j < nf; j += 32) {
                 const int r = B.reason[j];
                 const bool kept = r != M3E_REASON_NONE;
                 const bool has_tracks = r == M3E_REASON_NONE || r == M3E_REASON_TRACK_OVERFLOW ||
                                         r == M3E_REASON_COMB_OVERFLOW || r == M3E_REASON_VERTEX;
                 B.o_trk[j] = (MODE == kModeFull && has_tracks) ? (uint32_t)min(B.ntrk[j], P.max_tracks) : 0u;
                 B.o_kept[j] = kept ? 1u : 0u;
-                B.o_hits[j] = kept ? (S.offs[buf][4 * j + 4] - S.offs[buf][4 * j]) : 0u;
+                B.o_hits[j] = kept ? (W.offs[buf][4 * j + 4] - W.offs[buf][4 * j]) : 0u;
             }
-            for (int i = tid; i <= 4 * nf; i += kThreads) B.offs[i] = S.offs[buf][i];
-            __syncthreads();
-            if (warp == 0) {
-                warp_scan64(B.o_trk, nf);
-                warp_scan64(B.o_kept, nf);
-                warp_scan64(B.o_hits, nf);
-                publish_aggregate(A, b, make_uint3(B.o_trk[nf], B.o_kept[nf], B.o_hits[nf]));
+            __syncwarp();
+            warp_scan(B.o_trk, nf);
+            warp_scan(B.o_kept, nf);
+            warp_scan(B.o_hits, nf);
+            const uint32_t nt = B.o_trk[nf], nk = B.o_kept[nf];
+            uint32_t s_trk = 0, s_kept = 0;
+            if (lane == 0) {
+                if (nt && A.stage_trk) s_trk = atomicAdd(A.ticket + 1, nt);
+                if (nk) s_kept = atomicAdd(A.ticket + 2, nk);
             }
-            // the previous batch's predecessors have had a whole batch of time to publish
-            if (pending) {
-                __syncthreads();
-                finalize_batch<MODE>(A, S, S.st[par ^ 1],
-                                     MODE == kModeFull ? ctrk_base + (size_t)(par ^ 1) * A.trk_stride : nullptr);
+            s_trk = __shfl_sync(0xffffffffu, s_trk, 0);
+            s_kept = __shfl_sync(0xffffffffu, s_kept, 0);
+            bool overflow = false;
+            const m3e_outputs& O = A.out;
+            for (int j = lane; j < nf; j += 32) {
+                const int r = B.reason[j];
+                if (O.reason) O.reason[f0 + j] = (uint8_t)r;
+                if (O.frames) {   // track_first / kept_index: warp-batch relative until the pack kernel
+                    m3e_frame_out fo;
+                    fo.n_cand = (uint16_t)B.ncand[j];
+                    fo.n_tracks = (uint16_t)B.ntrk[j];
+                    fo.n_combs = (uint16_t)B.ncomb[j];
+                    fo.reason = (uint8_t)r;
+                    fo.n_neg = (uint8_t)min(B.nneg[j], 255);
+                    fo.track_first = B.o_trk[j];
+                    fo.kept_index = r != M3E_REASON_NONE ? B.o_kept[j] : 0xFFFFFFFFu;
+                    O.frames[f0 + j] = fo;
+                }
+                if (r != M3E_REASON_NONE) {
+                    const uint32_t k = s_kept + B.o_kept[j];
+                    if (k < A.stage_kept_cap) {
+                        KeptRec kr;
+                        kr.frame = f0 + j;
+                        kr.pad = 0;
+                        if (r == M3E_REASON_VERTEX) {
+                            kr.v = B.vtx[j];
+                        } else {
+                            kr.v = m3e_vertex{};
+                            kr.v.frame = 0xFFFFFFFFu;
+                        }
+                        A.stage_kept[k] = kr;
+                    } else {
+                        overflow = true;
+                    }
+                }
             }
-            pending = true;
-            par ^= 1;
+            if constexpr (MODE == kModeFull) {
+                if (A.stage_trk) {
+                    for (uint32_t e = lane; e < nt; e += 32) {
+                        const int j = find_frame(B.o_trk, nf, e);
+                        const uint32_t dst = s_trk + e;
+                        if (dst < A.stage_trk_cap) {
+                            const uint4* s4 = reinterpret_cast<const uint4*>(ctrk + (size_t)j * P.max_tracks +
+                                                                             (e - B.o_trk[j]));
+                            uint4* d4 = reinterpret_cast<uint4*>(A.stage_trk + dst);
+                            d4[0] = s4[0];
+                            d4[1] = s4[1];
+                        } else {
+                            overflow = true;
+                        }
+                    }
+                }
+            }
+            if (lane == 0) {
+                BatchStat bs;
+                bs.n_trk = nt;
+                bs.n_kept = nk;
+                bs.n_hits = B.o_hits[nf];
+                bs.s_trk = s_trk;
+                bs.s_kept = s_kept;
+                bs.nf = nf;
+                bs.pad[0] = bs.pad[1] = 0;
+                A.bstat[b] = bs;
+            }
+            // run summary (shared-memory accumulators, flushed once per CTA)
+            uint32_t kept_r[6] = {0, 0, 0, 0, 0, 0};
+            uint32_t cand = 0;
+            for (int j = lane; j < nf; j += 32) {
+                kept_r[B.reason[j]] += 1;
+                cand += B.nstored[j];
+            }
+            for (int r = 0; r < 6; ++r) kept_r[r] = warp_sum(kept_r[r]);
+            cand = warp_sum(cand);
+            if (lane == 0) {
+                atomicAdd(&S.s_frames, (unsigned long long)nf);
+                atomicAdd(&S.s_trk, (unsigned long long)nt);
+                atomicAdd(&S.s_hits, (unsigned long long)B.o_hits[nf]);
+                atomicAdd(&S.s_cand, (unsigned long long)cand);
+                atomicAdd(&S.s_vtx, (unsigned long long)kept_r[M3E_REASON_VERTEX]);
+                for (int r = 0; r < 6; ++r)
+                    if (kept_r[r]) atomicAdd(&S.s_kept[r], (unsigned long long)kept_r[r]);
+            }
+            if (__any_sync(0xffffffffu, overflow) && lane == 0) S.s_overflow = 1;
         }
-        __syncthreads();
+        __syncwarp();
         buf ^= 1;
     }
 
     if constexpr (kOut) {
-        if (pending) {
-            __syncthreads();
-            finalize_batch<MODE>(A, S, S.st[par ^ 1],
-                                 MODE == kModeFull ? ctrk_base + (size_t)(par ^ 1) * A.trk_stride : nullptr);
-        }
         __syncthreads();
         if (tid == 0 && A.out.summary) {
             m3e_summary* sm = A.out.summary;
@@ -736,6 +693,164 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
             if (S.s_overflow) atomicExch((unsigned long long*)&sm->overflow, 1ull);
         }
     }
+}
+
+// ------------------------------------------------------------- pack kernel ----
+// Output packer (north-star row (f)): tile t = warp-batches [256 t, 256 t + 256),
+// one warp per 32 warp-batches.  The tile's counts are summed at once, a decoupled
+// look-back over tiles gives its global bases, and every warp-batch's tracks,
+// kept-frame records, packed hits (SoA) and per-frame indices are written in frame
+// order.  Memory bound: reads the staged records once, writes the outputs once.
+struct PackSmem {
+    uint32_t wagg[kWarps][3];
+    uint32_t base[3];
+    uint32_t tile;
+};
+
+__global__ void __launch_bounds__(kThreads) pack_kernel(const KArgs A) {
+    __shared__ PackSmem S;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const m3e_outputs& O = A.out;
+    const uint32_t ntiles = (A.nbatch + kPackTile - 1) / kPackTile;
+    for (;;) {
+        if (tid == 0) S.tile = atomicAdd(A.ticket + 3, 1u);
+        __syncthreads();
+        const uint32_t t = S.tile;
+        if (t >= ntiles) break;
+        const uint32_t b = t * kPackTile + warp * 32 + lane;
+        BatchStat bs = {};
+        if (b < A.nbatch) bs = A.bstat[b];
+        // warp-inclusive scans of the three counts
+        uint32_t it = bs.n_trk, ik = bs.n_kept, ih = bs.n_hits;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t a = __shfl_up_sync(0xffffffffu, it, o);
+            const uint32_t c = __shfl_up_sync(0xffffffffu, ik, o);
+            const uint32_t d = __shfl_up_sync(0xffffffffu, ih, o);
+            if (lane >= o) { it += a; ik += c; ih += d; }
+        }
+        if (lane == 31) { S.wagg[warp][0] = it; S.wagg[warp][1] = ik; S.wagg[warp][2] = ih; }
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t a0 = lane < kWarps ? S.wagg[lane][0] : 0u, a1 = lane < kWarps ? S.wagg[lane][1] : 0u,
+                     a2 = lane < kWarps ? S.wagg[lane][2] : 0u;
+            const uint3 agg = make_uint3(warp_sum(a0), warp_sum(a1), warp_sum(a2));
+            publish_aggregate(A, t, agg);
+            const uint3 ex = resolve(A, t, agg);
+            if (lane == 0) { S.base[0] = ex.x; S.base[1] = ex.y; S.base[2] = ex.z; }
+        }
+        __syncthreads();
+        uint32_t wb0 = S.base[0], wb1 = S.base[1], wb2 = S.base[2];
+        for (int w = 0; w < warp; ++w) { wb0 += S.wagg[w][0]; wb1 += S.wagg[w][1]; wb2 += S.wagg[w][2]; }
+        // exclusive bases of this lane's warp-batch
+        const uint32_t eb_trk = wb0 + it - bs.n_trk, eb_kept = wb1 + ik - bs.n_kept, eb_hits = wb2 + ih - bs.n_hits;
+        bool overflow = false;
+        // each warp walks its 32 warp-batches; all lanes cooperate on one at a time
+        for (int src = 0; src < 32; ++src) {
+            const uint32_t bb = t * kPackTile + warp * 32 + src;
+            if (bb >= A.nbatch) break;
+            const uint32_t n_trk = __shfl_sync(0xffffffffu, bs.n_trk, src);
+            const uint32_t n_kept = __shfl_sync(0xffffffffu, bs.n_kept, src);
+            const uint32_t s_trk = __shfl_sync(0xffffffffu, bs.s_trk, src);
+            const uint32_t s_kept = __shfl_sync(0xffffffffu, bs.s_kept, src);
+            const uint32_t nf = __shfl_sync(0xffffffffu, bs.nf, src);
+            const uint32_t g_trk = __shfl_sync(0xffffffffu, eb_trk, src);
+            const uint32_t g_kept = __shfl_sync(0xffffffffu, eb_kept, src);
+            uint32_t g_hits = __shfl_sync(0xffffffffu, eb_hits, src);
+            const uint32_t f0 = bb * (uint32_t)A.fb;
+            // tracks
+            if (O.tracks && A.stage_trk) {
+                for (uint32_t e = lane; e < n_trk; e += 32) {
+                    const uint32_t dst = g_trk + e;
+                    if (dst < O.track_capacity && s_trk + e < A.stage_trk_cap) {
+                        const uint4* s4 = reinterpret_cast<const uint4*>(A.stage_trk + s_trk + e);
+                        uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst);
+                        d4[0] = s4[0];
+                        d4[1] = s4[1];
+                    } else {
+                        overflow = true;
+                    }
+                }
+            }
+            // per-frame indices: warp-batch relative -> call global
+            if (O.frames) {
+                for (uint32_t j = lane; j < nf; j += 32) {
+                    m3e_frame_out& fo = O.frames[f0 + j];
+                    fo.track_first += g_trk;
+                    if (fo.kept_index != 0xFFFFFFFFu) fo.kept_index += g_kept;
+                }
+            }
+            // kept frames: records, offsets and hits, in frame order
+            for (uint32_t k0 = 0; k0 < n_kept; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                uint32_t f = 0, nh = 0, lo = 0;
+                const bool valid = k < n_kept && s_kept + k < A.stage_kept_cap;
+                KeptRec kr;
+                if (valid) {
+                    kr = A.stage_kept[s_kept + k];
+                    f = kr.frame;
+                    lo = A.offsets[4 * (size_t)f];
+                    nh = A.offsets[4 * (size_t)f + 4] - lo;
+                }
+                if (k < n_kept && !valid) overflow = true;
+                // exclusive prefix of the kept frames' hit counts inside this warp-batch
+                uint32_t inc = nh;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += a;
+                }
+                const uint32_t hb = g_hits + inc - nh;
+                const uint32_t kidx = g_kept + k;
+                if (valid) {
+                    if (kidx < O.kept_capacity) {
+                        if (O.kept_frame) O.kept_frame[kidx] = f;
+                        if (O.vertices) O.vertices[kidx] = kr.v;
+                        if (O.kept_offsets)
+                            for (int l = 0; l < 4; ++l)
+                                O.kept_offsets[4 * (size_t)kidx + l] = hb + (A.offsets[4 * (size_t)f + l] - lo);
+                    } else {
+                        overflow = true;
+                    }
+                }
+                const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+                __syncwarp();
+                if (O.kept_x) {
+                    // simple per-frame loop: kept frames are rare (<< 1 % of frames)
+                    for (int src2 = 0; src2 < 32; ++src2) {
+                        const uint32_t kk = k0 + src2;
+                        if (kk >= n_kept) break;
+                        const uint32_t fl = __shfl_sync(0xffffffffu, lo, src2);
+                        const uint32_t fn = __shfl_sync(0xffffffffu, nh, src2);
+                        const uint32_t fh = __shfl_sync(0xffffffffu, hb, src2);
+                        for (uint32_t e = lane; e < fn; e += 32) {
+                            const uint32_t dst = fh + e;
+                            if (dst < O.kept_hit_capacity) {
+                                O.kept_x[dst] = A.x[fl + e];
+                                O.kept_y[dst] = A.y[fl + e];
+                                O.kept_z[dst] = A.z[fl + e];
+                            } else {
+                                overflow = true;
+                            }
+                        }
+                    }
+                }
+                g_hits += tot;
+            }
+            if (bb == A.nbatch - 1 && lane == 0 && O.kept_offsets) {   // close the packed offsets
+                const uint32_t K = g_kept + n_kept;
+                if (K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = g_hits;
+            }
+        }
+        if (__any_sync(0xffffffffu, overflow) && lane == 0 && O.summary)
+            atomicExch((unsigned long long*)&O.summary->overflow, 1ull);
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s) {
+    pack_kernel<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 template <int MODE>
@@ -758,20 +873,27 @@ cudaError_t launch_filter(int mode, const KArgs& a, int grid, cudaStream_t s) {
     return cudaErrorInvalidValue;
 }
 
-int blocks_per_sm(int mode) {
+template <int MODE>
+static int occupancy() {
     int n = 0;
     const size_t smem = smem_bytes();
-    cudaError_t e = cudaErrorInvalidValue;
+    if (cudaFuncSetAttribute(filter_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, filter_kernel<MODE>, kThreads, smem) != cudaSuccess)
+        return 1;
+    return n > 0 ? n : 1;
+}
+
+int blocks_per_sm(int mode) {
     switch (mode) {
-        case kModeFull:
-            cudaFuncSetAttribute(filter_kernel<kModeFull>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, filter_kernel<kModeFull>, kThreads, smem);
-            break;
-        default:
-            n = 1;
-            e = cudaSuccess;
+        case kModeFull: return occupancy<kModeFull>();
+        case kModeSelect: return occupancy<kModeSelect>();
+        case kModeFit: return occupancy<kModeFit>();
+        case kModeVertex: return occupancy<kModeVertex>();
+        case kModePack: return occupancy<kModePack>();
     }
-    return e == cudaSuccess && n > 0 ? n : 1;
+    return 1;
 }
 
 }  // namespace m3e

@@ -10,15 +10,33 @@
 
 namespace m3e {
 
-constexpr int kThreads = 256;        // 8 warps per CTA
+constexpr int kThreads = 256;        // 8 warps per CTA, each an independent pipeline
 constexpr int kWarps = kThreads / 32;
-constexpr int kFB = 64;              // frames per batch (upper bound; runtime fb <= kFB)
-constexpr int kHCap = 2048;          // hits of a batch staged in shared memory
+constexpr int kFB = 16;              // frames per warp-batch (upper bound; runtime fb <= kFB)
+constexpr int kHCap = 320;           // hits of a warp-batch staged in shared memory (per buffer)
 constexpr int kMaxTracksCap = 128;   // upper bound accepted for params.max_tracks
-constexpr int kMaxCombsCap = 256;    // upper bound accepted for params.max_combs + 1
+constexpr int kMaxCombsCap = 128;    // upper bound accepted for params.max_combs + 1
 constexpr int kMaxCutsCap = 1023;    // upper bound accepted for params.cuts_max
 
 enum { kModeFull = 0, kModeSelect = 1, kModeFit = 2, kModeVertex = 3, kModePack = 4 };
+
+constexpr int kPackTile = 256;       // warp-batches per CTA of the pack kernel (8 warps x 32)
+
+// per warp-batch counts and staging offsets, written by the filter kernel and
+// consumed by the pack kernel (32 B)
+struct BatchStat {
+    uint32_t n_trk, n_kept, n_hits;  // tracks, kept frames, hits of kept frames
+    uint32_t s_trk, s_kept;          // staging offsets of its tracks / kept-frame records
+    uint32_t nf;                     // frames in the warp-batch
+    uint32_t pad[2];
+};
+
+// kept-frame record staged by the filter kernel (64 B)
+struct KeptRec {
+    uint32_t frame;
+    uint32_t pad;
+    m3e_vertex v;                    // v.frame = 0xFFFFFFFF unless the frame has a vertex
+};
 
 struct KArgs {
     DevParams P;
@@ -30,16 +48,22 @@ struct KArgs {
     int fb;                // frames per batch
     uint32_t nbatch;
     // workspace
-    uint32_t* ticket;      // batch ticket counter (zeroed before the launch)
-    uint4* status;         // decoupled look-back status, one 16 B word per batch
+    uint32_t* ticket;      // counters (zeroed before the launch): [0] warp-batch ticket, [1] staged
+                           // tracks, [2] staged kept frames, [3] pack-kernel tile ticket
+    uint4* status;         // pack-kernel decoupled look-back, one 16 B word per tile
     uint32_t epoch;        // launch epoch tag of the status words (never 0)
+    BatchStat* bstat;      // [nbatch]
+    m3e_track* stage_trk;  // staged tracks
+    uint64_t stage_trk_cap;
+    KeptRec* stage_kept;   // staged kept-frame records
+    uint64_t stage_kept_cap;
     // per-CTA scratch (MODE_FULL)
     uint32_t* pool_idx;
     float* pool_rt;
     m3e_fit_record* pool_rec;
     m3e_track* pool_trk;
-    size_t pool_stride;    // candidate entries per CTA = fb * cuts_max
-    size_t trk_stride;     // track entries per CTA = fb * max_tracks
+    size_t pool_stride;    // candidate entries per warp >= fb * cuts_max
+    size_t trk_stride;     // track entries per warp >= fb * max_tracks
     // stage-mode fixed slots
     uint32_t* s_cand;
     float* s_rt;
@@ -55,6 +79,7 @@ struct KArgs {
 
 size_t smem_bytes();
 cudaError_t launch_filter(int mode, const KArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);
 int blocks_per_sm(int mode);
 
 }  // namespace m3e

@@ -49,6 +49,12 @@ struct Workspace {
     size_t pool_stride = 0, trk_stride = 0;
     int pool_ctas = 0;
     uint32_t epoch = 0;
+    BatchStat* bstat = nullptr;
+    size_t bstat_n = 0;
+    m3e_track* stage_trk = nullptr;
+    size_t stage_trk_n = 0;
+    KeptRec* stage_kept = nullptr;
+    size_t stage_kept_n = 0;
     size_t bytes = 0;
 };
 
@@ -85,6 +91,9 @@ struct m3e_context {
 namespace {
 
 void free_ws(Workspace& w) {
+    cudaFree(w.bstat);
+    cudaFree(w.stage_trk);
+    cudaFree(w.stage_kept);
     cudaFree(w.ticket);
     cudaFree(w.status);
     cudaFree(w.pool_idx);
@@ -116,7 +125,7 @@ int validate(const m3e_params* p) {
     if (p->max_tracks < 1 || p->max_tracks > kMaxTracksCap)
         return fail(M3E_ERR_INVALID_ARGUMENT, "max_tracks must be in [1, 128]");
     if (p->max_combs < 0 || p->max_combs + 1 > kMaxCombsCap)
-        return fail(M3E_ERR_INVALID_ARGUMENT, "max_combs must be in [0, 255]");
+        return fail(M3E_ERR_INVALID_ARGUMENT, "max_combs must be in [0, 127]");
     if (!(p->x_over_x0 > 0)) return fail(M3E_ERR_INVALID_ARGUMENT, "x_over_x0 must be > 0");
     if (!(p->target_r > 0) || !(p->target_half > 0))
         return fail(M3E_ERR_INVALID_ARGUMENT, "target dimensions must be > 0");
@@ -157,12 +166,12 @@ DevParams make_dev_params(const m3e_params* p) {
     return d;
 }
 
-// frames per batch: keep a batch's hits within the shared-memory window
+// frames per warp-batch: keep a batch's hits within the shared-memory window
 int choose_fb(uint64_t F, uint64_t H) {
     if (F == 0) return kFB;
     const double mean = (double)H / (double)F;
-    int fb = (int)((double)kHCap / (1.25 * std::max(mean, 1.0)));
-    return std::max(8, std::min(kFB, fb));
+    int fb = (int)((double)kHCap / (1.15 * std::max(mean, 1.0)));
+    return std::max(1, std::min(kFB, fb));
 }
 
 int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p, int fb, int ctas) {
@@ -170,10 +179,19 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
         CK(cudaMalloc(&w.ticket, 16));
         w.bytes += 16;
     }
-    if (w.status_n < nbatch) {
+    const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
+    if (w.bstat_n < nbatch) {
+        cudaFree(w.bstat);
+        w.bytes -= w.bstat_n * sizeof(BatchStat);
+        const size_t n = std::max<size_t>(nbatch, 4096);
+        CK(cudaMalloc(&w.bstat, n * sizeof(BatchStat)));
+        w.bstat_n = n;
+        w.bytes += n * sizeof(BatchStat);
+    }
+    if (w.status_n < ntiles) {
         cudaFree(w.status);
         w.bytes -= w.status_n * sizeof(uint4);
-        const size_t n = std::max<size_t>(nbatch, 1024);
+        const size_t n = std::max<size_t>(ntiles, 1024);
         CK(cudaMalloc(&w.status, n * sizeof(uint4)));
         CK(cudaMemset(w.status, 0, n * sizeof(uint4)));
         w.status_n = n;
@@ -182,19 +200,43 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
     }
     const size_t ps = (size_t)fb * p->cuts_max, ts = (size_t)fb * p->max_tracks;
     if (w.pool_ctas < ctas || w.pool_stride < ps || w.trk_stride < ts) {
+        w.bytes -= w.pool_ctas ? (size_t)w.pool_ctas * kWarps *
+                                     (w.pool_stride * (sizeof(uint32_t) + sizeof(float) + sizeof(m3e_fit_record)) +
+                                      w.trk_stride * sizeof(m3e_track))
+                               : 0;
         cudaFree(w.pool_idx); cudaFree(w.pool_rt); cudaFree(w.pool_rec); cudaFree(w.pool_trk);
         const size_t PS = std::max(ps, (size_t)kFB * 768), TS = std::max(ts, (size_t)kFB * 64);
-        const int n = std::max(ctas, w.pool_ctas);
+        const int n = std::max(ctas, w.pool_ctas) * kWarps;   // per warp
         CK(cudaMalloc(&w.pool_idx, PS * n * sizeof(uint32_t)));
         CK(cudaMalloc(&w.pool_rt, PS * n * sizeof(float)));
         CK(cudaMalloc(&w.pool_rec, PS * n * sizeof(m3e_fit_record)));
-        CK(cudaMalloc(&w.pool_trk, 2 * TS * n * sizeof(m3e_track)));  // double-buffered by batch parity
+        CK(cudaMalloc(&w.pool_trk, TS * n * sizeof(m3e_track)));
         w.pool_stride = PS;
         w.trk_stride = TS;
-        w.pool_ctas = n;
-        w.bytes += PS * n * (sizeof(uint32_t) + sizeof(float) + sizeof(m3e_fit_record)) + 2 * TS * n * sizeof(m3e_track);
+        w.pool_ctas = n / kWarps;
+        w.bytes += PS * n * (sizeof(uint32_t) + sizeof(float) + sizeof(m3e_fit_record)) + TS * n * sizeof(m3e_track);
     }
     (void)c;
+    return M3E_OK;
+}
+
+// staging of the filter kernel's tracks and kept-frame records, sized by the
+// caller's output capacities (the pack kernel copies them into place)
+int ensure_stage(Workspace& w, uint64_t trk, uint64_t kept) {
+    if (w.stage_trk_n < trk) {
+        cudaFree(w.stage_trk);
+        w.bytes -= w.stage_trk_n * sizeof(m3e_track);
+        CK(cudaMalloc(&w.stage_trk, trk * sizeof(m3e_track)));
+        w.stage_trk_n = trk;
+        w.bytes += trk * sizeof(m3e_track);
+    }
+    if (w.stage_kept_n < kept) {
+        cudaFree(w.stage_kept);
+        w.bytes -= w.stage_kept_n * sizeof(KeptRec);
+        CK(cudaMalloc(&w.stage_kept, kept * sizeof(KeptRec)));
+        w.stage_kept_n = kept;
+        w.bytes += kept * sizeof(KeptRec);
+    }
     return M3E_OK;
 }
 
@@ -229,9 +271,25 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     a.pool_idx = w.pool_idx; a.pool_rt = w.pool_rt; a.pool_rec = w.pool_rec; a.pool_trk = w.pool_trk;
     a.pool_stride = w.pool_stride;
     a.trk_stride = w.trk_stride;
-    CK(cudaMemsetAsync(w.ticket, 0, sizeof(uint32_t), s));
+    const bool packs = mode == kModeFull || mode == kModePack;
+    if (packs) {
+        const bool want_trk = mode == kModeFull && a.out.tracks != nullptr;
+        rc = ensure_stage(w, want_trk ? a.out.track_capacity : 0, a.out.kept_capacity);
+        if (rc) return rc;
+        a.bstat = w.bstat;
+        a.stage_trk = want_trk ? w.stage_trk : nullptr;
+        a.stage_trk_cap = want_trk ? a.out.track_capacity : 0;
+        a.stage_kept = w.stage_kept;
+        a.stage_kept_cap = a.out.kept_capacity;
+    }
+    CK(cudaMemsetAsync(w.ticket, 0, 4 * sizeof(uint32_t), s));
     if (a.out.summary) CK(cudaMemsetAsync(a.out.summary, 0, sizeof(m3e_summary), s));
     CK(launch_filter(mode, a, grid, s));
+    if (packs) {
+        const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
+        const int pgrid = (int)std::min<uint64_t>(ntiles, (uint64_t)ctx->sms * 8);
+        CK(launch_pack(a, pgrid, s));
+    }
     return M3E_OK;
 }
 
