@@ -99,6 +99,7 @@ struct __align__(16) WarpSmem {
     uint32_t b_batch[2], b_winlo[2], b_winhi[2];
     BatchState st;
     uint32_t pref[kFB + 1];          // candidates: exclusive prefix
+    int npos[kFB];                   // stored positive tracks per frame (vertex gate)
     uint32_t q[64];                  // Delta-lambda survivors (selection FIFO)
     uint8_t vlist[2][kMaxTracksCap];
     uint32_t vcomb[kMaxCombsCap];
@@ -228,6 +229,115 @@ __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) 
     return ex;
 }
 
+// Vertex selection of frame j (Sec. IV-C, Alg. 4; whole warp), out of line: it
+// runs for ~1.5% of frames and keeps its fp64 registers and code out of the
+// main loop.
+static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ Pp, WarpSmem& W, BatchState& B,
+                                                 int j, const m3e_track* tj, const Frame& Fv, uint32_t f0) {
+    const DevParams& P = *Pp;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int ncomb = 0, nneg_out = 0;
+    bool has_vtx = false;
+    if (B.reason[j] == M3E_REASON_NONE) {
+        const int nt = min(B.ntrk[j], P.max_tracks);
+        // charge-sorted index lists, in track order
+        int npos = 0, nneg = 0;
+        for (int i0 = 0; i0 < nt; i0 += 32) {
+            const int i = i0 + lane;
+            const float kap = i < nt ? tj[i].kappa : 0.0f;
+            const bool ispos = i < nt && kap > 0.0f, isneg = i < nt && kap < 0.0f;
+            const unsigned mp = __ballot_sync(0xffffffffu, ispos);
+            const unsigned mn = __ballot_sync(0xffffffffu, isneg);
+            if (ispos) W.vlist[0][npos + __popc(mp & lt_mask)] = (uint8_t)i;
+            if (isneg) W.vlist[1][nneg + __popc(mn & lt_mask)] = (uint8_t)i;
+            npos += __popc(mp);
+            nneg += __popc(mn);
+        }
+        __syncwarp();
+        nneg_out = nneg;
+        if (npos >= 2 && nneg >= 1) {
+            // Alg. 4 phase 1: energy test over (a < b, e) in row-major order
+            const int tot = npos * npos * nneg;
+            for (int base = 0; base < tot; base += 32) {
+                const int t = base + lane;
+                bool pass = false;
+                uint32_t code = 0;
+                if (t < tot) {
+                    const int ia = t / (npos * nneg), rem = t - ia * npos * nneg;
+                    const int ib = rem / nneg, ie = rem - ib * nneg;
+                    if (ia < ib) {
+                        const int a = W.vlist[0][ia], bb = W.vlist[0][ib], e = W.vlist[1][ie];
+                        const double dE = track_energy(P, tj[a].kappa) + track_energy(P, tj[bb].kappa) +
+                                          track_energy(P, tj[e].kappa) - kMuMass;
+                        pass = fabs(dE) <= P.e_window;
+                        code = (uint32_t)a | ((uint32_t)bb << 8) | ((uint32_t)e << 16);
+                    }
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, pass);
+                const int pos = ncomb + __popc(m & lt_mask);
+                if (pass && pos < P.max_combs) W.vcomb[pos] = code;
+                ncomb += __popc(m);
+                if (ncomb > P.max_combs) break;
+            }
+            __syncwarp();
+            if (ncomb > P.max_combs) {
+                ncomb = P.max_combs + 1;
+            } else {
+                // Alg. 4 phase 2: one lane per stored triple
+                double bchi = 1e300;
+                int bidx = 0x7fffffff;
+                VResult bres;
+                bres.pass = 0;
+                for (int c = lane; c < ncomb; c += 32) {
+                    const uint32_t code = W.vcomb[c];
+                    VTrk T[3];
+                    T[0] = make_vtrk(P, tj[code & 255u], Fv);
+                    T[1] = make_vtrk(P, tj[(code >> 8) & 255u], Fv);
+                    T[2] = make_vtrk(P, tj[(code >> 16) & 255u], Fv);
+                    const VResult r = vertex_triple(Pp, T);
+                    if (r.pass && r.chi2 < bchi) { bchi = r.chi2; bidx = c; bres = r; }
+                }
+                // lowest chi2 among passing triples, earliest on ties
+                double wchi = bchi;
+                int widx = bidx;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double oc = __shfl_xor_sync(0xffffffffu, wchi, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, widx, o);
+                    if (oc < wchi || (oc == wchi && oi < widx)) { wchi = oc; widx = oi; }
+                }
+                if (widx != 0x7fffffff) {
+                    has_vtx = true;
+                    if (bidx == widx) {
+                        const uint32_t code = W.vcomb[widx];
+                        m3e_vertex v;
+                        v.frame = f0 + j;
+                        v.track[0] = (uint16_t)(code & 255u);
+                        v.track[1] = (uint16_t)((code >> 8) & 255u);
+                        v.track[2] = (uint16_t)((code >> 16) & 255u);
+                        v.pad = 0;
+                        v.pad2 = 0;
+                        v.x = bres.x; v.y = bres.y; v.z = bres.z;
+                        v.chi2 = bres.chi2;
+                        v.target_dist = (float)bres.tdist;
+                        v.p_total = (float)bres.ptot;
+                        B.vtx[j] = v;
+                    }
+                }
+            }
+        }
+        if (lane == 0) {
+            B.ncomb[j] = ncomb;
+            B.nneg[j] = nneg_out;
+            if (ncomb > P.max_combs) B.reason[j] = M3E_REASON_COMB_OVERFLOW;
+            else if (has_vtx) B.reason[j] = M3E_REASON_VERTEX;
+        }
+    } else if (lane == 0) {
+        B.ncomb[j] = 0;
+    }
+}
+
 // ------------------------------------------------------------------ kernel ----
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
@@ -352,82 +462,86 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
             }
         }
 
-        // -------------------------------------- F: Triplet fit, one lane per candidate
+        // --------- F + T: triplet fit, one lane per candidate, fused with the
+        // per-frame ballot compaction of the accepted tracks (candidate order)
         if constexpr (MODE == kModeFull || MODE == kModeFit) {
-            for (int j = lane; j < nf; j += 32) W.pref[j] = (uint32_t)B.nstored[j];
+            for (int j = lane; j < nf; j += 32) {
+                W.pref[j] = (uint32_t)B.nstored[j];
+                B.ntrk[j] = 0;
+                B.nneg[j] = 0;
+                W.npos[j] = 0;
+            }
             __syncwarp();
             warp_scan(W.pref, nf);
             const int total = (int)W.pref[nf];
-            for (int e = lane; e < total; e += 32) {
-                const int j = find_frame(W.pref, nf, (uint32_t)e);
-                const size_t slot = cfirst + (size_t)j * P.cuts_max + (e - (int)W.pref[j]);
-                const uint32_t pk = cidx[slot];
-                const Frame Fv = frame_view(A, W, buf, j);
-                const FitOut o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, crt[slot]);
-                m3e_fit_record r;
-                r.status = (uint8_t)o.status;
-                r.pad = 0;
-                r.hit3 = o.hit3 < 0 ? (uint16_t)0xFFFF : (uint16_t)o.hit3;
-                r.kappa1 = o.kappa1;
-                r.kappa2 = o.kappa2;
-                r.var1 = o.var1;
-                r.var2 = o.var2;
-                r.kappa = o.kappa;
-                r.chi2 = o.chi2;
-                r.cos_theta01 = o.cth01;
-                r.cx = o.cx;
-                r.cy = o.cy;
-                crec[slot] = r;
+            for (int e0 = 0; e0 < total; e0 += 32) {
+                const int e = e0 + lane;
+                const bool valid = e < total;
+                const int j = valid ? find_frame(W.pref, nf, (uint32_t)e) : kFB;
+                FitOut o;
+                uint32_t pk = 0;
+                size_t slot = 0;
+                o.status = 7;
+                if (valid) {
+                    slot = cfirst + (size_t)j * P.cuts_max + (e - (int)W.pref[j]);
+                    pk = cidx[slot];
+                    const Frame Fv = frame_view(A, W, buf, j);
+                    o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, crt[slot]);
+                }
+                if constexpr (MODE == kModeFit) {   // per-candidate record (stage tap)
+                    if (valid) {
+                        m3e_fit_record r;
+                        r.status = (uint8_t)o.status;
+                        r.pad = 0;
+                        r.hit3 = o.hit3 < 0 ? (uint16_t)0xFFFF : (uint16_t)o.hit3;
+                        r.kappa1 = o.kappa1;
+                        r.kappa2 = o.kappa2;
+                        r.var1 = o.var1;
+                        r.var2 = o.var2;
+                        r.kappa = o.kappa;
+                        r.chi2 = o.chi2;
+                        r.cos_theta01 = o.cth01;
+                        r.cx = o.cx;
+                        r.cy = o.cy;
+                        crec[slot] = r;
+                    }
+                }
+                const bool acc = valid && o.status == 0 && B.reason[j] == M3E_REASON_NONE;
+                const unsigned m_acc = __ballot_sync(0xffffffffu, acc);
+                const unsigned grp = __match_any_sync(0xffffffffu, j);   // lanes of the same frame
+                const int pos = (valid ? B.ntrk[j] : 0) + __popc(m_acc & grp & lt_mask);
+                const bool store = acc && pos < P.max_tracks;
+                if (store) {
+                    m3e_track t;
+                    t.frame = f0 + j;
+                    t.hit[0] = (uint16_t)(pk & 1023u);
+                    t.hit[1] = (uint16_t)((pk >> 10) & 1023u);
+                    t.hit[2] = (uint16_t)((pk >> 20) & 1023u);
+                    t.hit[3] = (uint16_t)o.hit3;
+                    t.kappa = o.kappa;
+                    t.chi2 = o.chi2;
+                    t.cos_theta01 = o.cth01;
+                    t.cx = o.cx;
+                    t.cy = o.cy;
+                    ctrk[tfirst + (size_t)j * P.max_tracks + pos] = t;
+                }
+                const unsigned m_neg = __ballot_sync(0xffffffffu, store && o.kappa < 0.0f);
+                const unsigned m_pos = __ballot_sync(0xffffffffu, store && o.kappa > 0.0f);
+                __syncwarp();
+                if (valid && lane == __ffs(grp) - 1) {   // group leader updates the frame's counters
+                    B.ntrk[j] += __popc(m_acc & grp);
+                    B.nneg[j] += __popc(m_neg & grp);
+                    W.npos[j] += __popc(m_pos & grp);
+                }
+                __syncwarp();
             }
-            __syncwarp();
-
-            // ------------------------- T: per-frame track compaction (ballot / popc)
-            for (int j = 0; j < nf; ++j) {
-                if (B.reason[j] != M3E_REASON_NONE) {
-                    if (lane == 0) { B.ntrk[j] = 0; B.nneg[j] = 0; }
-                    continue;
-                }
-                const int n = B.nstored[j];
-                const size_t cb = cfirst + (size_t)j * P.cuts_max;
-                m3e_track* tj = ctrk + tfirst + (size_t)j * P.max_tracks;
-                int cnt = 0, nneg = 0;
-                for (int i0 = 0; i0 < n; i0 += 32) {
-                    const int i = i0 + lane;
-                    bool acc = false;
-                    m3e_fit_record r;
-                    if (i < n) {
-                        r = crec[cb + i];
-                        acc = r.status == 0;
-                    }
-                    const unsigned m = __ballot_sync(0xffffffffu, acc);
-                    const int pos = cnt + __popc(m & lt_mask);
-                    const bool store = acc && pos < P.max_tracks;
-                    if (store) {
-                        const uint32_t pk = cidx[cb + i];
-                        m3e_track t;
-                        t.frame = f0 + j;
-                        t.hit[0] = (uint16_t)(pk & 1023u);
-                        t.hit[1] = (uint16_t)((pk >> 10) & 1023u);
-                        t.hit[2] = (uint16_t)((pk >> 20) & 1023u);
-                        t.hit[3] = r.hit3;
-                        t.kappa = r.kappa;
-                        t.chi2 = r.chi2;
-                        t.cos_theta01 = r.cos_theta01;
-                        t.cx = r.cx;
-                        t.cy = r.cy;
-                        tj[pos] = t;
-                    }
-                    nneg += __popc(__ballot_sync(0xffffffffu, store && r.kappa < 0.0f));
-                    cnt += __popc(m);
-                }
-                if (lane == 0) {
-                    B.ntrk[j] = min(cnt, P.max_tracks + 1);
-                    if (cnt > P.max_tracks) {
-                        B.reason[j] = M3E_REASON_TRACK_OVERFLOW;
-                        B.nneg[j] = 0;
-                    } else {
-                        B.nneg[j] = nneg;
-                    }
+            for (int j = lane; j < nf; j += 32) {
+                if (B.reason[j] != M3E_REASON_NONE) continue;
+                const int cnt = B.ntrk[j];
+                B.ntrk[j] = min(cnt, P.max_tracks + 1);
+                if (cnt > P.max_tracks) {
+                    B.reason[j] = M3E_REASON_TRACK_OVERFLOW;
+                    B.nneg[j] = 0;
                 }
             }
             __syncwarp();
@@ -450,111 +564,17 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
         // --------------------------------------------- V: vertex selection (fp64)
         if constexpr (MODE == kModeFull || MODE == kModeVertex) {
             for (int j = 0; j < nf; ++j) {
-                int ncomb = 0, nneg_out = 0;
-                bool has_vtx = false;
-                if (B.reason[j] == M3E_REASON_NONE) {
-                    const int nt = min(B.ntrk[j], P.max_tracks);
-                    const m3e_track* tj = ctrk + tfirst + (size_t)j * P.max_tracks;
-                    // charge-sorted index lists, in track order
-                    int npos = 0, nneg = 0;
-                    for (int i0 = 0; i0 < nt; i0 += 32) {
-                        const int i = i0 + lane;
-                        const float kap = i < nt ? tj[i].kappa : 0.0f;
-                        const bool ispos = i < nt && kap > 0.0f, isneg = i < nt && kap < 0.0f;
-                        const unsigned mp = __ballot_sync(0xffffffffu, ispos);
-                        const unsigned mn = __ballot_sync(0xffffffffu, isneg);
-                        if (ispos) W.vlist[0][npos + __popc(mp & lt_mask)] = (uint8_t)i;
-                        if (isneg) W.vlist[1][nneg + __popc(mn & lt_mask)] = (uint8_t)i;
-                        npos += __popc(mp);
-                        nneg += __popc(mn);
+                if constexpr (MODE == kModeFull) {   // charge counts known from F: skip frames without e+e+e-
+                    if (B.reason[j] != M3E_REASON_NONE || W.npos[j] < 2 || B.nneg[j] < 1) {
+                        if (lane == 0) B.ncomb[j] = 0;
+                        continue;
                     }
-                    __syncwarp();
-                    nneg_out = nneg;
-                    if (npos >= 2 && nneg >= 1) {
-                        const Frame Fv = frame_view(A, W, buf, j);
-                        // Alg. 4 phase 1: energy test over (a < b, e) in row-major order
-                        const int tot = npos * npos * nneg;
-                        for (int base = 0; base < tot; base += 32) {
-                            const int t = base + lane;
-                            bool pass = false;
-                            uint32_t code = 0;
-                            if (t < tot) {
-                                const int ia = t / (npos * nneg), rem = t - ia * npos * nneg;
-                                const int ib = rem / nneg, ie = rem - ib * nneg;
-                                if (ia < ib) {
-                                    const int a = W.vlist[0][ia], bb = W.vlist[0][ib], e = W.vlist[1][ie];
-                                    const double dE = track_energy(P, tj[a].kappa) + track_energy(P, tj[bb].kappa) +
-                                                      track_energy(P, tj[e].kappa) - kMuMass;
-                                    pass = fabs(dE) <= P.e_window;
-                                    code = (uint32_t)a | ((uint32_t)bb << 8) | ((uint32_t)e << 16);
-                                }
-                            }
-                            const unsigned m = __ballot_sync(0xffffffffu, pass);
-                            const int pos = ncomb + __popc(m & lt_mask);
-                            if (pass && pos < P.max_combs) W.vcomb[pos] = code;
-                            ncomb += __popc(m);
-                            if (ncomb > P.max_combs) break;
-                        }
-                        __syncwarp();
-                        if (ncomb > P.max_combs) {
-                            ncomb = P.max_combs + 1;
-                        } else {
-                            // Alg. 4 phase 2: one lane per stored triple
-                            double bchi = 1e300;
-                            int bidx = 0x7fffffff;
-                            VResult bres;
-                            bres.pass = 0;
-                            for (int c = lane; c < ncomb; c += 32) {
-                                const uint32_t code = W.vcomb[c];
-                                VTrk T[3];
-                                T[0] = make_vtrk(P, tj[code & 255u], Fv);
-                                T[1] = make_vtrk(P, tj[(code >> 8) & 255u], Fv);
-                                T[2] = make_vtrk(P, tj[(code >> 16) & 255u], Fv);
-                                const VResult r = vertex_triple(&S.P, T);
-                                if (r.pass && r.chi2 < bchi) { bchi = r.chi2; bidx = c; bres = r; }
-                            }
-                            // lowest chi2 among passing triples, earliest on ties
-                            double wchi = bchi;
-                            int widx = bidx;
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) {
-                                const double oc = __shfl_xor_sync(0xffffffffu, wchi, o);
-                                const int oi = __shfl_xor_sync(0xffffffffu, widx, o);
-                                if (oc < wchi || (oc == wchi && oi < widx)) { wchi = oc; widx = oi; }
-                            }
-                            if (widx != 0x7fffffff) {
-                                has_vtx = true;
-                                if (bidx == widx) {
-                                    const uint32_t code = W.vcomb[widx];
-                                    m3e_vertex v;
-                                    v.frame = f0 + j;
-                                    v.track[0] = (uint16_t)(code & 255u);
-                                    v.track[1] = (uint16_t)((code >> 8) & 255u);
-                                    v.track[2] = (uint16_t)((code >> 16) & 255u);
-                                    v.pad = 0;
-                                    v.pad2 = 0;
-                                    v.x = bres.x; v.y = bres.y; v.z = bres.z;
-                                    v.chi2 = bres.chi2;
-                                    v.target_dist = (float)bres.tdist;
-                                    v.p_total = (float)bres.ptot;
-                                    B.vtx[j] = v;
-                                }
-                            }
-                        }
-                    }
-                    if (lane == 0) {
-                        B.ncomb[j] = ncomb;
-                        B.nneg[j] = nneg_out;
-                        if (ncomb > P.max_combs) B.reason[j] = M3E_REASON_COMB_OVERFLOW;
-                        else if (has_vtx) B.reason[j] = M3E_REASON_VERTEX;
-                    }
-                } else if (lane == 0) {
-                    B.ncomb[j] = 0;
                 }
+                const Frame Fv = frame_view(A, W, buf, j);
+                vertex_frame(&S.P, W, B, j, ctrk + tfirst + (size_t)j * P.max_tracks, Fv, f0);
                 __syncwarp();
             }
         }
-
         if constexpr (MODE == kModeVertex) {
             for (int j = lane; j < nf; j += 32) {
                 m3e_frame_out fo;
@@ -656,14 +676,11 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                 A.bstat[b] = bs;
             }
             // run summary (shared-memory accumulators, flushed once per CTA)
-            uint32_t kept_r[6] = {0, 0, 0, 0, 0, 0};
-            uint32_t cand = 0;
-            for (int j = lane; j < nf; j += 32) {
-                kept_r[B.reason[j]] += 1;
-                cand += B.nstored[j];
-            }
-            for (int r = 0; r < 6; ++r) kept_r[r] = warp_sum(kept_r[r]);
-            cand = warp_sum(cand);
+            uint32_t kept_r[6];
+            const int rj = lane < nf ? B.reason[lane] : -1;   // nf <= kFB <= 32
+#pragma unroll
+            for (int r = 0; r < 6; ++r) kept_r[r] = __popc(__ballot_sync(0xffffffffu, rj == r));
+            const uint32_t cand = warp_sum(lane < nf ? (uint32_t)B.nstored[lane] : 0u);
             if (lane == 0) {
                 atomicAdd(&S.s_frames, (unsigned long long)nf);
                 atomicAdd(&S.s_trk, (unsigned long long)nt);
