@@ -185,7 +185,9 @@ def main():
     H = len(d["x"])
     frames = m3e.DeviceFrames(d, device=dev)
     ctx = m3e.Context(local)
-    res = m3e.Result(F, H, track_capacity=12 * F, kept_capacity=max(1024, F // 20), device=dev)
+    trk_cap = (64 if a.workload.startswith("phase2") else 12) * F
+    kept_cap = F if a.workload.startswith("phase2") else max(1024, F // 20)
+    res = m3e.Result(F, H, track_capacity=trk_cap, kept_capacity=kept_cap, device=dev)
     stream = torch.cuda.Stream(device=dev)
     in_bytes = 12 * H + 16 * F + 4
 

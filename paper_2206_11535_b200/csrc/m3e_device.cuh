@@ -199,7 +199,7 @@ M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2
     T.q = rtc > 0.0f ? 1 : -1;
     const float r = fabsf(rtc);
     const float ir = rcp(r);
-    float th[2], sth0 = 0.0f, dth[2];
+    float sthv[2], cthv[2], sth0 = 0.0f, dth[2];
     const float3 H[3] = {h0, h1, h2};
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
@@ -218,7 +218,8 @@ M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2
         const float dphi = 2.0f * ikc * ikc * ikc * rcp(r * r * ch * rcp(s) + 2.0f * z * z * iphc * iphc * iphc);
         // dtheta/dk = -z (Phi - k Phi') / (Phi^2 sin theta)
         dth[a] = -z * (phc - kc * dphi) * iphc * iphc * rcp(sth);
-        th[a] = atan2f(sth, cth);
+        sthv[a] = sth;
+        cthv[a] = cth;
         if (a == 0) sth0 = sth;
         T.phc[a] = phc;
         T.kc[a] = kc;
@@ -229,7 +230,9 @@ M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2
     T.b_phi = 0.5f * T.q * (T.dphi[0] + T.dphi[1]);
     T.al_phi = 0.25f * T.q * dk * (T.dphi[0] - T.dphi[1]);
     T.b_th = dth[1] - dth[0];
-    T.al_th = (th[1] - th[0]) - 0.5f * dk * (dth[1] + dth[0]);
+    // theta_12 - theta_01 (both in (0, pi)) with one atan2
+    const float dtheta = atan2f(sthv[1] * cthv[0] - cthv[1] * sthv[0], cthv[1] * cthv[0] + sthv[1] * sthv[0]);
+    T.al_th = dtheta - 0.5f * dk * (dth[1] + dth[0]);
     const float sig = P.chl * T.kref;
     T.w_th = rcp(sig * sig);
     T.w_phi = sth0 * sth0 * T.w_th;
@@ -275,8 +278,7 @@ M3E_HD_CALL bool arc_phi(float d, float z, float k, float start, float& phi) {
 // Sec. IV-B-2 "Using this preliminary helix, the hit position in the fourth
 // layer is estimated" (R9): continue the arc h1 -> h2 of curvature k past h2 to
 // its first crossing of the layer-3 cylinder.
-M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet& T,
-                                            float3& out) {
+M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet& T, float3& out) {
     const float k = T.khat;
     const float dx = h2.x - h1.x, dy = h2.y - h1.y, z = h2.z - h1.z;
     const float d = sqrtf(dx * dx + dy * dy);
@@ -284,29 +286,35 @@ M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet&
     if (!arc_phi(d, z, k, T.phc[1] + T.dphi[1] * (k - T.kc[1]), phi)) return false;
     const float ik = rcp(k);
     const float cth = fminf(fmaxf(z * k * rcp(phi), -1.0f), 1.0f);
-    const float sth = sqrtf(1.0f - cth * cth);
-    const float psi = atan2f(dy, dx) - T.q * 0.5f * phi;     // heading at h2
-    const float rt = sth * ik;
-    float sp, cp;
-    sincosf(psi, &sp, &cp);
-    const float cx = h2.x + T.q * rt * sp, cy = h2.y - T.q * rt * cp;
-    const float C = sqrtf(cx * cx + cy * cy);
+    const float rt = sqrtf(1.0f - cth * cth) * ik;
+    // heading at h2 = chord direction turned by -q phi/2 (a clockwise arc turns by -phi)
+    float sh, ch;
+    sincos_half(0.5f * phi, sh, ch);
+    const float id = rcp(d), ux = dx * id, uy = dy * id;
+    const float ex = ux * ch + T.q * uy * sh, ey = uy * ch - T.q * ux * sh;
+    // centre: clockwise (q = +1) to the right of the heading
+    const float cx = h2.x + T.q * rt * ey, cy = h2.y - T.q * rt * ex;
+    const float C2 = cx * cx + cy * cy, C = sqrtf(C2);
     if (C == 0.0f) return false;
-    const float arg = (P.R3sq - C * C - rt * rt) * rcp(2.0f * rt * C);
-    if (arg > 1.0f || arg < -1.0f) return false;
-    const float phic = atan2f(cy, cx), da = acosf(arg);
-    const float phi0 = atan2f(h2.y - cy, h2.x - cx);
-    float best = 1e30f;
+    // crossings of |p| = r3 and |p - c| = rt: p = a c^ +- hh n^ (no trigonometry)
+    const float iC = rcp(C);
+    const float a = (P.R3sq - rt * rt + C2) * 0.5f * iC;
+    const float hh2 = P.R3sq - a * a;
+    if (hh2 < 0.0f) return false;                    // the helix never reaches layer 3
+    const float hh = sqrtf(hh2);
+    const float cux = cx * iC, cuy = cy * iC;
+    const float ax = h2.x - cx, ay = h2.y - cy;
+    float best = 1e30f, bx = 0.0f, by = 0.0f;
 #pragma unroll
     for (int s = -1; s <= 1; s += 2) {
-        float t = T.q * (phi0 - (phic + s * da));
-        t -= 2.0f * kPiF * floorf(t * (0.5f / kPiF));   // to [0, 2 pi)
-        if (t > 0.0f && t < best) best = t;
+        const float px = a * cux - s * hh * cuy, py = a * cuy + s * hh * cux;
+        const float qx = px - cx, qy = py - cy;
+        // turning angle from h2 to p in the direction of motion, in [0, 2 pi)
+        float t = -T.q * atan2f(ax * qy - ay * qx, ax * qx + ay * qy);
+        if (t < 0.0f) t += 2.0f * kPiF;
+        if (t > 0.0f && t < best) { best = t; bx = px; by = py; }
     }
-    const float ph = phi0 - T.q * best;
-    float s2, c2;
-    sincosf(ph, &s2, &c2);
-    out = make_float3(cx + rt * c2, cy + rt * s2, h2.z + cth * ik * best);
+    out = make_float3(bx, by, h2.z + cth * ik * best);
     return true;
 }
 

@@ -90,26 +90,33 @@ struct BatchState {
     m3e_vertex vtx[kFB];
 };
 
+// A warp-batch computes for ~10^5 cycles against a ~10^3-cycle bulk-copy latency,
+// so one staging buffer per warp suffices; the freed shared memory keeps L1 large
+// and holds the warp-batch's candidates instead.
+constexpr int kNBuf = 1;
+constexpr int kCandSmem = 256;   // candidates of a warp-batch kept in shared memory
+
 struct __align__(16) WarpSmem {
-    float hx[2][kHCap];
-    float hy[2][kHCap];
-    float hz[2][kHCap];
-    uint32_t offs[2][4 * kFB + 4];
-    uint64_t bar[2];
-    uint32_t b_batch[2], b_winlo[2], b_winhi[2];
+    float hx[kNBuf][kHCap];
+    float hy[kNBuf][kHCap];
+    float hz[kNBuf][kHCap];
+    uint32_t offs[kNBuf][4 * kFB + 4];
+    uint64_t bar[kNBuf];
+    uint32_t b_batch[kNBuf], b_winlo[kNBuf], b_winhi[kNBuf];
+    uint32_t cidx[kCandSmem];        // candidates (flat warp-batch index < kCandSmem), FULL mode
+    float crt[kCandSmem];
     BatchState st;
     uint32_t pref[kFB + 1];          // candidates: exclusive prefix
     int npos[kFB];                   // stored positive tracks per frame (vertex gate)
     uint32_t q[64];                  // Delta-lambda survivors (selection FIFO)
     uint8_t vlist[2][kMaxTracksCap];
     uint32_t vcomb[kMaxCombsCap];
+    uint32_t acc[12];                // run summary: kept_by_reason[6], cand, frames, tracks, hits, overflow
 };
 
 struct Smem {
     WarpSmem w[kWarps];
     DevParams P;   // copy for the out-of-line vertex routine (no address of a kernel parameter is taken)
-    unsigned long long s_kept[6], s_cand, s_trk, s_hits, s_vtx, s_frames;
-    int s_overflow;
 };
 
 size_t smem_bytes() { return sizeof(Smem); }
@@ -350,22 +357,18 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
     WarpSmem& W = S.w[warp];
     const size_t gwarp = (size_t)blockIdx.x * kWarps + warp;
 
-    if (tid == 0) {
-        S.P = A.P;
-        for (int i = 0; i < 6; ++i) S.s_kept[i] = 0;
-        S.s_cand = S.s_trk = S.s_hits = S.s_vtx = S.s_frames = 0;
-        S.s_overflow = 0;
-    }
+    if (tid == 0) S.P = A.P;
     if (lane == 0) {
-        mbar_init(&W.bar[0], 1);
-        mbar_init(&W.bar[1], 1);
+        for (int i = 0; i < kNBuf; ++i) mbar_init(&W.bar[i], 1);
         fence_mbar_init();
     }
     __syncthreads();   // the only CTA barrier before the final summary flush
     if (lane == 0) issue_load(A, W, 0, atomicAdd(A.ticket, 1u));
     __syncwarp();
     int buf = 0;
-    uint32_t phase0 = 0u, phase1 = 0u;
+    uint32_t phase[kNBuf] = {};
+    if (lane < 12) W.acc[lane] = 0u;   // run summary of this warp (shared memory, lane 0 updates)
+    __syncwarp();
 
     // candidate / track slots: per-warp scratch (FULL) or the caller's fixed slots
     // (stage modes)
@@ -388,9 +391,9 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
     for (;;) {
         const uint32_t b = W.b_batch[buf];
         if (b >= A.nbatch) break;
-        if (lane == 0) issue_load(A, W, buf ^ 1, atomicAdd(A.ticket, 1u));
-        if (buf == 0) { mbar_wait(&W.bar[0], phase0); phase0 ^= 1u; }
-        else { mbar_wait(&W.bar[1], phase1); phase1 ^= 1u; }
+        if (kNBuf == 2 && lane == 0) issue_load(A, W, buf ^ 1, atomicAdd(A.ticket, 1u));
+        mbar_wait(&W.bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
 
         BatchState& B = W.st;
         const uint32_t f0 = b * (uint32_t)A.fb;
@@ -401,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
 
         // ---------------------------------------------------- S: Selection Cuts
         if constexpr (MODE == kModeFull || MODE == kModeSelect) {
+            uint32_t cbase = 0;   // FULL: flat candidate index of frame j's first candidate
             for (int j = 0; j < nf; ++j) {
                 const Frame Fv = frame_view(A, W, buf, j);
                 const bool inval = Fv.n[0] > kMaxLayerHits || Fv.n[1] > kMaxLayerHits ||
@@ -409,18 +413,32 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                 if (!inval) {
                     uint32_t* ci = cidx + cfirst + (size_t)j * P.cuts_max;
                     float* cr = crt + cfirst + (size_t)j * P.cuts_max;
-                    count = select_frame_warp(P, Fv, W.q, [&](int pos, uint32_t packed, float rt) {
-                        ci[pos] = packed;
-                        cr[pos] = rt;
-                    });
+                    auto emit = [&](int pos, uint32_t packed, float rt) {
+                        if constexpr (MODE == kModeFull) {
+                            const uint32_t fi = cbase + (uint32_t)pos;
+                            if (fi < (uint32_t)kCandSmem) {
+                                W.cidx[fi] = packed;
+                                W.crt[fi] = rt;
+                            } else {
+                                cidx[fi] = packed;
+                                crt[fi] = rt;
+                            }
+                        } else {
+                            ci[pos] = packed;
+                            cr[pos] = rt;
+                        }
+                    };
+                    count = select_frame_warp(P, Fv, W.q, emit);
+                    __syncwarp();
                 }
+                const int r = inval ? M3E_REASON_INVALID
+                                    : (count > P.cuts_max ? M3E_REASON_TRIPLET_OVERFLOW : M3E_REASON_NONE);
                 if (lane == 0) {
                     B.ncand[j] = count;
-                    const int r = inval ? M3E_REASON_INVALID
-                                        : (count > P.cuts_max ? M3E_REASON_TRIPLET_OVERFLOW : M3E_REASON_NONE);
                     B.reason[j] = r;
                     B.nstored[j] = r == M3E_REASON_NONE ? count : 0;
                 }
+                cbase += r == M3E_REASON_NONE ? (uint32_t)count : 0u;
             }
         } else if constexpr (MODE == kModeFit) {
             for (int j = lane; j < nf; j += 32) {
@@ -483,10 +501,23 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                 size_t slot = 0;
                 o.status = 7;
                 if (valid) {
-                    slot = cfirst + (size_t)j * P.cuts_max + (e - (int)W.pref[j]);
-                    pk = cidx[slot];
+                    float rt;
+                    if constexpr (MODE == kModeFull) {   // flat warp-batch candidate index
+                        slot = (size_t)e;
+                        if (e < kCandSmem) {
+                            pk = W.cidx[e];
+                            rt = W.crt[e];
+                        } else {
+                            pk = cidx[e];
+                            rt = crt[e];
+                        }
+                    } else {
+                        slot = cfirst + (size_t)j * P.cuts_max + (e - (int)W.pref[j]);
+                        pk = cidx[slot];
+                        rt = crt[slot];
+                    }
                     const Frame Fv = frame_view(A, W, buf, j);
-                    o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, crt[slot]);
+                    o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
                 }
                 if constexpr (MODE == kModeFit) {   // per-candidate record (stage tap)
                     if (valid) {
@@ -675,39 +706,43 @@ __global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
                 bs.pad[0] = bs.pad[1] = 0;
                 A.bstat[b] = bs;
             }
-            // run summary (shared-memory accumulators, flushed once per CTA)
-            uint32_t kept_r[6];
+            // run summary: per-warp counters in shared memory, flushed once at the end
             const int rj = lane < nf ? B.reason[lane] : -1;   // nf <= kFB <= 32
+            uint32_t kr[6];
 #pragma unroll
-            for (int r = 0; r < 6; ++r) kept_r[r] = __popc(__ballot_sync(0xffffffffu, rj == r));
+            for (int r = 0; r < 6; ++r) kr[r] = __popc(__ballot_sync(0xffffffffu, rj == r));
             const uint32_t cand = warp_sum(lane < nf ? (uint32_t)B.nstored[lane] : 0u);
             if (lane == 0) {
-                atomicAdd(&S.s_frames, (unsigned long long)nf);
-                atomicAdd(&S.s_trk, (unsigned long long)nt);
-                atomicAdd(&S.s_hits, (unsigned long long)B.o_hits[nf]);
-                atomicAdd(&S.s_cand, (unsigned long long)cand);
-                atomicAdd(&S.s_vtx, (unsigned long long)kept_r[M3E_REASON_VERTEX]);
-                for (int r = 0; r < 6; ++r)
-                    if (kept_r[r]) atomicAdd(&S.s_kept[r], (unsigned long long)kept_r[r]);
+                for (int r = 0; r < 6; ++r) W.acc[r] += kr[r];
+                W.acc[6] += cand;
+                W.acc[7] += nf;
+                W.acc[8] += nt;
+                W.acc[9] += B.o_hits[nf];
             }
-            if (__any_sync(0xffffffffu, overflow) && lane == 0) S.s_overflow = 1;
+            if (__any_sync(0xffffffffu, overflow) && lane == 0) W.acc[10] = 1u;
         }
         __syncwarp();
-        buf ^= 1;
+        if constexpr (kNBuf == 2) {
+            buf ^= 1;
+        } else if (lane == 0) {
+            issue_load(A, W, 0, atomicAdd(A.ticket, 1u));
+        }
+        __syncwarp();
     }
 
     if constexpr (kOut) {
-        __syncthreads();
-        if (tid == 0 && A.out.summary) {
+        __syncwarp();
+        if (lane == 0 && A.out.summary) {
             m3e_summary* sm = A.out.summary;
-            atomicAdd((unsigned long long*)&sm->frames, S.s_frames);
+            typedef unsigned long long u64;
+            if (W.acc[7]) atomicAdd((u64*)&sm->frames, (u64)W.acc[7]);
             for (int i = 0; i < 6; ++i)
-                if (S.s_kept[i]) atomicAdd((unsigned long long*)&sm->kept_by_reason[i], S.s_kept[i]);
-            atomicAdd((unsigned long long*)&sm->candidates, S.s_cand);
-            atomicAdd((unsigned long long*)&sm->tracks, S.s_trk);
-            atomicAdd((unsigned long long*)&sm->kept_hits, S.s_hits);
-            atomicAdd((unsigned long long*)&sm->vertices, S.s_vtx);
-            if (S.s_overflow) atomicExch((unsigned long long*)&sm->overflow, 1ull);
+                if (W.acc[i]) atomicAdd((u64*)&sm->kept_by_reason[i], (u64)W.acc[i]);
+            if (W.acc[6]) atomicAdd((u64*)&sm->candidates, (u64)W.acc[6]);
+            if (W.acc[8]) atomicAdd((u64*)&sm->tracks, (u64)W.acc[8]);
+            if (W.acc[9]) atomicAdd((u64*)&sm->kept_hits, (u64)W.acc[9]);
+            if (W.acc[M3E_REASON_VERTEX]) atomicAdd((u64*)&sm->vertices, (u64)W.acc[M3E_REASON_VERTEX]);
+            if (W.acc[10]) atomicExch((u64*)&sm->overflow, 1ull);
         }
     }
 }

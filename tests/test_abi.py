@@ -62,3 +62,14 @@ def test_product_package_does_not_import_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert "import oracle" not in txt and "m3e_oracle" not in txt and "or_params" not in txt, fn
+
+
+def test_library_has_no_unresolved_internal_symbols():
+    """Every C++ symbol of the library is defined in it (a shared library links
+    with undefined symbols; this catches a missing kernel launcher on CPU)."""
+    import subprocess
+    from paper_2206_11535_b200 import m3e
+    out = subprocess.run(["nm", "-D", "--undefined-only", m3e.LIB_PATH], capture_output=True, text=True).stdout
+    bad = [l for l in out.split("\n") if "m3e" in l]
+    assert not bad, bad
+    ctypes.CDLL(m3e.LIB_PATH, mode=os.RTLD_NOW)
