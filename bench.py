@@ -48,7 +48,8 @@ def gbps_equiv(frames_per_s: float) -> float:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the timed
+    region (one `nvidia-smi -lms 50` process, started before and stopped after)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -60,26 +61,28 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
-
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        import tempfile
+        self._f = tempfile.TemporaryFile(mode="w+")
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "50"], stdout=self._f,
+                                       stderr=subprocess.DEVNULL)
+        except OSError:
+            self._p = None
+        time.sleep(0.3)   # nvidia-smi start-up before the timed region
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join()
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                self._p.wait(5)
+            except subprocess.TimeoutExpired:
+                self._p.kill()
+        self._f.seek(0)
+        self.rows = [[c.strip() for c in l.split(",")] for l in self._f.read().splitlines() if l.strip()]
+        self._f.close()
 
     def summary(self):
         if not self.rows:
@@ -90,6 +93,20 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+def load_traffic(workload: str, frames: int, seed: int):
+    """DRAM bytes per filter-kernel launch from the committed ncu capture of this
+    exact configuration (profiles/*_bench_traffic.json), else None."""
+    import glob
+    for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_bench_traffic.json")), reverse=True):
+        try:
+            t = json.load(open(fn))
+        except Exception:
+            continue
+        if t.get("workload") == workload and t.get("frames") == frames and t.get("seed") == seed:
+            return t["dram_read_bytes"] + t["dram_write_bytes"]
+    return None
 
 
 def load_peaks():
@@ -150,7 +167,7 @@ def run_reference(a, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--frames", type=int, default=int(PHASE1_FRAMES_PER_S), help="frames per GPU per step")
@@ -197,6 +214,7 @@ def main():
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize(dev)
+    ctx.set_timing(True)   # CUDA events around each of the two kernels, on the launch stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     if world > 1:
         dist.barrier()
@@ -211,6 +229,7 @@ def main():
         dist.barrier()
     ms = [s.elapsed_time(e) for s, e in ev]
     ms_step = statistics.mean(ms)
+    ms_filter, ms_pack = ctx.kernel_times()
     sm = res.summary_np()
     kept = int(sum(sm["kept_by_reason"][1:]))
     assert int(sm["frames"]) == F and not int(sm["overflow"]), "output capacity exceeded"
@@ -286,7 +305,7 @@ def main():
         # dominant (only) kernel: filter_kernel<FULL>; algorithmic bytes per launch =
         # input hit stream + per-frame outputs + tracks + packed kept frames
         alg_bytes = in_bytes + out_bytes
-        achieved = alg_bytes / (ms_step / 1e3) / 1e9
+        achieved = alg_bytes / (ms_filter / 1e3) / 1e9
         clocks = clk.summary()
         line = {
             "metric": METRIC, "value": round(gbps_equiv(fps), 3), "unit": "Gbps", "n_gpus": world,
@@ -306,10 +325,12 @@ def main():
                        "l2": "inputs (%.2f GB) >> 126 MB L2, no flush needed" % (in_bytes / 1e9),
                        "parallelism": f"frame-sharded dp{world}", "generation_s": round(t_gen, 1)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "m3e::filter_kernel<0> (one launch per step)",
+                         "frac": round(achieved / peak, 4),
+                         "traffic": load_traffic(a.workload, F, a.seed), "peak_kind": peak_kind,
+                         "kernel": "m3e::filter_kernel<0>", "kernel_ms": round(ms_filter, 4),
+                         "share_of_step": round(ms_filter / ms_step, 4), "pack_kernel_ms": round(ms_pack, 4),
                          "algorithmic_bytes_per_launch": int(alg_bytes)},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": a.steps, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * a.steps, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

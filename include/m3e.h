@@ -155,6 +155,12 @@ int m3e_create(m3e_context** ctx, int device, uint64_t max_frames, uint64_t max_
 int m3e_destroy(m3e_context* ctx);
 /* Bytes of device workspace the context holds (informational). */
 uint64_t m3e_workspace_bytes(const m3e_context* ctx);
+/* Kernel timing: when enabled, every m3e_filter call records CUDA events on its
+ * stream around each of its two kernels (up to 1024 calls); m3e_kernel_times()
+ * waits for them and returns the MEAN durations in ms over those calls
+ * (ms[0] = filter kernel, ms[1] = pack kernel), then resets the record. */
+int m3e_set_timing(m3e_context* ctx, int enable);
+int m3e_kernel_times(m3e_context* ctx, float ms[2]);
 
 /* Full hot path on device-resident input (the call bench.py times):
  * select -> fit -> vertex -> pack for frames [0, F).  Outputs [dev]. */

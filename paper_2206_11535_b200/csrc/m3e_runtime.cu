@@ -86,6 +86,9 @@ struct m3e_context {
     cudaStream_t st[2] = {nullptr, nullptr};
     Chunk ch[2];
     uint64_t chunk_frames = 0;
+    bool timing = false;
+    std::vector<cudaEvent_t> tev;   // 3 events per timed m3e_filter call
+    size_t tev_used = 0;
 };
 
 namespace {
@@ -284,11 +287,19 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     }
     CK(cudaMemsetAsync(w.ticket, 0, 4 * sizeof(uint32_t), s));
     if (a.out.summary) CK(cudaMemsetAsync(a.out.summary, 0, sizeof(m3e_summary), s));
+    const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + 3 <= ctx->tev.size();
+    cudaEvent_t* ev = tm ? &ctx->tev[ctx->tev_used] : nullptr;
+    if (tm) CK(cudaEventRecord(ev[0], s));
     CK(launch_filter(mode, a, grid, s));
+    if (tm) CK(cudaEventRecord(ev[1], s));
     if (packs) {
         const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
         const int pgrid = (int)std::min<uint64_t>(ntiles, (uint64_t)ctx->sms * 8);
         CK(launch_pack(a, pgrid, s));
+    }
+    if (tm) {
+        CK(cudaEventRecord(ev[2], s));
+        ctx->tev_used += 3;
     }
     return M3E_OK;
 }
@@ -333,11 +344,43 @@ int m3e_destroy(m3e_context* c) {
         free_chunk(c->ch[i]);
         if (c->st[i]) cudaStreamDestroy(c->st[i]);
     }
+    for (auto& e : c->tev) cudaEventDestroy(e);
     delete c;
     return M3E_OK;
 }
 
 uint64_t m3e_workspace_bytes(const m3e_context* c) { return c ? c->ws[0].bytes + c->ws[1].bytes : 0; }
+
+int m3e_set_timing(m3e_context* c, int enable) {
+    if (!c) return fail(M3E_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    CK(cudaSetDevice(c->device));
+    if (enable && c->tev.empty()) {
+        c->tev.resize(3 * 1024);   // up to 1024 timed calls between two m3e_kernel_times()
+        for (auto& e : c->tev) CK(cudaEventCreate(&e));
+    }
+    c->timing = enable != 0;
+    c->tev_used = 0;
+    return M3E_OK;
+}
+
+int m3e_kernel_times(m3e_context* c, float ms[2]) {
+    if (!c || !ms) return fail(M3E_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (c->tev_used == 0) return fail(M3E_ERR_INVALID_ARGUMENT, "no timed call since the last reset");
+    double a = 0, b = 0;
+    const size_t n = c->tev_used / 3;
+    for (size_t i = 0; i < n; ++i) {
+        float x = 0, y = 0;
+        CK(cudaEventSynchronize(c->tev[3 * i + 2]));
+        CK(cudaEventElapsedTime(&x, c->tev[3 * i], c->tev[3 * i + 1]));
+        CK(cudaEventElapsedTime(&y, c->tev[3 * i + 1], c->tev[3 * i + 2]));
+        a += x;
+        b += y;
+    }
+    ms[0] = (float)(a / n);
+    ms[1] = (float)(b / n);
+    c->tev_used = 0;
+    return M3E_OK;
+}
 
 int m3e_filter(m3e_context* ctx, const m3e_params* p, const float* x, const float* y, const float* z,
                const uint32_t* offsets, uint64_t F, uint64_t H, const m3e_outputs* out, void* stream) {

@@ -75,6 +75,8 @@ def lib():
         L.m3e_destroy.argtypes = [_vp]
         L.m3e_workspace_bytes.restype = _u64
         L.m3e_workspace_bytes.argtypes = [_vp]
+        L.m3e_set_timing.argtypes = [_vp, ctypes.c_int]
+        L.m3e_kernel_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_float)]
         P = ctypes.POINTER(Params)
         O = ctypes.POINTER(Outputs)
         L.m3e_filter.argtypes = [_vp, P, _vp, _vp, _vp, _vp, _u64, _u64, O, _vp]
@@ -89,6 +91,7 @@ def lib():
 
 # names of every symbol include/m3e.h declares (checked by the CPU tests)
 EXPORTED = ["m3e_version", "m3e_last_error", "m3e_create", "m3e_destroy", "m3e_workspace_bytes",
+            "m3e_set_timing", "m3e_kernel_times",
             "m3e_filter", "m3e_filter_host", "m3e_select_triplets", "m3e_fit_tracks",
             "m3e_vertex_select", "m3e_pack_frames"]
 
@@ -155,6 +158,15 @@ class Context:
 
     def workspace_bytes(self) -> int:
         return int(lib().m3e_workspace_bytes(self._h))
+
+    def set_timing(self, enable: bool = True):
+        _check(lib().m3e_set_timing(self._h, int(enable)))
+
+    def kernel_times(self):
+        """(filter kernel ms, pack kernel ms) of the last m3e_filter call."""
+        ms = (ctypes.c_float * 2)()
+        _check(lib().m3e_kernel_times(self._h, ms))
+        return float(ms[0]), float(ms[1])
 
 
 def make_outputs(**kw) -> Outputs:
