@@ -129,11 +129,15 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
     const long long total = (long long)n0 * n1 * n2;
     if (total == 0) return 0;
     const unsigned lt_mask = (1u << lane) - 1u;
-    // mixed-radix digits of the lane's first combination and of the step 32
+    // mixed-radix digits of the lane's first combination and of the step 32; the
+    // quotients of x < 64 by n are floor((x + 0.5) / n): >= 0.5/n away from an
+    // integer, far above the 1-ulp error of rcp (no integer division)
     const int n12 = n1 * n2;
-    int i0 = lane / n12, rem = lane - i0 * n12;
-    int i1 = rem / n2, i2 = rem - i1 * n2;
-    const int a = 32 / n12, r32 = 32 - a * n12, b = r32 / n2, c = r32 - b * n2;
+    const float in12 = rcp((float)n12), in2 = rcp((float)n2);
+    int i0 = (int)(((float)lane + 0.5f) * in12), rem = lane - i0 * n12;
+    int i1 = (int)(((float)rem + 0.5f) * in2), i2 = rem - i1 * n2;
+    const int a = (int)(32.5f * in12), r32 = 32 - a * n12;
+    const int b = (int)(((float)r32 + 0.5f) * in2), c = r32 - b * n2;
     int count = 0, qn = 0;
     // test q[0..n) (n <= 32) for the remaining cuts; true once the frame overflows
     auto drain = [&](int n) -> bool {

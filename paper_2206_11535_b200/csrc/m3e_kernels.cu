@@ -27,6 +27,10 @@
 #include "m3e_device.cuh"
 #include "m3e_kernels.h"
 
+#ifndef M3E_MIN_BLOCKS
+#define M3E_MIN_BLOCKS 3   // CTAs per SM the register allocation targets (80 regs: 24 warps/SM)
+#endif
+
 namespace m3e {
 
 // ------------------------------------------------------------ PTX helpers ----
@@ -347,7 +351,7 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
 
 // ------------------------------------------------------------------ kernel ----
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2) filter_kernel(const KArgs A) {
+__global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const KArgs A) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
