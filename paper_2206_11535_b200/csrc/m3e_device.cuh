@@ -180,6 +180,169 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
     return count;
 }
 
+// Where a selected candidate goes: flat index base + pos; below `split` into
+// the shared-memory array (s*), else into the global array (g*).
+struct CandSink {
+    uint32_t* si;
+    float* sr;
+    uint32_t* gi;
+    float* gr;
+    uint32_t base, split;
+    __device__ __forceinline__ void put(int pos, uint32_t packed, float rt) const {
+        const uint32_t fi = base + (uint32_t)pos;
+        if (fi < split) { si[fi] = packed; sr[fi] = rt; }
+        else { gi[fi] = packed; gr[fi] = rt; }
+    }
+};
+
+__device__ __forceinline__ bool pass_rt(const DevParams& P, const Frame& F, int i0, int i1, int i2, float& rt) {
+    const int g0 = F.s[0] + i0, g1 = F.s[1] + i1, g2 = F.s[2] + i2;
+    rt = circle_radius(make_float3(F.x[g0], F.y[g0], 0.0f), make_float3(F.x[g1], F.y[g1], 0.0f),
+                       make_float3(F.x[g2], F.y[g2], 0.0f));
+    const float ar = fabsf(rt);
+    return ar >= P.rt_min && ar <= P.rt_max;
+}
+
+// ballot-compact the pairs (ia in layer la, ib in layer lb) passing cos Phi >= cmin
+// in row-major order (ia outer), with t = (z_b - z_a) / (r_b - r_a); returns the
+// count (> cap: overflow, lists incomplete)
+__device__ __forceinline__ int pair_list(const Frame& F, int la, int lb, float inv_rr, float cmin, float inv_dr,
+                                         uint32_t* lst, float* tv, int cap) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int na = F.n[la], nb = F.n[lb];
+    const int tot = na * nb;
+    const float inb = rcp((float)nb);   // quotients of x < 64 by nb, as in select_frame_warp
+    int ia = (int)(((float)lane + 0.5f) * inb), ib = lane - ia * nb;
+    const int sa = (int)(32.5f * inb), sb = 32 - sa * nb;
+    int cnt = 0;
+    for (int base = 0; base < tot; base += 32) {
+        bool pass = false;
+        float t = 0.0f;
+        if (ia < na) {
+            const int ga = F.s[la] + ia, gb = F.s[lb] + ib;
+            pass = (F.x[ga] * F.x[gb] + F.y[ga] * F.y[gb]) * inv_rr >= cmin;
+            t = (F.z[gb] - F.z[ga]) * inv_dr;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        const int pos = cnt + __popc(m & lt_mask);
+        if (pass && pos < cap) {
+            lst[pos] = (uint32_t)ia | ((uint32_t)ib << 10);
+            tv[pos] = t;
+        }
+        cnt += __popc(m);
+        if (cnt > cap) return cnt;
+        ib += sb;
+        if (ib >= nb) { ib -= nb; ++ia; }
+        ia += sa;
+    }
+    return cnt;
+}
+
+// Selection Cuts of a big frame (phase-II occupancy), pair-factorised: Phi_01
+// depends only on (i0, i1), Phi_12 only on (i1, i2), and Delta-lambda =
+// t12(i1, i2) - t01(i0, i1) (Eq. 2-4).  1. list the (i0, i1) pairs passing Phi_01,
+// row-major, with t01; 2. list the (i1, i2) pairs passing Phi_12 (grouped by i1)
+// with t12; 3. enumerate list-1 entries x their i1's group of list 2 in row-major
+// (i0, i1, i2) order, test Delta-lambda, push survivors to the FIFO and test r_tc
+// on full warps (same survivor set and order as select_frame_warp, R3 overflow).
+// Returns -1 if a list exceeds kPairCapG (caller falls back to select_frame_warp).
+// Out of line: phase-I frames never take it, so its code stays out of the I-cache.
+static __device__ __noinline__ int select_frame_big(const DevParams* __restrict__ Pp, const Frame& F, uint32_t* q,
+                                                    uint32_t* X, CandSink sink, int cap) {
+    const DevParams& P = *Pp;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int n1 = F.n[1];
+    uint32_t* l01 = X;
+    float* t01 = reinterpret_cast<float*>(X + cap);
+    uint32_t* l12 = X + 2 * cap;
+    float* t12 = reinterpret_cast<float*>(X + 3 * cap);
+    uint32_t* off12 = X + 4 * cap;                 // n1 + 1 entries
+    uint32_t* wpre = off12 + (kMaxLayerHits + 2);  // cap + 1 entries
+    const int c01 = pair_list(F, 0, 1, P.inv_r0r1, P.c01_min, P.inv_dr01, l01, t01, cap);
+    if (c01 > cap) return -1;
+    const int c12 = pair_list(F, 1, 2, P.inv_r1r2, P.c12_min, P.inv_dr12, l12, t12, cap);
+    if (c12 > cap) return -1;
+    __syncwarp();
+    for (int i1 = lane; i1 <= n1; i1 += 32) {      // off12[i1] = lower bound of i1 in list 2
+        int lo = 0, hi = c12;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((int)(l12[mid] & 1023u) < i1) lo = mid + 1; else hi = mid;
+        }
+        off12[i1] = (uint32_t)lo;
+    }
+    __syncwarp();
+    uint32_t run = 0;                               // work prefix over list 1
+    for (int b0 = 0; b0 < c01; b0 += 32) {
+        const int p = b0 + lane;
+        uint32_t w = 0;
+        if (p < c01) {
+            const int i1 = (l01[p] >> 10) & 1023u;
+            w = off12[i1 + 1] - off12[i1];
+        }
+        uint32_t inc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (p < c01) wpre[p] = run + inc - w;
+        run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    __syncwarp();
+    const long long Wk = run;
+    int count = 0, qn = 0;
+    auto drain = [&](int n) -> bool {
+        float rt = 0.0f;
+        uint32_t pk = 0;
+        bool pass = false;
+        if (lane < n) {
+            pk = q[lane];
+            pass = pass_rt(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        const int pos = count + __popc(m & lt_mask);
+        if (pass && pos < P.cuts_max) sink.put(pos, pk, rt);
+        count += __popc(m);
+        return count > P.cuts_max;
+    };
+    for (long long base = 0; base < Wk; base += 32) {
+        const long long e = base + lane;
+        bool pass = false;
+        uint32_t pk = 0;
+        if (e < Wk) {
+            int lo = 0, hi = c01 - 1;               // list-1 entry: largest p with wpre[p] <= e
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if ((long long)wpre[mid] <= e) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t a = l01[lo];
+            const int i1 = (a >> 10) & 1023u;
+            const int k = (int)off12[i1] + (int)(e - (long long)wpre[lo]);
+            const int i2 = (l12[k] >> 10) & 1023u;
+            pass = fabsf(t12[k] - t01[lo]) <= P.dl_max;
+            pk = (a & 1023u) | ((uint32_t)i1 << 10) | ((uint32_t)i2 << 20);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (pass) q[qn + __popc(m & lt_mask)] = pk;
+        qn += __popc(m);
+        if (qn >= 32) {
+            __syncwarp();
+            if (drain(32)) return P.cuts_max + 1;
+            const uint32_t v = lane < qn - 32 ? q[32 + lane] : 0u;
+            __syncwarp();
+            if (lane < qn - 32) q[lane] = v;
+            qn -= 32;
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    if (qn > 0 && drain(qn)) return P.cuts_max + 1;
+    return count;
+}
+
 // ------------------------------------------------------------ Triplet Fit ----
 // Single-triplet fit (Sec. IV-B-1, Eq. 6, readings R6-R8).  Each arc's bending
 // angle Phi and polar angle theta are linearised in the 3D curvature k around

@@ -350,7 +350,7 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
 }
 
 // ------------------------------------------------------------------ kernel ----
-template <int MODE>
+template <int MODE, bool BIG>
 __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const KArgs A) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -432,7 +432,18 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
                             cr[pos] = rt;
                         }
                     };
-                    count = select_frame_warp(P, Fv, W.q, emit);
+                    count = -1;
+                    if (BIG && (long long)Fv.n[0] * Fv.n[1] * Fv.n[2] > kBigCombos && A.pair_scratch) {
+                        CandSink sk;
+                        if constexpr (MODE == kModeFull) {
+                            sk = CandSink{W.cidx, W.crt, cidx, crt, cbase, (uint32_t)kCandSmem};
+                        } else {
+                            sk = CandSink{ci, cr, ci, cr, 0u, 0u};
+                        }
+                        count = select_frame_big(&S.P, Fv, W.q, A.pair_scratch + gwarp * kPairWords, sk, kPairCapG);
+                        __syncwarp();
+                    }
+                    if (count < 0) count = select_frame_warp(P, Fv, W.q, emit);
                     __syncwarp();
                 }
                 const int r = inval ? M3E_REASON_INVALID
@@ -909,45 +920,48 @@ cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int MODE>
+template <int MODE, bool BIG>
 static cudaError_t launch_mode(const KArgs& a, int grid, cudaStream_t s) {
     const size_t smem = smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(filter_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(filter_kernel<MODE, BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    filter_kernel<MODE><<<grid, kThreads, smem, s>>>(a);
+    filter_kernel<MODE, BIG><<<grid, kThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t launch_filter(int mode, const KArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStream_t s) {
     switch (mode) {
-        case kModeFull: return launch_mode<kModeFull>(a, grid, s);
-        case kModeSelect: return launch_mode<kModeSelect>(a, grid, s);
-        case kModeFit: return launch_mode<kModeFit>(a, grid, s);
-        case kModeVertex: return launch_mode<kModeVertex>(a, grid, s);
-        case kModePack: return launch_mode<kModePack>(a, grid, s);
+        case kModeFull: return big ? launch_mode<kModeFull, true>(a, grid, s) : launch_mode<kModeFull, false>(a, grid, s);
+        case kModeSelect:
+            return big ? launch_mode<kModeSelect, true>(a, grid, s) : launch_mode<kModeSelect, false>(a, grid, s);
+        case kModeFit: return launch_mode<kModeFit, false>(a, grid, s);
+        case kModeVertex: return launch_mode<kModeVertex, false>(a, grid, s);
+        case kModePack: return launch_mode<kModePack, false>(a, grid, s);
     }
     return cudaErrorInvalidValue;
 }
 
-template <int MODE>
+
+template <int MODE, bool BIG>
 static int occupancy() {
     int n = 0;
     const size_t smem = smem_bytes();
-    if (cudaFuncSetAttribute(filter_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(filter_kernel<MODE, BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, filter_kernel<MODE>, kThreads, smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, filter_kernel<MODE, BIG>, kThreads, smem) != cudaSuccess)
         return 1;
     return n > 0 ? n : 1;
 }
 
-int blocks_per_sm(int mode) {
+int blocks_per_sm(int mode, bool big) {
     switch (mode) {
-        case kModeFull: return occupancy<kModeFull>();
-        case kModeSelect: return occupancy<kModeSelect>();
-        case kModeFit: return occupancy<kModeFit>();
-        case kModeVertex: return occupancy<kModeVertex>();
-        case kModePack: return occupancy<kModePack>();
+        case kModeFull: return big ? occupancy<kModeFull, true>() : occupancy<kModeFull, false>();
+        case kModeSelect: return big ? occupancy<kModeSelect, true>() : occupancy<kModeSelect, false>();
+        case kModeFit: return occupancy<kModeFit, false>();
+        case kModeVertex: return occupancy<kModeVertex, false>();
+        case kModePack: return occupancy<kModePack, false>();
     }
     return 1;
 }

@@ -20,6 +20,12 @@ constexpr int kMaxCutsCap = 1023;    // upper bound accepted for params.cuts_max
 
 enum { kModeFull = 0, kModeSelect = 1, kModeFit = 2, kModeVertex = 3, kModePack = 4 };
 
+// big frames (phase-II occupancy): pair-factorised selection with per-warp lists
+constexpr long long kBigCombos = 4096;   // n0 n1 n2 above which the pair path is used
+constexpr double kBigMeanHits = 60.0;    // calls with more hits per frame use the BIG kernel variant
+constexpr int kPairCapG = 8192;          // entries of each pair list
+constexpr size_t kPairWords = 4 * (size_t)kPairCapG + (kMaxLayerHits + 2) + (kPairCapG + 1);
+
 constexpr int kPackTile = 256;       // warp-batches per CTA of the pack kernel (8 warps x 32)
 
 // per warp-batch counts and staging offsets, written by the filter kernel and
@@ -63,6 +69,7 @@ struct KArgs {
     m3e_fit_record* pool_rec;
     m3e_track* pool_trk;
     size_t pool_stride;    // candidate entries per warp >= fb * cuts_max
+    uint32_t* pair_scratch;   // per-warp pair lists of the big-frame selection (kPairWords words per warp)
     size_t trk_stride;     // track entries per warp >= fb * max_tracks
     // stage-mode fixed slots
     uint32_t* s_cand;
@@ -78,8 +85,8 @@ struct KArgs {
 };
 
 size_t smem_bytes();
-cudaError_t launch_filter(int mode, const KArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);
-int blocks_per_sm(int mode);
+int blocks_per_sm(int mode, bool big);
 
 }  // namespace m3e

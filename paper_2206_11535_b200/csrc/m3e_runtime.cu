@@ -55,6 +55,8 @@ struct Workspace {
     size_t stage_trk_n = 0;
     KeptRec* stage_kept = nullptr;
     size_t stage_kept_n = 0;
+    uint32_t* pair_scratch = nullptr;   // big-frame selection lists, kPairWords per warp
+    int pair_warps = 0;
     size_t bytes = 0;
 };
 
@@ -94,6 +96,7 @@ struct m3e_context {
 namespace {
 
 void free_ws(Workspace& w) {
+    cudaFree(w.pair_scratch);
     cudaFree(w.bstat);
     cudaFree(w.stage_trk);
     cudaFree(w.stage_kept);
@@ -219,6 +222,13 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
         w.pool_ctas = n / kWarps;
         w.bytes += PS * n * (sizeof(uint32_t) + sizeof(float) + sizeof(m3e_fit_record)) + TS * n * sizeof(m3e_track);
     }
+    if (w.pair_warps < ctas * kWarps) {
+        cudaFree(w.pair_scratch);
+        w.bytes -= (size_t)w.pair_warps * kPairWords * sizeof(uint32_t);
+        w.pair_warps = ctas * kWarps;
+        CK(cudaMalloc(&w.pair_scratch, (size_t)w.pair_warps * kPairWords * sizeof(uint32_t)));
+        w.bytes += (size_t)w.pair_warps * kPairWords * sizeof(uint32_t);
+    }
     (void)c;
     return M3E_OK;
 }
@@ -259,7 +269,9 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     if (!x || !y || !z || !offsets) return fail(M3E_ERR_INVALID_ARGUMENT, "input pointer is NULL");
     const int fb = choose_fb(F, H);
     const uint64_t nbatch = (F + fb - 1) / fb;
-    const int bps = blocks_per_sm(mode);
+    // big-frame variant (pair-factorised selection compiled in) for high occupancy
+    const bool big = (mode == kModeFull || mode == kModeSelect) && (double)H > kBigMeanHits * (double)F;
+    const int bps = blocks_per_sm(mode, big);
     const int grid = (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * bps);
     rc = ensure_ws(ctx, w, nbatch, p, fb, grid);
     if (rc) return rc;
@@ -273,6 +285,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     a.epoch = next_epoch(w);
     a.pool_idx = w.pool_idx; a.pool_rt = w.pool_rt; a.pool_rec = w.pool_rec; a.pool_trk = w.pool_trk;
     a.pool_stride = w.pool_stride;
+    a.pair_scratch = w.pair_scratch;
     a.trk_stride = w.trk_stride;
     const bool packs = mode == kModeFull || mode == kModePack;
     if (packs) {
@@ -290,7 +303,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + 3 <= ctx->tev.size();
     cudaEvent_t* ev = tm ? &ctx->tev[ctx->tev_used] : nullptr;
     if (tm) CK(cudaEventRecord(ev[0], s));
-    CK(launch_filter(mode, a, grid, s));
+    CK(launch_filter(mode, big, a, grid, s));
     if (tm) CK(cudaEventRecord(ev[1], s));
     if (packs) {
         const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
