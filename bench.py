@@ -162,12 +162,13 @@ def run_reference(a, rank, world):
         if s >= a.warmup:
             times.append(dt)
     fps = sample / statistics.mean(times)
-    v = gbps_equiv(fps)
+    v = gbps_equiv(fps, synth.preset(a.workload).muon_rate)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "Gbps", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * statistics.mean(times), 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"{a.workload}: sample of {sample} frames per step of "
-                                            f"the 1 s phase-I stream", "frames_per_step": sample},
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD_TEXT.get(a.workload, a.workload).format(F=a.frames),
+                       "sample_frames_per_step": sample, "parallelism": "single core"},
             "cpu_baseline": {"value": round(v, 6), "unit": "Gbps", "cores": 1, "kind": "oracle",
                              "sample": f"{sample} frames per step, single-threaded fp64 C oracle",
                              "frames_per_s": round(fps, 1)},
