@@ -144,3 +144,52 @@ def test_noiseless_generated_signal_frames(P):
         assert res.vertex.p_total < 0.05
         checked += 1
     assert checked > 30
+
+
+def _noisy_signal_tracks(seed):
+    rng = np.random.default_rng(seed)
+    m = _signal_momenta(rng)
+    v = (6.0, -4.0, 12.0)
+    kicks = rng.normal(size=(3, 3)) * 0.3
+    return [_vtrack_from_helix(v, m[0] + kicks[0], +1), _vtrack_from_helix(v, m[1] + kicks[1], +1),
+            _vtrack_from_helix(v, m[2] + kicks[2], -1)]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_vertex_weights_scale_with_sigma_ms(cfg, seed):
+    """Eq. 10 with sigma_pixel = 0: every sigma_i^2 is proportional to sigma_MS^2
+    (Highland ~ sqrt(X)(1 + 0.038 ln X)); scaling X changes all weights by the same
+    factor, so the vertex (Eq. 9, 11) is unchanged and chi2 (Eq. 12) scales by
+    exactly 1 / (sigma ratio)^2 -- a wrong power of s or sigma in Eq. 10/12 fails."""
+    vt = _noisy_signal_tracks(seed)
+    base = dict(cfg, sigma_pixel=0.0, e_window=1e9, chi2_vertex_max=1e30, target_dist_max=1e9, p_total_max=1e9)
+    X1, X2 = 0.00115, 0.0046
+    r1, v1 = oracle.vertex_frame(oracle.make_params(dict(base, x_over_x0=X1)), vt)
+    r2, v2 = oracle.vertex_frame(oracle.make_params(dict(base, x_over_x0=X2)), vt)
+    assert v1 and len(v1) == len(v2)
+    ratio = (oracle.highland(30.0, X2) / oracle.highland(30.0, X1)) ** 2
+    for a, b in zip(v1, v2):
+        assert (b.x, b.y, b.z) == pytest.approx((a.x, a.y, a.z), abs=1e-9)
+        assert b.chi2 == pytest.approx(a.chi2 / ratio, rel=1e-9)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_vertex_equal_weights_is_centroid(cfg, seed):
+    """Eq. 9 with equal weights (sigma_MS -> 0, sigma_pixel dominant) reduces to
+    the arithmetic mean: mu_t is the centroid of one choice of pairwise circle
+    intersections, and mu_z the mean of the three Eq. 11 z values."""
+    vt = _noisy_signal_tracks(seed)
+    P = oracle.make_params(dict(cfg, x_over_x0=1e-30, sigma_pixel=1.0, e_window=1e9, chi2_vertex_max=1e30,
+                                target_dist_max=1e9, p_total_max=1e9))
+    res, verts = oracle.vertex_frame(P, vt)
+    assert verts
+    circles = []
+    for t in vt:
+        k = abs(t.kappa)
+        rt = math.sqrt(1 - t.cos_theta01 ** 2) / k
+        circles.append(((t.cx, t.cy), rt))
+    pts = [oracle.circle_intersections(circles[i][0], circles[i][1], circles[j][0], circles[j][1])[0]
+           for i, j in ((0, 1), (0, 2), (1, 2))]
+    cents = [((a[0] + b[0] + c[0]) / 3, (a[1] + b[1] + c[1]) / 3) for a in pts[0] for b in pts[1] for c in pts[2]]
+    v = verts[0]
+    assert min(math.hypot(v.x - cx, v.y - cy) for cx, cy in cents) < 1e-9
