@@ -28,7 +28,7 @@
 #include "m3e_kernels.h"
 
 #ifndef M3E_MIN_BLOCKS
-#define M3E_MIN_BLOCKS 3   // CTAs per SM the register allocation targets (80 regs: 24 warps/SM)
+#define M3E_MIN_BLOCKS 4   // CTAs per SM the register allocation targets (64 regs: 32 warps/SM)
 #endif
 
 namespace m3e {
@@ -91,7 +91,6 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
 struct BatchState {
     int nstored[kFB], ncand[kFB], ntrk[kFB], nneg[kFB], ncomb[kFB], reason[kFB];
     uint32_t o_trk[kFB + 1], o_kept[kFB + 1], o_hits[kFB + 1];   // exclusive prefixes (+ total)
-    m3e_vertex vtx[kFB];
 };
 
 // A warp-batch computes for ~10^5 cycles against a ~10^3-cycle bulk-copy latency,
@@ -99,6 +98,14 @@ struct BatchState {
 // and holds the warp-batch's candidates instead.
 constexpr int kNBuf = 1;
 constexpr int kCandSmem = 256;   // candidates of a warp-batch kept in shared memory
+
+// Cold vertex-stage scratch of one warp, in global memory (L1/L2 resident;
+// touched for ~1.5% of frames), so that it does not cost shared memory.
+struct VScratch {
+    m3e_vertex vtx[kFB];
+    uint32_t vcomb[kMaxCombsCap];
+    uint8_t vlist[2][kMaxTracksCap];
+};
 
 struct __align__(16) WarpSmem {
     float hx[kNBuf][kHCap];
@@ -113,8 +120,6 @@ struct __align__(16) WarpSmem {
     uint32_t pref[kFB + 1];          // candidates: exclusive prefix
     int npos[kFB];                   // stored positive tracks per frame (vertex gate)
     uint32_t q[64];                  // Delta-lambda survivors (selection FIFO)
-    uint8_t vlist[2][kMaxTracksCap];
-    uint32_t vcomb[kMaxCombsCap];
     uint32_t acc[12];                // run summary: kept_by_reason[6], cand, frames, tracks, hits, overflow
 };
 
@@ -243,7 +248,7 @@ __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) 
 // Vertex selection of frame j (Sec. IV-C, Alg. 4; whole warp), out of line: it
 // runs for ~1.5% of frames and keeps its fp64 registers and code out of the
 // main loop.
-static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ Pp, WarpSmem& W, BatchState& B,
+static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ Pp, VScratch& V, BatchState& B,
                                                  int j, const m3e_track* tj, const Frame& Fv, uint32_t f0) {
     const DevParams& P = *Pp;
     const int lane = threadIdx.x & 31;
@@ -260,8 +265,8 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
             const bool ispos = i < nt && kap > 0.0f, isneg = i < nt && kap < 0.0f;
             const unsigned mp = __ballot_sync(0xffffffffu, ispos);
             const unsigned mn = __ballot_sync(0xffffffffu, isneg);
-            if (ispos) W.vlist[0][npos + __popc(mp & lt_mask)] = (uint8_t)i;
-            if (isneg) W.vlist[1][nneg + __popc(mn & lt_mask)] = (uint8_t)i;
+            if (ispos) V.vlist[0][npos + __popc(mp & lt_mask)] = (uint8_t)i;
+            if (isneg) V.vlist[1][nneg + __popc(mn & lt_mask)] = (uint8_t)i;
             npos += __popc(mp);
             nneg += __popc(mn);
         }
@@ -278,7 +283,7 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
                     const int ia = t / (npos * nneg), rem = t - ia * npos * nneg;
                     const int ib = rem / nneg, ie = rem - ib * nneg;
                     if (ia < ib) {
-                        const int a = W.vlist[0][ia], bb = W.vlist[0][ib], e = W.vlist[1][ie];
+                        const int a = V.vlist[0][ia], bb = V.vlist[0][ib], e = V.vlist[1][ie];
                         const double dE = track_energy(P, tj[a].kappa) + track_energy(P, tj[bb].kappa) +
                                           track_energy(P, tj[e].kappa) - kMuMass;
                         pass = fabs(dE) <= P.e_window;
@@ -287,7 +292,7 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, pass);
                 const int pos = ncomb + __popc(m & lt_mask);
-                if (pass && pos < P.max_combs) W.vcomb[pos] = code;
+                if (pass && pos < P.max_combs) V.vcomb[pos] = code;
                 ncomb += __popc(m);
                 if (ncomb > P.max_combs) break;
             }
@@ -301,7 +306,7 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
                 VResult bres;
                 bres.pass = 0;
                 for (int c = lane; c < ncomb; c += 32) {
-                    const uint32_t code = W.vcomb[c];
+                    const uint32_t code = V.vcomb[c];
                     VTrk T[3];
                     T[0] = make_vtrk(P, tj[code & 255u], Fv);
                     T[1] = make_vtrk(P, tj[(code >> 8) & 255u], Fv);
@@ -321,7 +326,7 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
                 if (widx != 0x7fffffff) {
                     has_vtx = true;
                     if (bidx == widx) {
-                        const uint32_t code = W.vcomb[widx];
+                        const uint32_t code = V.vcomb[widx];
                         m3e_vertex v;
                         v.frame = f0 + j;
                         v.track[0] = (uint16_t)(code & 255u);
@@ -333,7 +338,7 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
                         v.chi2 = bres.chi2;
                         v.target_dist = (float)bres.tdist;
                         v.p_total = (float)bres.ptot;
-                        B.vtx[j] = v;
+                        V.vtx[j] = v;
                     }
                 }
             }
@@ -360,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
     constexpr bool kOut = MODE == kModeFull || MODE == kModePack;   // ordered outputs
     WarpSmem& W = S.w[warp];
     const size_t gwarp = (size_t)blockIdx.x * kWarps + warp;
+    VScratch& V = reinterpret_cast<VScratch*>(A.vscratch)[gwarp];
 
     if (tid == 0) S.P = A.P;
     if (lane == 0) {
@@ -617,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
                     }
                 }
                 const Frame Fv = frame_view(A, W, buf, j);
-                vertex_frame(&S.P, W, B, j, ctrk + tfirst + (size_t)j * P.max_tracks, Fv, f0);
+                vertex_frame(&S.P, V, B, j, ctrk + tfirst + (size_t)j * P.max_tracks, Fv, f0);
                 __syncwarp();
             }
         }
@@ -632,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
                 fo.track_first = (uint32_t)(tfirst + (size_t)j * P.max_tracks);
                 fo.kept_index = 0xFFFFFFFFu;
                 A.out.frames[f0 + j] = fo;
-                if (B.reason[j] == M3E_REASON_VERTEX && A.s_vtx) A.s_vtx[f0 + j] = B.vtx[j];
+                if (B.reason[j] == M3E_REASON_VERTEX && A.s_vtx) A.s_vtx[f0 + j] = V.vtx[j];
             }
         }
 
@@ -682,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
                         kr.frame = f0 + j;
                         kr.pad = 0;
                         if (r == M3E_REASON_VERTEX) {
-                            kr.v = B.vtx[j];
+                            kr.v = V.vtx[j];
                         } else {
                             kr.v = m3e_vertex{};
                             kr.v.frame = 0xFFFFFFFFu;
@@ -967,3 +973,5 @@ int blocks_per_sm(int mode, bool big) {
 }
 
 }  // namespace m3e
+
+static_assert(sizeof(m3e::VScratch) <= m3e::kVScratchBytes, "kVScratchBytes too small");

@@ -13,10 +13,11 @@ namespace m3e {
 constexpr int kThreads = 256;        // 8 warps per CTA, each an independent pipeline
 constexpr int kWarps = kThreads / 32;
 constexpr int kFB = 16;              // frames per warp-batch (upper bound; runtime fb <= kFB)
-constexpr int kHCap = 320;           // hits of a warp-batch staged in shared memory (per buffer)
+constexpr int kHCap = 256;           // hits of a warp-batch staged in shared memory
 constexpr int kMaxTracksCap = 128;   // upper bound accepted for params.max_tracks
 constexpr int kMaxCombsCap = 128;    // upper bound accepted for params.max_combs + 1
 constexpr int kMaxCutsCap = 1023;    // upper bound accepted for params.cuts_max
+constexpr size_t kVScratchBytes = 2048;   // >= sizeof(VScratch), checked in m3e_kernels.cu
 
 enum { kModeFull = 0, kModeSelect = 1, kModeFit = 2, kModeVertex = 3, kModePack = 4 };
 
@@ -70,6 +71,7 @@ struct KArgs {
     m3e_track* pool_trk;
     size_t pool_stride;    // candidate entries per warp >= fb * cuts_max
     uint32_t* pair_scratch;   // per-warp pair lists of the big-frame selection (kPairWords words per warp)
+    void* vscratch;           // per-warp vertex-stage scratch (kVScratchBytes per warp)
     size_t trk_stride;     // track entries per warp >= fb * max_tracks
     // stage-mode fixed slots
     uint32_t* s_cand;

@@ -57,6 +57,7 @@ struct Workspace {
     size_t stage_kept_n = 0;
     uint32_t* pair_scratch = nullptr;   // big-frame selection lists, kPairWords per warp
     int pair_warps = 0;
+    void* vscratch = nullptr;           // vertex-stage scratch, kVScratchBytes per warp
     size_t bytes = 0;
 };
 
@@ -97,6 +98,7 @@ namespace {
 
 void free_ws(Workspace& w) {
     cudaFree(w.pair_scratch);
+    cudaFree(w.vscratch);
     cudaFree(w.bstat);
     cudaFree(w.stage_trk);
     cudaFree(w.stage_kept);
@@ -224,10 +226,12 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
     }
     if (w.pair_warps < ctas * kWarps) {
         cudaFree(w.pair_scratch);
-        w.bytes -= (size_t)w.pair_warps * kPairWords * sizeof(uint32_t);
+        cudaFree(w.vscratch);
+        w.bytes -= (size_t)w.pair_warps * (kPairWords * sizeof(uint32_t) + kVScratchBytes);
         w.pair_warps = ctas * kWarps;
         CK(cudaMalloc(&w.pair_scratch, (size_t)w.pair_warps * kPairWords * sizeof(uint32_t)));
-        w.bytes += (size_t)w.pair_warps * kPairWords * sizeof(uint32_t);
+        CK(cudaMalloc(&w.vscratch, (size_t)w.pair_warps * kVScratchBytes));
+        w.bytes += (size_t)w.pair_warps * (kPairWords * sizeof(uint32_t) + kVScratchBytes);
     }
     (void)c;
     return M3E_OK;
@@ -286,6 +290,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     a.pool_idx = w.pool_idx; a.pool_rt = w.pool_rt; a.pool_rec = w.pool_rec; a.pool_trk = w.pool_trk;
     a.pool_stride = w.pool_stride;
     a.pair_scratch = w.pair_scratch;
+    a.vscratch = w.vscratch;
     a.trk_stride = w.trk_stride;
     const bool packs = mode == kModeFull || mode == kModePack;
     if (packs) {
