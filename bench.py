@@ -106,8 +106,8 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def load_traffic(workload: str, frames: int, seed: int):
-    """DRAM bytes per filter-kernel launch from the committed ncu capture of this
+def load_traffic(workload: str, frames: int, seed: int, kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of this
     exact configuration (profiles/*_bench_traffic.json), else None."""
     import glob
     for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_bench_traffic.json")), reverse=True):
@@ -115,7 +115,8 @@ def load_traffic(workload: str, frames: int, seed: int):
             t = json.load(open(fn))
         except Exception:
             continue
-        if t.get("workload") == workload and t.get("frames") == frames and t.get("seed") == seed:
+        if (t.get("workload") == workload and t.get("frames") == frames and t.get("seed") == seed
+                and t.get("kernel") == kernel):
             return t["dram_read_bytes"] + t["dram_write_bytes"]
     return None
 
@@ -242,7 +243,7 @@ def main():
         dist.barrier()
     ms = [s.elapsed_time(e) for s, e in ev]
     ms_step = statistics.mean(ms)
-    ms_filter, ms_pack = ctx.kernel_times()
+    ms_select, ms_filter, ms_pack = ctx.kernel_times()
     sm = res.summary_np()
     kept = int(sum(sm["kept_by_reason"][1:]))
     assert int(sm["frames"]) == F and not int(sm["overflow"]), "output capacity exceeded"
@@ -314,11 +315,22 @@ def main():
 
     if rank == 0:
         peak, peak_kind = load_peaks()
-        achieved = out_bytes_total = None
-        # dominant (only) kernel: filter_kernel<FULL>; algorithmic bytes per launch =
-        # input hit stream + per-frame outputs + tracks + packed kept frames
-        alg_bytes = in_bytes + out_bytes
-        achieved = alg_bytes / (ms_filter / 1e3) / 1e9
+        # algorithmic bytes per launch:
+        #   selection kernel: hit stream in + per-frame selection word + candidates out
+        #   filter kernel: hit stream + selection words + candidates in, per-frame
+        #   outputs + tracks + kept records out (fused path: hit stream + outputs)
+        split = ms_select > 0
+        cand = int(sm["candidates"])
+        big = H > 60 * F
+        if split:
+            sel_bytes = in_bytes + 4 * F + 8 * cand
+            kernels = [("m3e::filter_kernel<SELECT_C, BIG=false>", ms_select, sel_bytes),
+                       ("m3e::filter_kernel<FULL, BIG=false>", ms_filter, sel_bytes + out_bytes)]
+        else:
+            kernels = [("m3e::filter_kernel<FULL, BIG=%s>" % ("true" if big else "false"), ms_filter,
+                        in_bytes + out_bytes)]
+        kname, kms, alg_bytes = max(kernels, key=lambda k: k[1])
+        achieved = alg_bytes / (kms / 1e3) / 1e9
         clocks = clk.summary()
         line = {
             "metric": METRIC, "value": round(gbps_equiv(fps, rate), 3), "unit": "Gbps", "n_gpus": world,
@@ -338,11 +350,12 @@ def main():
                        "parallelism": f"frame-sharded dp{world}", "generation_s": round(t_gen, 1)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
-                         "traffic": load_traffic(a.workload, F, a.seed), "peak_kind": peak_kind,
-                         "kernel": "m3e::filter_kernel<FULL, BIG=false>" if F and H < 60 * F else "m3e::filter_kernel<FULL, BIG=true>", "kernel_ms": round(ms_filter, 4),
-                         "share_of_step": round(ms_filter / ms_step, 4), "pack_kernel_ms": round(ms_pack, 4),
-                         "algorithmic_bytes_per_launch": int(alg_bytes)},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * a.steps, "clocks": clocks,
+                         "traffic": load_traffic(a.workload, F, a.seed, kname), "peak_kind": peak_kind,
+                         "kernel": kname, "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms_step, 4),
+                         "algorithmic_bytes_per_launch": int(alg_bytes),
+                         "kernels_ms": {"select": round(ms_select, 4), "filter": round(ms_filter, 4),
+                                        "pack": round(ms_pack, 4)}},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (3 if split else 2) * a.steps, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

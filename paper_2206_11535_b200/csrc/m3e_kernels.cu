@@ -30,6 +30,9 @@
 #ifndef M3E_MIN_BLOCKS
 #define M3E_MIN_BLOCKS 4   // CTAs per SM the register allocation targets (64 regs: 32 warps/SM)
 #endif
+#ifndef M3E_MIN_BLOCKS_SEL
+#define M3E_MIN_BLOCKS_SEL 4   // same for the selection kernel of the split path
+#endif
 
 namespace m3e {
 
@@ -356,7 +359,8 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
 
 // ------------------------------------------------------------------ kernel ----
 template <int MODE, bool BIG>
-__global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const KArgs A) {
+__global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCKS_SEL : M3E_MIN_BLOCKS)
+    filter_kernel(const KArgs A) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
         fence_mbar_init();
     }
     __syncthreads();   // the only CTA barrier before the final summary flush
-    if (lane == 0) issue_load(A, W, 0, atomicAdd(A.ticket, 1u));
+    if (lane == 0) issue_load(A, W, 0, atomicAdd(A.bticket, 1u));
     __syncwarp();
     int buf = 0;
     uint32_t phase[kNBuf] = {};
@@ -386,7 +390,8 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
     float* crt;
     m3e_fit_record* crec;
     m3e_track* ctrk_base;
-    if constexpr (MODE == kModeFull) {
+    constexpr bool kFlat = MODE == kModeFull || MODE == kModeSelectC;   // flat warp-batch candidate index
+    if constexpr (kFlat) {
         cidx = A.pool_idx + gwarp * A.pool_stride;
         crt = A.pool_rt + gwarp * A.pool_stride;
         crec = A.pool_rec + gwarp * A.pool_stride;
@@ -401,20 +406,35 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
     for (;;) {
         const uint32_t b = W.b_batch[buf];
         if (b >= A.nbatch) break;
-        if (kNBuf == 2 && lane == 0) issue_load(A, W, buf ^ 1, atomicAdd(A.ticket, 1u));
+        if (kNBuf == 2 && lane == 0) issue_load(A, W, buf ^ 1, atomicAdd(A.bticket, 1u));
         mbar_wait(&W.bar[buf], phase[buf]);
         phase[buf] ^= 1u;
 
         BatchState& B = W.st;
         const uint32_t f0 = b * (uint32_t)A.fb;
         const int nf = (int)min(A.F - f0, (uint32_t)A.fb);
-        const size_t cfirst = MODE == kModeFull ? 0 : (size_t)f0 * P.cuts_max;   // slot of frame 0
+        const size_t cfirst = kFlat ? 0 : (size_t)f0 * P.cuts_max;   // slot of frame 0
         const size_t tfirst = MODE == kModeFull ? 0 : (size_t)f0 * P.max_tracks;
         m3e_track* ctrk = ctrk_base;
 
+        // split path: the Selection Cuts already ran (kModeSelectC) unless the
+        // warp-batch's candidates did not fit the store
+        uint32_t gbase = kSpilled;
+        if constexpr (MODE == kModeFull && !BIG) {
+            if (A.presel) gbase = A.bsel[b];
+        }
+        if (gbase != kSpilled) {
+            for (int j = lane; j < nf; j += 32) {
+                const uint32_t w = A.sel[f0 + j];
+                const int r = (int)(w >> 16), n = (int)(w & 0xFFFFu);
+                B.ncand[j] = n;
+                B.reason[j] = r;
+                B.nstored[j] = r == M3E_REASON_NONE ? n : 0;
+            }
+        } else
         // ---------------------------------------------------- S: Selection Cuts
-        if constexpr (MODE == kModeFull || MODE == kModeSelect) {
-            uint32_t cbase = 0;   // FULL: flat candidate index of frame j's first candidate
+        if constexpr (MODE == kModeFull || MODE == kModeSelect || MODE == kModeSelectC) {
+            uint32_t cbase = 0;   // flat: candidate index of frame j's first candidate
             for (int j = 0; j < nf; ++j) {
                 const Frame Fv = frame_view(A, W, buf, j);
                 const bool inval = Fv.n[0] > kMaxLayerHits || Fv.n[1] > kMaxLayerHits ||
@@ -424,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
                     uint32_t* ci = cidx + cfirst + (size_t)j * P.cuts_max;
                     float* cr = crt + cfirst + (size_t)j * P.cuts_max;
                     auto emit = [&](int pos, uint32_t packed, float rt) {
-                        if constexpr (MODE == kModeFull) {
+                        if constexpr (kFlat) {
                             const uint32_t fi = cbase + (uint32_t)pos;
                             if (fi < (uint32_t)kCandSmem) {
                                 W.cidx[fi] = packed;
@@ -441,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
                     count = -1;
                     if (BIG && (long long)Fv.n[0] * Fv.n[1] * Fv.n[2] > kBigCombos && A.pair_scratch) {
                         CandSink sk;
-                        if constexpr (MODE == kModeFull) {
+                        if constexpr (kFlat) {
                             sk = CandSink{W.cidx, W.crt, cidx, crt, cbase, (uint32_t)kCandSmem};
                         } else {
                             sk = CandSink{ci, cr, ci, cr, 0u, 0u};
@@ -487,6 +507,33 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
         }
         __syncwarp();
 
+        if constexpr (MODE == kModeSelectC) {   // candidates -> store, warp-batch contiguous
+            uint32_t tot = 0;
+            for (int j = lane; j < nf; j += 32) {
+                A.sel[f0 + j] = (uint32_t)B.ncand[j] | ((uint32_t)B.reason[j] << 16);
+                tot += (uint32_t)B.nstored[j];
+            }
+            tot = warp_sum(tot);
+            unsigned long long base = 0;
+            if (lane == 0 && tot) base = atomicAdd(reinterpret_cast<unsigned long long*>(A.ticket + 6), tot);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const bool fits = base + tot <= A.cand_cap;
+            if (fits) {
+                for (uint32_t e = lane; e < tot; e += 32) {
+                    uint2 c;
+                    if (e < (uint32_t)kCandSmem) {
+                        c.x = W.cidx[e];
+                        c.y = __float_as_uint(W.crt[e]);
+                    } else {
+                        c.x = cidx[e];
+                        c.y = __float_as_uint(crt[e]);
+                    }
+                    A.cand_g[base + e] = c;
+                }
+            }
+            if (lane == 0) A.bsel[b] = fits ? (uint32_t)base : kSpilled;
+        }
+
         if constexpr (MODE == kModeSelect) {
             for (int j = lane; j < nf; j += 32) {
                 m3e_frame_out fo;
@@ -525,7 +572,11 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
                     float rt;
                     if constexpr (MODE == kModeFull) {   // flat warp-batch candidate index
                         slot = (size_t)e;
-                        if (e < kCandSmem) {
+                        if (gbase != kSpilled) {
+                            const uint2 c = A.cand_g[gbase + e];
+                            pk = c.x;
+                            rt = __uint_as_float(c.y);
+                        } else if (e < kCandSmem) {
                             pk = W.cidx[e];
                             rt = W.crt[e];
                         } else {
@@ -746,7 +797,7 @@ __global__ void __launch_bounds__(kThreads, M3E_MIN_BLOCKS) filter_kernel(const 
         if constexpr (kNBuf == 2) {
             buf ^= 1;
         } else if (lane == 0) {
-            issue_load(A, W, 0, atomicAdd(A.ticket, 1u));
+            issue_load(A, W, 0, atomicAdd(A.bticket, 1u));
         }
         __syncwarp();
     }
@@ -941,6 +992,7 @@ cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStre
         case kModeFull: return big ? launch_mode<kModeFull, true>(a, grid, s) : launch_mode<kModeFull, false>(a, grid, s);
         case kModeSelect:
             return big ? launch_mode<kModeSelect, true>(a, grid, s) : launch_mode<kModeSelect, false>(a, grid, s);
+        case kModeSelectC: return launch_mode<kModeSelectC, false>(a, grid, s);
         case kModeFit: return launch_mode<kModeFit, false>(a, grid, s);
         case kModeVertex: return launch_mode<kModeVertex, false>(a, grid, s);
         case kModePack: return launch_mode<kModePack, false>(a, grid, s);
@@ -965,6 +1017,7 @@ int blocks_per_sm(int mode, bool big) {
     switch (mode) {
         case kModeFull: return big ? occupancy<kModeFull, true>() : occupancy<kModeFull, false>();
         case kModeSelect: return big ? occupancy<kModeSelect, true>() : occupancy<kModeSelect, false>();
+        case kModeSelectC: return occupancy<kModeSelectC, false>();
         case kModeFit: return occupancy<kModeFit, false>();
         case kModeVertex: return occupancy<kModeVertex, false>();
         case kModePack: return occupancy<kModePack, false>();

@@ -19,7 +19,11 @@ constexpr int kMaxCombsCap = 128;    // upper bound accepted for params.max_comb
 constexpr int kMaxCutsCap = 1023;    // upper bound accepted for params.cuts_max
 constexpr size_t kVScratchBytes = 2048;   // >= sizeof(VScratch), checked in m3e_kernels.cu
 
-enum { kModeFull = 0, kModeSelect = 1, kModeFit = 2, kModeVertex = 3, kModePack = 4 };
+// kModeSelectC: the Selection Cuts alone, candidates written compactly to the
+// candidate store (first kernel of the split production path); kModeFull then
+// reads them (A.presel) instead of selecting again
+enum { kModeFull = 0, kModeSelect = 1, kModeFit = 2, kModeVertex = 3, kModePack = 4, kModeSelectC = 5 };
+constexpr uint32_t kSpilled = 0xFFFFFFFFu;   // bsel[] entry of a warp-batch whose candidates did not fit
 
 // big frames (phase-II occupancy): pair-factorised selection with per-warp lists
 constexpr long long kBigCombos = 4096;   // n0 n1 n2 above which the pair path is used
@@ -55,8 +59,16 @@ struct KArgs {
     int fb;                // frames per batch
     uint32_t nbatch;
     // workspace
-    uint32_t* ticket;      // counters (zeroed before the launch): [0] warp-batch ticket, [1] staged
-                           // tracks, [2] staged kept frames, [3] pack-kernel tile ticket
+    uint32_t* ticket;      // counters (zeroed before the launch): [0] select warp-batch ticket, [1] staged
+                           // tracks, [2] staged kept frames, [3] pack-kernel tile ticket, [4] filter
+                           // warp-batch ticket, [6..7] candidate-store fill (u64)
+    uint32_t* bticket;     // this launch's warp-batch ticket (ticket + 0 or ticket + 4)
+    // candidate store of the split path (kModeSelectC writes, kModeFull + presel reads)
+    int presel;            // kModeFull: take candidates from the store (batches not spilled)
+    uint2* cand_g;         // {packed hit indices, r_tc bits}, warp-batch contiguous, frame order
+    uint64_t cand_cap;     // entries of cand_g (< 2^32)
+    uint32_t* sel;         // [F] per frame: n_cand | reason << 16
+    uint32_t* bsel;        // [nbatch] first store entry of the warp-batch, or kSpilled
     uint4* status;         // pack-kernel decoupled look-back, one 16 B word per tile
     uint32_t epoch;        // launch epoch tag of the status words (never 0)
     BatchStat* bstat;      // [nbatch]

@@ -6,6 +6,7 @@
 // is filled"; "CUDA streams are used").
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -58,6 +59,12 @@ struct Workspace {
     uint32_t* pair_scratch = nullptr;   // big-frame selection lists, kPairWords per warp
     int pair_warps = 0;
     void* vscratch = nullptr;           // vertex-stage scratch, kVScratchBytes per warp
+    uint2* cand_g = nullptr;            // candidate store of the split path
+    size_t cand_n = 0;
+    uint32_t* sel = nullptr;            // per-frame selection words of the split path
+    size_t sel_n = 0;
+    uint32_t* bsel = nullptr;           // per-warp-batch store offsets of the split path
+    size_t bsel_n = 0;
     size_t bytes = 0;
 };
 
@@ -90,13 +97,18 @@ struct m3e_context {
     Chunk ch[2];
     uint64_t chunk_frames = 0;
     bool timing = false;
-    std::vector<cudaEvent_t> tev;   // 3 events per timed m3e_filter call
+    bool split = true;              // two-kernel production path (M3E_FUSED=1 in the environment: one kernel)
+    std::vector<cudaEvent_t> tev;   // 4 events per timed m3e_filter call
     size_t tev_used = 0;
+    size_t tev_split = 0;           // timed calls that ran the split path
 };
 
 namespace {
 
 void free_ws(Workspace& w) {
+    cudaFree(w.cand_g);
+    cudaFree(w.sel);
+    cudaFree(w.bsel);
     cudaFree(w.pair_scratch);
     cudaFree(w.vscratch);
     cudaFree(w.bstat);
@@ -184,8 +196,8 @@ int choose_fb(uint64_t F, uint64_t H) {
 
 int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p, int fb, int ctas) {
     if (!w.ticket) {
-        CK(cudaMalloc(&w.ticket, 16));
-        w.bytes += 16;
+        CK(cudaMalloc(&w.ticket, 8 * sizeof(uint32_t)));
+        w.bytes += 8 * sizeof(uint32_t);
     }
     const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
     if (w.bstat_n < nbatch) {
@@ -237,6 +249,36 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
     return M3E_OK;
 }
 
+// split path: candidate store (kCandPerFrame entries per frame; warp-batches
+// that do not fit are flagged and re-selected by the filter kernel), per-frame
+// selection words and per-warp-batch store offsets
+constexpr uint64_t kCandPerFrame = 24;
+int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch) {
+    const uint64_t nc = std::min<uint64_t>(std::max<uint64_t>(kCandPerFrame * F, 1u << 16), 0xFFFFFFF0ull);
+    if (w.cand_n < nc) {
+        cudaFree(w.cand_g);
+        w.bytes -= w.cand_n * sizeof(uint2);
+        CK(cudaMalloc(&w.cand_g, nc * sizeof(uint2)));
+        w.cand_n = nc;
+        w.bytes += nc * sizeof(uint2);
+    }
+    if (w.sel_n < F) {
+        cudaFree(w.sel);
+        w.bytes -= w.sel_n * sizeof(uint32_t);
+        CK(cudaMalloc(&w.sel, F * sizeof(uint32_t)));
+        w.sel_n = F;
+        w.bytes += F * sizeof(uint32_t);
+    }
+    if (w.bsel_n < nbatch) {
+        cudaFree(w.bsel);
+        w.bytes -= w.bsel_n * sizeof(uint32_t);
+        CK(cudaMalloc(&w.bsel, nbatch * sizeof(uint32_t)));
+        w.bsel_n = nbatch;
+        w.bytes += nbatch * sizeof(uint32_t);
+    }
+    return M3E_OK;
+}
+
 // staging of the filter kernel's tracks and kept-frame records, sized by the
 // caller's output capacities (the pack kernel copies them into place)
 int ensure_stage(Workspace& w, uint64_t trk, uint64_t kept) {
@@ -275,16 +317,26 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     const uint64_t nbatch = (F + fb - 1) / fb;
     // big-frame variant (pair-factorised selection compiled in) for high occupancy
     const bool big = (mode == kModeFull || mode == kModeSelect) && (double)H > kBigMeanHits * (double)F;
+    // production path split in two kernels (Selection Cuts | fit, vertex, output)
+    // so that each keeps its hot code in the instruction cache
+    const bool split = mode == kModeFull && !big && ctx->split;
     const int bps = blocks_per_sm(mode, big);
     const int grid = (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * bps);
-    rc = ensure_ws(ctx, w, nbatch, p, fb, grid);
+    const int sgrid = split ? (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * blocks_per_sm(kModeSelectC, false))
+                            : 0;
+    rc = ensure_ws(ctx, w, nbatch, p, fb, std::max(grid, sgrid));
     if (rc) return rc;
+    if (split) {
+        rc = ensure_split(w, F, nbatch);
+        if (rc) return rc;
+    }
     a.P = make_dev_params(p);
     a.x = x; a.y = y; a.z = z; a.offsets = offsets;
     a.F = (uint32_t)F;
     a.fb = fb;
     a.nbatch = (uint32_t)nbatch;
     a.ticket = w.ticket;
+    a.bticket = w.ticket;
     a.status = w.status;
     a.epoch = next_epoch(w);
     a.pool_idx = w.pool_idx; a.pool_rt = w.pool_rt; a.pool_rec = w.pool_rec; a.pool_trk = w.pool_trk;
@@ -303,21 +355,37 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         a.stage_kept = w.stage_kept;
         a.stage_kept_cap = a.out.kept_capacity;
     }
-    CK(cudaMemsetAsync(w.ticket, 0, 4 * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(w.ticket, 0, 8 * sizeof(uint32_t), s));
     if (a.out.summary) CK(cudaMemsetAsync(a.out.summary, 0, sizeof(m3e_summary), s));
-    const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + 3 <= ctx->tev.size();
+    const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + 4 <= ctx->tev.size();
     cudaEvent_t* ev = tm ? &ctx->tev[ctx->tev_used] : nullptr;
     if (tm) CK(cudaEventRecord(ev[0], s));
-    CK(launch_filter(mode, big, a, grid, s));
+    if (split) {
+        KArgs sa = a;
+        sa.cand_g = w.cand_g;
+        sa.cand_cap = w.cand_n;
+        sa.sel = w.sel;
+        sa.bsel = w.bsel;
+        CK(launch_filter(kModeSelectC, false, sa, sgrid, s));
+        a.presel = 1;
+        a.cand_g = w.cand_g;
+        a.cand_cap = w.cand_n;
+        a.sel = w.sel;
+        a.bsel = w.bsel;
+        a.bticket = w.ticket + 4;
+    }
     if (tm) CK(cudaEventRecord(ev[1], s));
+    CK(launch_filter(mode, big, a, grid, s));
+    if (tm) CK(cudaEventRecord(ev[2], s));
     if (packs) {
         const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
         const int pgrid = (int)std::min<uint64_t>(ntiles, (uint64_t)ctx->sms * 8);
         CK(launch_pack(a, pgrid, s));
     }
     if (tm) {
-        CK(cudaEventRecord(ev[2], s));
-        ctx->tev_used += 3;
+        CK(cudaEventRecord(ev[3], s));
+        ctx->tev_used += 4;
+        ctx->tev_split += split ? 1 : 0;
     }
     return M3E_OK;
 }
@@ -343,6 +411,8 @@ int m3e_create(m3e_context** out, int device, uint64_t max_frames, uint64_t max_
     c->sms = prop.multiProcessorCount;
     c->max_frames = max_frames;
     c->max_hits = max_hits;
+    const char* fused = std::getenv("M3E_FUSED");
+    c->split = !(fused && fused[0] == '1');
     for (int i = 0; i < 2; ++i) {
         if (cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) != cudaSuccess) {
             delete c;
@@ -373,30 +443,32 @@ int m3e_set_timing(m3e_context* c, int enable) {
     if (!c) return fail(M3E_ERR_INVALID_ARGUMENT, "ctx is NULL");
     CK(cudaSetDevice(c->device));
     if (enable && c->tev.empty()) {
-        c->tev.resize(3 * 1024);   // up to 1024 timed calls between two m3e_kernel_times()
+        c->tev.resize(4 * 1024);   // up to 1024 timed calls between two m3e_kernel_times()
         for (auto& e : c->tev) CK(cudaEventCreate(&e));
     }
     c->timing = enable != 0;
     c->tev_used = 0;
+    c->tev_split = 0;
     return M3E_OK;
 }
 
-int m3e_kernel_times(m3e_context* c, float ms[2]) {
+int m3e_kernel_times(m3e_context* c, float ms[3]) {
     if (!c || !ms) return fail(M3E_ERR_INVALID_ARGUMENT, "NULL argument");
     if (c->tev_used == 0) return fail(M3E_ERR_INVALID_ARGUMENT, "no timed call since the last reset");
-    double a = 0, b = 0;
-    const size_t n = c->tev_used / 3;
+    double acc[3] = {0, 0, 0};
+    const size_t n = c->tev_used / 4;
     for (size_t i = 0; i < n; ++i) {
-        float x = 0, y = 0;
-        CK(cudaEventSynchronize(c->tev[3 * i + 2]));
-        CK(cudaEventElapsedTime(&x, c->tev[3 * i], c->tev[3 * i + 1]));
-        CK(cudaEventElapsedTime(&y, c->tev[3 * i + 1], c->tev[3 * i + 2]));
-        a += x;
-        b += y;
+        CK(cudaEventSynchronize(c->tev[4 * i + 3]));
+        for (int k = 0; k < 3; ++k) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, c->tev[4 * i + k], c->tev[4 * i + k + 1]));
+            acc[k] += t;
+        }
     }
-    ms[0] = (float)(a / n);
-    ms[1] = (float)(b / n);
+    for (int k = 0; k < 3; ++k) ms[k] = (float)(acc[k] / n);
+    if (c->tev_split == 0) ms[0] = 0.0f;   // no selection kernel ran (fused path)
     c->tev_used = 0;
+    c->tev_split = 0;
     return M3E_OK;
 }
 

@@ -15,7 +15,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libm3e.so")
+# M3E_LIB: path of an alternative build (tuning experiments); default the in-tree build
+LIB_PATH = os.environ.get("M3E_LIB") or os.path.join(_HERE, "lib", "libm3e.so")
 ROOT = os.path.dirname(_HERE)
 DEFAULT_CONFIG = os.path.join(ROOT, "config", "thresholds.json")
 
@@ -163,10 +164,12 @@ class Context:
         _check(lib().m3e_set_timing(self._h, int(enable)))
 
     def kernel_times(self):
-        """(filter kernel ms, pack kernel ms) of the last m3e_filter call."""
-        ms = (ctypes.c_float * 2)()
+        """Mean (selection kernel ms, filter kernel ms, pack kernel ms) over the
+        m3e_filter calls since the last reset; the selection kernel is 0 on the
+        single-kernel (M3E_FUSED=1) path."""
+        ms = (ctypes.c_float * 3)()
         _check(lib().m3e_kernel_times(self._h, ms))
-        return float(ms[0]), float(ms[1])
+        return float(ms[0]), float(ms[1]), float(ms[2])
 
 
 def make_outputs(**kw) -> Outputs:
