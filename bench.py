@@ -243,7 +243,7 @@ def main():
         dist.barrier()
     ms = [s.elapsed_time(e) for s, e in ev]
     ms_step = statistics.mean(ms)
-    ms_select, ms_filter, ms_pack = ctx.kernel_times()
+    ms_select, ms_fit, ms_filter, ms_pack = ctx.kernel_times()
     sm = res.summary_np()
     kept = int(sum(sm["kept_by_reason"][1:]))
     assert int(sm["frames"]) == F and not int(sm["overflow"]), "output capacity exceeded"
@@ -316,16 +316,18 @@ def main():
     if rank == 0:
         peak, peak_kind = load_peaks()
         # algorithmic bytes per launch:
-        #   selection kernel: hit stream in + per-frame selection word + candidates out
-        #   filter kernel: hit stream + selection words + candidates in, per-frame
-        #   outputs + tracks + kept records out (fused path: hit stream + outputs)
+        #   selection kernel: hit stream in, selection words (4 B/frame) + store entries (16 B) out
+        #   fit kernel: store entries + the candidates' frames (hit stream) in, fit records (32 B) out
+        #   filter kernel: offsets + selection words + fit records in, per-frame outputs,
+        #   tracks, kept records out (fused path: hit stream in + outputs)
         split = ms_select > 0
         cand = int(sm["candidates"])
         big = H > 60 * F
         if split:
-            sel_bytes = in_bytes + 4 * F + 8 * cand
-            kernels = [("m3e::filter_kernel<SELECT_C, BIG=false>", ms_select, sel_bytes),
-                       ("m3e::filter_kernel<FULL, BIG=false>", ms_filter, sel_bytes + out_bytes)]
+            kernels = [("m3e::filter_kernel<SELECT_C, BIG=false>", ms_select, in_bytes + 4 * F + 16 * cand),
+                       ("m3e::fit_kernel", ms_fit, in_bytes + 16 * cand + 32 * cand),
+                       ("m3e::filter_kernel<FULL, BIG=false>", ms_filter,
+                        16 * F + 4 * F + 32 * cand + out_bytes)]
         else:
             kernels = [("m3e::filter_kernel<FULL, BIG=%s>" % ("true" if big else "false"), ms_filter,
                         in_bytes + out_bytes)]
@@ -353,9 +355,10 @@ def main():
                          "traffic": load_traffic(a.workload, F, a.seed, kname), "peak_kind": peak_kind,
                          "kernel": kname, "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms_step, 4),
                          "algorithmic_bytes_per_launch": int(alg_bytes),
-                         "kernels_ms": {"select": round(ms_select, 4), "filter": round(ms_filter, 4),
-                                        "pack": round(ms_pack, 4)}},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (3 if split else 2) * a.steps, "clocks": clocks,
+                         "kernels_ms": {"select": round(ms_select, 4), "fit": round(ms_fit, 4),
+                                        "filter": round(ms_filter, 4), "pack": round(ms_pack, 4)},
+                         "candidates_per_frame": round(cand / F, 3)},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (4 if split else 2) * a.steps, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -157,14 +157,15 @@ int m3e_destroy(m3e_context* ctx);
 uint64_t m3e_workspace_bytes(const m3e_context* ctx);
 /* Kernel timing: when enabled, every m3e_filter call records CUDA events on its
  * stream around each of its kernels (up to 1024 calls); m3e_kernel_times()
- * waits for them and returns the MEAN durations in ms over those calls
- * (ms[0] = selection kernel of the split path, 0 when the call ran the single
- * fused filter kernel; ms[1] = filter kernel (fit, vertex, output staging);
- * ms[2] = pack kernel), then resets the record.  The split path is the
- * default; M3E_FUSED=1 in the environment at m3e_create selects the single
- * fused kernel (same results). */
+ * waits for them and returns the MEAN durations in ms over those calls, then
+ * resets the record:
+ *   ms[0] selection kernel, ms[1] fit kernel (both 0 when the call ran the
+ *   single fused filter kernel), ms[2] filter kernel (vertex selection and
+ *   output staging; the whole path on the fused variant), ms[3] pack kernel.
+ * The split path is the default; M3E_FUSED=1 in the environment at m3e_create
+ * selects the single fused kernel (same results). */
 int m3e_set_timing(m3e_context* ctx, int enable);
-int m3e_kernel_times(m3e_context* ctx, float ms[3]);
+int m3e_kernel_times(m3e_context* ctx, float ms[4]);
 
 /* Full hot path on device-resident input (the call bench.py times):
  * select -> fit -> vertex -> pack for frames [0, F).  Outputs [dev]. */

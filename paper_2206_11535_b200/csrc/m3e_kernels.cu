@@ -508,19 +508,22 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
         __syncwarp();
 
         if constexpr (MODE == kModeSelectC) {   // candidates -> store, warp-batch contiguous
-            uint32_t tot = 0;
             for (int j = lane; j < nf; j += 32) {
                 A.sel[f0 + j] = (uint32_t)B.ncand[j] | ((uint32_t)B.reason[j] << 16);
-                tot += (uint32_t)B.nstored[j];
+                W.pref[j] = (uint32_t)B.nstored[j];
             }
-            tot = warp_sum(tot);
+            __syncwarp();
+            warp_scan(W.pref, nf);
+            const uint32_t tot = W.pref[nf];
             unsigned long long base = 0;
             if (lane == 0 && tot) base = atomicAdd(reinterpret_cast<unsigned long long*>(A.ticket + 6), tot);
             base = __shfl_sync(0xffffffffu, base, 0);
             const bool fits = base + tot <= A.cand_cap;
-            if (fits) {
-                for (uint32_t e = lane; e < tot; e += 32) {
-                    uint2 c;
+            // a warp-batch that does not fit leaves its (partial) range marked unused
+            const uint32_t nw = fits ? tot : (base < A.cand_cap ? (uint32_t)(A.cand_cap - base) : 0u);
+            for (uint32_t e = lane; e < nw; e += 32) {
+                uint4 c = make_uint4(0u, 0u, kSpilled, 0u);
+                if (fits) {
                     if (e < (uint32_t)kCandSmem) {
                         c.x = W.cidx[e];
                         c.y = __float_as_uint(W.crt[e]);
@@ -528,8 +531,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                         c.x = cidx[e];
                         c.y = __float_as_uint(crt[e]);
                     }
-                    A.cand_g[base + e] = c;
+                    c.z = f0 + (uint32_t)find_frame(W.pref, nf, e);
                 }
+                A.cand_g[base + e] = c;
             }
             if (lane == 0) A.bsel[b] = fits ? (uint32_t)base : kSpilled;
         }
@@ -569,13 +573,21 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                 size_t slot = 0;
                 o.status = 7;
                 if (valid) {
-                    float rt;
+                    float rt = 0.0f;
+                    bool fitted = false;
                     if constexpr (MODE == kModeFull) {   // flat warp-batch candidate index
                         slot = (size_t)e;
-                        if (gbase != kSpilled) {
-                            const uint2 c = A.cand_g[gbase + e];
-                            pk = c.x;
-                            rt = __uint_as_float(c.y);
+                        if (gbase != kSpilled) {   // fitted by fit_kernel
+                            const m3e_track r = A.fit_g[gbase + e];
+                            pk = (uint32_t)r.hit[0] | ((uint32_t)r.hit[1] << 10) | ((uint32_t)r.hit[2] << 20);
+                            o.status = r.frame == kSpilled ? 1 : 0;
+                            o.hit3 = r.hit[3];
+                            o.kappa = r.kappa;
+                            o.chi2 = r.chi2;
+                            o.cth01 = r.cos_theta01;
+                            o.cx = r.cx;
+                            o.cy = r.cy;
+                            fitted = true;
                         } else if (e < kCandSmem) {
                             pk = W.cidx[e];
                             rt = W.crt[e];
@@ -588,8 +600,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                         pk = cidx[slot];
                         rt = crt[slot];
                     }
-                    const Frame Fv = frame_view(A, W, buf, j);
-                    o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
+                    if (!fitted) {
+                        const Frame Fv = frame_view(A, W, buf, j);
+                        o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
+                    }
                 }
                 if constexpr (MODE == kModeFit) {   // per-candidate record (stage tap)
                     if (valid) {
@@ -666,13 +680,16 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
 
         // --------------------------------------------- V: vertex selection (fp64)
         if constexpr (MODE == kModeFull || MODE == kModeVertex) {
-            for (int j = 0; j < nf; ++j) {
-                if constexpr (MODE == kModeFull) {   // charge counts known from F: skip frames without e+e+e-
-                    if (B.reason[j] != M3E_REASON_NONE || W.npos[j] < 2 || B.nneg[j] < 1) {
-                        if (lane == 0) B.ncomb[j] = 0;
-                        continue;
-                    }
-                }
+            // FULL: charge counts known from F, only frames with e+e+e- candidates
+            // (nf <= kFB <= 32: one lane per frame)
+            bool need = lane < nf;
+            if constexpr (MODE == kModeFull) {
+                need = need && B.reason[lane] == M3E_REASON_NONE && W.npos[lane] >= 2 && B.nneg[lane] >= 1;
+                if (lane < nf && !need) B.ncomb[lane] = 0;
+            }
+            __syncwarp();
+            for (unsigned todo = __ballot_sync(0xffffffffu, need); todo; todo &= todo - 1) {
+                const int j = __ffs(todo) - 1;
                 const Frame Fv = frame_view(A, W, buf, j);
                 vertex_frame(&S.P, V, B, j, ctrk + tfirst + (size_t)j * P.max_tracks, Fv, f0);
                 __syncwarp();
@@ -970,6 +987,64 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const KArgs A) {
             atomicExch((unsigned long long*)&O.summary->overflow, 1ull);
         __syncthreads();
     }
+}
+
+// ------------------------------------------------------------ fit kernel ----
+// Split path, F: the triplet fit of every candidate in the store, one thread per
+// candidate (dense lanes; the frame's hits are read through L1/L2, consecutive
+// candidates share frames).  Record c = the accepted track, frame = kSpilled
+// when the fit rejects it (status != 0).  PAPER.md Sec. III-C, Eqs. 5-8.
+#ifndef M3E_FIT_MIN_BLOCKS
+#define M3E_FIT_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const __grid_constant__ KArgs A) {
+    const unsigned long long filled = *reinterpret_cast<const volatile unsigned long long*>(A.ticket + 6);
+    const uint64_t n = filled < A.cand_cap ? filled : A.cand_cap;
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t c = (uint64_t)blockIdx.x * kThreads + threadIdx.x; c < n; c += stride) {
+        const uint4 e = A.cand_g[c];
+        if (e.z == kSpilled) continue;
+        const uint4 o4 = *reinterpret_cast<const uint4*>(A.offsets + 4 * (size_t)e.z);
+        const uint32_t o5 = A.offsets[4 * (size_t)e.z + 4];
+        Frame F;
+        F.x = A.x + o4.x;
+        F.y = A.y + o4.x;
+        F.z = A.z + o4.x;
+        F.s[0] = 0;
+        F.s[1] = (int)(o4.y - o4.x);
+        F.s[2] = (int)(o4.z - o4.x);
+        F.s[3] = (int)(o4.w - o4.x);
+        F.n[0] = F.s[1];
+        F.n[1] = (int)(o4.z - o4.y);
+        F.n[2] = (int)(o4.w - o4.z);
+        F.n[3] = (int)(o5 - o4.w);
+        const uint32_t pk = e.x;
+        const FitOut o = fit_candidate(A.P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u,
+                                       __uint_as_float(e.y));
+        m3e_track t;
+        t.frame = o.status == 0 ? e.z : kSpilled;
+        t.hit[0] = (uint16_t)(pk & 1023u);
+        t.hit[1] = (uint16_t)((pk >> 10) & 1023u);
+        t.hit[2] = (uint16_t)((pk >> 20) & 1023u);
+        t.hit[3] = (uint16_t)o.hit3;
+        t.kappa = o.kappa;
+        t.chi2 = o.chi2;
+        t.cos_theta01 = o.cth01;
+        t.cx = o.cx;
+        t.cy = o.cy;
+        A.fit_g[c] = t;
+    }
+}
+
+cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s) {
+    fit_kernel<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+int fit_blocks_per_sm() {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fit_kernel, kThreads, 0) != cudaSuccess) return 1;
+    return n > 0 ? n : 1;
 }
 
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s) {

@@ -65,7 +65,9 @@ struct KArgs {
     uint32_t* bticket;     // this launch's warp-batch ticket (ticket + 0 or ticket + 4)
     // candidate store of the split path (kModeSelectC writes, kModeFull + presel reads)
     int presel;            // kModeFull: take candidates from the store (batches not spilled)
-    uint2* cand_g;         // {packed hit indices, r_tc bits}, warp-batch contiguous, frame order
+    uint4* cand_g;         // {packed hit indices, r_tc bits, frame, 0}, warp-batch contiguous, frame
+                           // order; frame = kSpilled marks an unused entry
+    m3e_track* fit_g;      // fit of store entry c (fit_kernel); frame = kSpilled: not accepted
     uint64_t cand_cap;     // entries of cand_g (< 2^32)
     uint32_t* sel;         // [F] per frame: n_cand | reason << 16
     uint32_t* bsel;        // [nbatch] first store entry of the warp-batch, or kSpilled
@@ -101,6 +103,8 @@ struct KArgs {
 size_t smem_bytes();
 cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s);
+int fit_blocks_per_sm();
 int blocks_per_sm(int mode, bool big);
 
 }  // namespace m3e

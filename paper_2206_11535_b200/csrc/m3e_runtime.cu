@@ -59,7 +59,8 @@ struct Workspace {
     uint32_t* pair_scratch = nullptr;   // big-frame selection lists, kPairWords per warp
     int pair_warps = 0;
     void* vscratch = nullptr;           // vertex-stage scratch, kVScratchBytes per warp
-    uint2* cand_g = nullptr;            // candidate store of the split path
+    uint4* cand_g = nullptr;            // candidate store of the split path
+    m3e_track* fit_g = nullptr;         // fit records of the store entries
     size_t cand_n = 0;
     uint32_t* sel = nullptr;            // per-frame selection words of the split path
     size_t sel_n = 0;
@@ -98,7 +99,8 @@ struct m3e_context {
     uint64_t chunk_frames = 0;
     bool timing = false;
     bool split = true;              // two-kernel production path (M3E_FUSED=1 in the environment: one kernel)
-    std::vector<cudaEvent_t> tev;   // 4 events per timed m3e_filter call
+    uint64_t cand_per_frame = 16;   // candidate-store entries per frame (M3E_CAND_STORE; tests force spills)
+    std::vector<cudaEvent_t> tev;   // 5 events per timed m3e_filter call
     size_t tev_used = 0;
     size_t tev_split = 0;           // timed calls that ran the split path
 };
@@ -107,6 +109,7 @@ namespace {
 
 void free_ws(Workspace& w) {
     cudaFree(w.cand_g);
+    cudaFree(w.fit_g);
     cudaFree(w.sel);
     cudaFree(w.bsel);
     cudaFree(w.pair_scratch);
@@ -252,15 +255,18 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
 // split path: candidate store (kCandPerFrame entries per frame; warp-batches
 // that do not fit are flagged and re-selected by the filter kernel), per-frame
 // selection words and per-warp-batch store offsets
-constexpr uint64_t kCandPerFrame = 24;
-int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch) {
-    const uint64_t nc = std::min<uint64_t>(std::max<uint64_t>(kCandPerFrame * F, 1u << 16), 0xFFFFFFF0ull);
+constexpr uint64_t kCandPerFrame = 16;
+int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame) {
+    const uint64_t nc = std::min<uint64_t>(std::max<uint64_t>(per_frame * F, 1u << 10), 0xFFFFFFF0ull);
     if (w.cand_n < nc) {
         cudaFree(w.cand_g);
-        w.bytes -= w.cand_n * sizeof(uint2);
-        CK(cudaMalloc(&w.cand_g, nc * sizeof(uint2)));
+        cudaFree(w.fit_g);
+        w.bytes -= w.cand_n * (sizeof(uint4) + sizeof(m3e_track));
+        w.cand_n = 0;
+        CK(cudaMalloc(&w.cand_g, nc * sizeof(uint4)));
+        CK(cudaMalloc(&w.fit_g, nc * sizeof(m3e_track)));
         w.cand_n = nc;
-        w.bytes += nc * sizeof(uint2);
+        w.bytes += nc * (sizeof(uint4) + sizeof(m3e_track));
     }
     if (w.sel_n < F) {
         cudaFree(w.sel);
@@ -327,7 +333,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     rc = ensure_ws(ctx, w, nbatch, p, fb, std::max(grid, sgrid));
     if (rc) return rc;
     if (split) {
-        rc = ensure_split(w, F, nbatch);
+        rc = ensure_split(w, F, nbatch, ctx->cand_per_frame);
         if (rc) return rc;
     }
     a.P = make_dev_params(p);
@@ -357,34 +363,39 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     }
     CK(cudaMemsetAsync(w.ticket, 0, 8 * sizeof(uint32_t), s));
     if (a.out.summary) CK(cudaMemsetAsync(a.out.summary, 0, sizeof(m3e_summary), s));
-    const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + 4 <= ctx->tev.size();
+    const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + 5 <= ctx->tev.size();
     cudaEvent_t* ev = tm ? &ctx->tev[ctx->tev_used] : nullptr;
     if (tm) CK(cudaEventRecord(ev[0], s));
     if (split) {
         KArgs sa = a;
         sa.cand_g = w.cand_g;
-        sa.cand_cap = w.cand_n;
+        sa.cand_cap = std::min<uint64_t>(w.cand_n, std::max<uint64_t>(ctx->cand_per_frame * F, 1u << 10));
         sa.sel = w.sel;
         sa.bsel = w.bsel;
         CK(launch_filter(kModeSelectC, false, sa, sgrid, s));
+        if (tm) CK(cudaEventRecord(ev[1], s));
         a.presel = 1;
         a.cand_g = w.cand_g;
-        a.cand_cap = w.cand_n;
+        a.fit_g = w.fit_g;
+        a.cand_cap = sa.cand_cap;
         a.sel = w.sel;
         a.bsel = w.bsel;
         a.bticket = w.ticket + 4;
+        CK(launch_fit(a, ctx->sms * fit_blocks_per_sm(), s));
+    } else if (tm) {
+        CK(cudaEventRecord(ev[1], s));
     }
-    if (tm) CK(cudaEventRecord(ev[1], s));
-    CK(launch_filter(mode, big, a, grid, s));
     if (tm) CK(cudaEventRecord(ev[2], s));
+    CK(launch_filter(mode, big, a, grid, s));
+    if (tm) CK(cudaEventRecord(ev[3], s));
     if (packs) {
         const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
         const int pgrid = (int)std::min<uint64_t>(ntiles, (uint64_t)ctx->sms * 8);
         CK(launch_pack(a, pgrid, s));
     }
     if (tm) {
-        CK(cudaEventRecord(ev[3], s));
-        ctx->tev_used += 4;
+        CK(cudaEventRecord(ev[4], s));
+        ctx->tev_used += 5;
         ctx->tev_split += split ? 1 : 0;
     }
     return M3E_OK;
@@ -413,6 +424,8 @@ int m3e_create(m3e_context** out, int device, uint64_t max_frames, uint64_t max_
     c->max_hits = max_hits;
     const char* fused = std::getenv("M3E_FUSED");
     c->split = !(fused && fused[0] == '1');
+    if (const char* cs = std::getenv("M3E_CAND_STORE")) c->cand_per_frame = std::strtoull(cs, nullptr, 10);
+    else c->cand_per_frame = kCandPerFrame;
     for (int i = 0; i < 2; ++i) {
         if (cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) != cudaSuccess) {
             delete c;
@@ -443,7 +456,7 @@ int m3e_set_timing(m3e_context* c, int enable) {
     if (!c) return fail(M3E_ERR_INVALID_ARGUMENT, "ctx is NULL");
     CK(cudaSetDevice(c->device));
     if (enable && c->tev.empty()) {
-        c->tev.resize(4 * 1024);   // up to 1024 timed calls between two m3e_kernel_times()
+        c->tev.resize(5 * 1024);   // up to 1024 timed calls between two m3e_kernel_times()
         for (auto& e : c->tev) CK(cudaEventCreate(&e));
     }
     c->timing = enable != 0;
@@ -452,21 +465,21 @@ int m3e_set_timing(m3e_context* c, int enable) {
     return M3E_OK;
 }
 
-int m3e_kernel_times(m3e_context* c, float ms[3]) {
+int m3e_kernel_times(m3e_context* c, float ms[4]) {
     if (!c || !ms) return fail(M3E_ERR_INVALID_ARGUMENT, "NULL argument");
     if (c->tev_used == 0) return fail(M3E_ERR_INVALID_ARGUMENT, "no timed call since the last reset");
-    double acc[3] = {0, 0, 0};
-    const size_t n = c->tev_used / 4;
+    double acc[4] = {0, 0, 0, 0};
+    const size_t n = c->tev_used / 5;
     for (size_t i = 0; i < n; ++i) {
-        CK(cudaEventSynchronize(c->tev[4 * i + 3]));
-        for (int k = 0; k < 3; ++k) {
+        CK(cudaEventSynchronize(c->tev[5 * i + 4]));
+        for (int k = 0; k < 4; ++k) {
             float t = 0;
-            CK(cudaEventElapsedTime(&t, c->tev[4 * i + k], c->tev[4 * i + k + 1]));
+            CK(cudaEventElapsedTime(&t, c->tev[5 * i + k], c->tev[5 * i + k + 1]));
             acc[k] += t;
         }
     }
-    for (int k = 0; k < 3; ++k) ms[k] = (float)(acc[k] / n);
-    if (c->tev_split == 0) ms[0] = 0.0f;   // no selection kernel ran (fused path)
+    for (int k = 0; k < 4; ++k) ms[k] = (float)(acc[k] / n);
+    if (c->tev_split == 0) ms[0] = ms[1] = 0.0f;   // fused path: no selection / fit kernel ran
     c->tev_used = 0;
     c->tev_split = 0;
     return M3E_OK;

@@ -164,12 +164,12 @@ class Context:
         _check(lib().m3e_set_timing(self._h, int(enable)))
 
     def kernel_times(self):
-        """Mean (selection kernel ms, filter kernel ms, pack kernel ms) over the
-        m3e_filter calls since the last reset; the selection kernel is 0 on the
-        single-kernel (M3E_FUSED=1) path."""
-        ms = (ctypes.c_float * 3)()
+        """Mean (selection, fit, filter, pack) kernel ms over the m3e_filter calls
+        since the last reset; selection and fit are 0 on the single-kernel
+        (M3E_FUSED=1) path, where the filter kernel runs every stage."""
+        ms = (ctypes.c_float * 4)()
         _check(lib().m3e_kernel_times(self._h, ms))
-        return float(ms[0]), float(ms[1]), float(ms[2])
+        return tuple(float(v) for v in ms)
 
 
 def make_outputs(**kw) -> Outputs:

@@ -257,6 +257,39 @@ def test_full_parity(ctx, gp, P, name, n, seed):
         assert np.all(np.diff(tracks_np["frame"].astype(np.int64)) >= 0)
 
 
+def _outputs(res, n):
+    sm = res.summary_np()
+    T, K = int(sm["tracks"]), int(sum(sm["kept_by_reason"][1:]))
+    return (res.reason.cpu().numpy()[:n].copy(), res.frames_np(n).copy(), res.tracks_np(T).copy(),
+            res.kept_frame.cpu().numpy()[:K].copy(), res.vertices_np(K).copy(), sm.copy())
+
+
+@pytest.mark.parametrize("store", ["0", "2"])
+def test_split_spill_and_fused_agree(gp, monkeypatch, store):
+    """The production path runs the Selection Cuts in their own kernel and
+    hands candidates to the fit kernel through a bounded store; warp-batches
+    that do not fit are re-selected inside the fit kernel.  Forcing spills
+    (M3E_CAND_STORE entries per frame, read at m3e_create) and the single fused
+    kernel (M3E_FUSED=1) must give byte-identical outputs."""
+    n = 6000
+    d, fr, df = _gen("signal_only", n, 701)   # ~30 candidates per frame: store of 2/frame spills
+    outs = []
+    for env in [{}, {"M3E_CAND_STORE": store}, {"M3E_FUSED": "1"}]:
+        for k in ["M3E_CAND_STORE", "M3E_FUSED"]:
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        c = m3e.Context(0)
+        res = m3e.run_filter(c, gp, df)
+        torch.cuda.synchronize()
+        outs.append(_outputs(res, n))
+        c.close()
+    assert int(outs[0][5]["overflow"]) == 0
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+
+
 def test_host_path_matches_device(ctx, gp):
     """m3e_filter_host (chunked, two streams) == m3e_filter on the same frames."""
     n = 5000
