@@ -318,16 +318,16 @@ def main():
         # algorithmic bytes per launch:
         #   selection kernel: hit stream in, selection words (4 B/frame) + store entries (16 B) out
         #   fit kernel: store entries + the candidates' frames (hit stream) in, fit records (32 B) out
-        #   filter kernel: offsets + selection words + fit records in, per-frame outputs,
-        #   tracks, kept records out (fused path: hit stream in + outputs)
+        #   finish kernel (+ the fused kernel over spilled warp-batches, ~0): offsets +
+        #   selection words + fit records in, per-frame outputs, tracks, kept records out
+        #   (fused path: one kernel, hit stream in + outputs)
         split = ms_select > 0
         cand = int(sm["candidates"])
         big = H > 60 * F
         if split:
             kernels = [("m3e::filter_kernel<SELECT_C, BIG=false>", ms_select, in_bytes + 4 * F + 16 * cand),
                        ("m3e::fit_kernel", ms_fit, in_bytes + 16 * cand + 32 * cand),
-                       ("m3e::filter_kernel<FULL, BIG=false>", ms_filter,
-                        16 * F + 4 * F + 32 * cand + out_bytes)]
+                       ("m3e::finish_kernel", ms_filter, 16 * F + 4 * F + 32 * cand + out_bytes)]
         else:
             kernels = [("m3e::filter_kernel<FULL, BIG=%s>" % ("true" if big else "false"), ms_filter,
                         in_bytes + out_bytes)]
@@ -356,7 +356,7 @@ def main():
                          "kernel": kname, "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms_step, 4),
                          "algorithmic_bytes_per_launch": int(alg_bytes),
                          "kernels_ms": {"select": round(ms_select, 4), "fit": round(ms_fit, 4),
-                                        "filter": round(ms_filter, 4), "pack": round(ms_pack, 4)},
+                                        "finish": round(ms_filter, 4), "pack": round(ms_pack, 4)},
                          "candidates_per_frame": round(cand / F, 3)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (4 if split else 2) * a.steps, "clocks": clocks,
         }

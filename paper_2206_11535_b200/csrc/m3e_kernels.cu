@@ -105,7 +105,7 @@ constexpr int kCandSmem = 256;   // candidates of a warp-batch kept in shared me
 // Cold vertex-stage scratch of one warp, in global memory (L1/L2 resident;
 // touched for ~1.5% of frames), so that it does not cost shared memory.
 struct VScratch {
-    m3e_vertex vtx[kFB];
+    m3e_vertex vtx[32];   // by frame lane: kFB frames of a warp-batch, 32 of a finish-kernel group
     uint32_t vcomb[kMaxCombsCap];
     uint8_t vlist[2][kMaxTracksCap];
 };
@@ -158,6 +158,14 @@ __device__ __forceinline__ Frame frame_view(const KArgs& A, const WarpSmem& W, i
 }
 
 // lane 0: claim warp-batch b into buffer buf and start its bulk copies
+// next warp-batch of this launch (>= nbatch: none left); the split path's fused
+// launch only takes the warp-batches the selection kernel could not store
+__device__ __forceinline__ uint32_t claim_batch(const KArgs& A) {
+    const uint32_t t = atomicAdd(A.bticket, 1u);
+    if (!A.spill_list) return t;
+    return t < *reinterpret_cast<volatile const uint32_t*>(A.ticket + 5) ? A.spill_list[t] : A.nbatch;
+}
+
 __device__ __forceinline__ void issue_load(const KArgs& A, WarpSmem& W, int buf, uint32_t b) {
     W.b_batch[buf] = b;
     if (b >= A.nbatch) return;
@@ -251,15 +259,21 @@ __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) 
 // Vertex selection of frame j (Sec. IV-C, Alg. 4; whole warp), out of line: it
 // runs for ~1.5% of frames and keeps its fp64 registers and code out of the
 // main loop.
-static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ Pp, VScratch& V, BatchState& B,
-                                                 int j, const m3e_track* tj, const Frame& Fv, uint32_t f0) {
+// nt accepted tracks tj[0..nt) of frame `frame` (reason none); returns the
+// combination count (max_combs + 1 on overflow) and the negative-track count;
+// the vertex, if any, goes to *vout.
+struct VOut {
+    int ncomb, nneg, vtx;
+};
+static __device__ __noinline__ VOut vertex_frame(const DevParams* __restrict__ Pp, VScratch& V, int nt,
+                                                 const m3e_track* tj, const Frame& Fv, uint32_t frame,
+                                                 m3e_vertex* vout) {
     const DevParams& P = *Pp;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     int ncomb = 0, nneg_out = 0;
     bool has_vtx = false;
-    if (B.reason[j] == M3E_REASON_NONE) {
-        const int nt = min(B.ntrk[j], P.max_tracks);
+    {
         // charge-sorted index lists, in track order
         int npos = 0, nneg = 0;
         for (int i0 = 0; i0 < nt; i0 += 32) {
@@ -331,7 +345,7 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
                     if (bidx == widx) {
                         const uint32_t code = V.vcomb[widx];
                         m3e_vertex v;
-                        v.frame = f0 + j;
+                        v.frame = frame;
                         v.track[0] = (uint16_t)(code & 255u);
                         v.track[1] = (uint16_t)((code >> 8) & 255u);
                         v.track[2] = (uint16_t)((code >> 16) & 255u);
@@ -341,20 +355,30 @@ static __device__ __noinline__ void vertex_frame(const DevParams* __restrict__ P
                         v.chi2 = bres.chi2;
                         v.target_dist = (float)bres.tdist;
                         v.p_total = (float)bres.ptot;
-                        V.vtx[j] = v;
+                        *vout = v;
                     }
                 }
             }
         }
-        if (lane == 0) {
-            B.ncomb[j] = ncomb;
-            B.nneg[j] = nneg_out;
-            if (ncomb > P.max_combs) B.reason[j] = M3E_REASON_COMB_OVERFLOW;
-            else if (has_vtx) B.reason[j] = M3E_REASON_VERTEX;
-        }
-    } else if (lane == 0) {
-        B.ncomb[j] = 0;
     }
+    VOut r;
+    r.ncomb = ncomb;
+    r.nneg = nneg_out;
+    r.vtx = has_vtx ? 1 : 0;
+    return r;
+}
+
+// per-warp run summary -> the call's m3e_summary (one lane)
+__device__ __forceinline__ void flush_summary(m3e_summary* sm, const uint32_t* acc) {
+    typedef unsigned long long u64;
+    if (acc[7]) atomicAdd((u64*)&sm->frames, (u64)acc[7]);
+    for (int i = 0; i < 6; ++i)
+        if (acc[i]) atomicAdd((u64*)&sm->kept_by_reason[i], (u64)acc[i]);
+    if (acc[6]) atomicAdd((u64*)&sm->candidates, (u64)acc[6]);
+    if (acc[8]) atomicAdd((u64*)&sm->tracks, (u64)acc[8]);
+    if (acc[9]) atomicAdd((u64*)&sm->kept_hits, (u64)acc[9]);
+    if (acc[M3E_REASON_VERTEX]) atomicAdd((u64*)&sm->vertices, (u64)acc[M3E_REASON_VERTEX]);
+    if (acc[10]) atomicExch((u64*)&sm->overflow, 1ull);
 }
 
 // ------------------------------------------------------------------ kernel ----
@@ -377,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
         fence_mbar_init();
     }
     __syncthreads();   // the only CTA barrier before the final summary flush
-    if (lane == 0) issue_load(A, W, 0, atomicAdd(A.bticket, 1u));
+    if (lane == 0) issue_load(A, W, 0, claim_batch(A));
     __syncwarp();
     int buf = 0;
     uint32_t phase[kNBuf] = {};
@@ -406,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
     for (;;) {
         const uint32_t b = W.b_batch[buf];
         if (b >= A.nbatch) break;
-        if (kNBuf == 2 && lane == 0) issue_load(A, W, buf ^ 1, atomicAdd(A.bticket, 1u));
+        if (kNBuf == 2 && lane == 0) issue_load(A, W, buf ^ 1, claim_batch(A));
         mbar_wait(&W.bar[buf], phase[buf]);
         phase[buf] ^= 1u;
 
@@ -417,21 +441,6 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
         const size_t tfirst = MODE == kModeFull ? 0 : (size_t)f0 * P.max_tracks;
         m3e_track* ctrk = ctrk_base;
 
-        // split path: the Selection Cuts already ran (kModeSelectC) unless the
-        // warp-batch's candidates did not fit the store
-        uint32_t gbase = kSpilled;
-        if constexpr (MODE == kModeFull && !BIG) {
-            if (A.presel) gbase = A.bsel[b];
-        }
-        if (gbase != kSpilled) {
-            for (int j = lane; j < nf; j += 32) {
-                const uint32_t w = A.sel[f0 + j];
-                const int r = (int)(w >> 16), n = (int)(w & 0xFFFFu);
-                B.ncand[j] = n;
-                B.reason[j] = r;
-                B.nstored[j] = r == M3E_REASON_NONE ? n : 0;
-            }
-        } else
         // ---------------------------------------------------- S: Selection Cuts
         if constexpr (MODE == kModeFull || MODE == kModeSelect || MODE == kModeSelectC) {
             uint32_t cbase = 0;   // flat: candidate index of frame j's first candidate
@@ -535,7 +544,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                 }
                 A.cand_g[base + e] = c;
             }
-            if (lane == 0) A.bsel[b] = fits ? (uint32_t)base : kSpilled;
+            if (lane == 0) {
+                A.bsel[b] = fits ? (uint32_t)base : kSpilled;
+                if (!fits) A.spill_out[atomicAdd(A.ticket + 5, 1u)] = b;   // for the fused kernel
+            }
         }
 
         if constexpr (MODE == kModeSelect) {
@@ -573,22 +585,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                 size_t slot = 0;
                 o.status = 7;
                 if (valid) {
-                    float rt = 0.0f;
-                    bool fitted = false;
+                    float rt;
                     if constexpr (MODE == kModeFull) {   // flat warp-batch candidate index
                         slot = (size_t)e;
-                        if (gbase != kSpilled) {   // fitted by fit_kernel
-                            const m3e_track r = A.fit_g[gbase + e];
-                            pk = (uint32_t)r.hit[0] | ((uint32_t)r.hit[1] << 10) | ((uint32_t)r.hit[2] << 20);
-                            o.status = r.frame == kSpilled ? 1 : 0;
-                            o.hit3 = r.hit[3];
-                            o.kappa = r.kappa;
-                            o.chi2 = r.chi2;
-                            o.cth01 = r.cos_theta01;
-                            o.cx = r.cx;
-                            o.cy = r.cy;
-                            fitted = true;
-                        } else if (e < kCandSmem) {
+                        if (e < kCandSmem) {
                             pk = W.cidx[e];
                             rt = W.crt[e];
                         } else {
@@ -600,10 +600,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                         pk = cidx[slot];
                         rt = crt[slot];
                     }
-                    if (!fitted) {
-                        const Frame Fv = frame_view(A, W, buf, j);
-                        o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
-                    }
+                    const Frame Fv = frame_view(A, W, buf, j);
+                    o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
                 }
                 if constexpr (MODE == kModeFit) {   // per-candidate record (stage tap)
                     if (valid) {
@@ -691,7 +689,18 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
             for (unsigned todo = __ballot_sync(0xffffffffu, need); todo; todo &= todo - 1) {
                 const int j = __ffs(todo) - 1;
                 const Frame Fv = frame_view(A, W, buf, j);
-                vertex_frame(&S.P, V, B, j, ctrk + tfirst + (size_t)j * P.max_tracks, Fv, f0);
+                if (B.reason[j] == M3E_REASON_NONE) {
+                    const VOut r = vertex_frame(&S.P, V, min(B.ntrk[j], P.max_tracks),
+                                                ctrk + tfirst + (size_t)j * P.max_tracks, Fv, f0 + j, &V.vtx[j]);
+                    if (lane == 0) {
+                        B.ncomb[j] = r.ncomb;
+                        B.nneg[j] = r.nneg;
+                        if (r.ncomb > P.max_combs) B.reason[j] = M3E_REASON_COMB_OVERFLOW;
+                        else if (r.vtx) B.reason[j] = M3E_REASON_VERTEX;
+                    }
+                } else if (lane == 0) {
+                    B.ncomb[j] = 0;
+                }
                 __syncwarp();
             }
         }
@@ -814,25 +823,14 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
         if constexpr (kNBuf == 2) {
             buf ^= 1;
         } else if (lane == 0) {
-            issue_load(A, W, 0, atomicAdd(A.bticket, 1u));
+            issue_load(A, W, 0, claim_batch(A));
         }
         __syncwarp();
     }
 
     if constexpr (kOut) {
         __syncwarp();
-        if (lane == 0 && A.out.summary) {
-            m3e_summary* sm = A.out.summary;
-            typedef unsigned long long u64;
-            if (W.acc[7]) atomicAdd((u64*)&sm->frames, (u64)W.acc[7]);
-            for (int i = 0; i < 6; ++i)
-                if (W.acc[i]) atomicAdd((u64*)&sm->kept_by_reason[i], (u64)W.acc[i]);
-            if (W.acc[6]) atomicAdd((u64*)&sm->candidates, (u64)W.acc[6]);
-            if (W.acc[8]) atomicAdd((u64*)&sm->tracks, (u64)W.acc[8]);
-            if (W.acc[9]) atomicAdd((u64*)&sm->kept_hits, (u64)W.acc[9]);
-            if (W.acc[M3E_REASON_VERTEX]) atomicAdd((u64*)&sm->vertices, (u64)W.acc[M3E_REASON_VERTEX]);
-            if (W.acc[10]) atomicExch((u64*)&sm->overflow, 1ull);
-        }
+        if (lane == 0 && A.out.summary) flush_summary(A.out.summary, W.acc);
     }
 }
 
@@ -1034,6 +1032,236 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
         t.cy = o.cy;
         A.fit_g[c] = t;
     }
+}
+
+// --------------------------------------------------------- finish kernel ----
+// Split path, T + V + O for the warp-batches fitted by fit_kernel: one warp
+// takes G = 32 / fb consecutive warp-batches at a time, one lane per frame, so
+// every global round trip serves up to 32 frames.  Results are identical to the
+// fused kernel's stages T, V and O (frame records warp-batch relative, tracks
+// and kept-frame records staged, BatchStat per warp-batch for the pack kernel).
+__device__ __forceinline__ uint32_t warp_incl(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+struct FinishSmem {
+    DevParams P;
+    uint32_t acc[kWarps][12];
+};
+
+#ifndef M3E_FINISH_MIN_BLOCKS
+#define M3E_FINISH_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel(const __grid_constant__ KArgs A) {
+    __shared__ FinishSmem S;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const DevParams& P = A.P;
+    const size_t gwarp = (size_t)blockIdx.x * kWarps + warp;
+    VScratch& V = reinterpret_cast<VScratch*>(A.vscratch)[gwarp];
+    m3e_track* pool = A.pool_trk + gwarp * A.trk_stride;   // tracks of the frame under vertex selection
+    if (tid == 0) S.P = A.P;
+    if (lane < 12) S.acc[warp][lane] = 0u;
+    __syncthreads();
+    const m3e_outputs& O = A.out;
+    const int fb = A.fb;
+    const int G = 32 / fb;                      // warp-batches per group (fb <= kFB <= 16)
+    const int bl = lane / fb;                   // this lane's warp-batch within the group
+    const int fl = bl * fb;                     // its first lane
+    const uint32_t ngroups = (A.nbatch + G - 1) / G;
+    const uint32_t nwarps = gridDim.x * kWarps;
+    bool overflow = false;
+    for (uint32_t g = (uint32_t)gwarp; g < ngroups; g += nwarps) {
+        const uint32_t b = g * (uint32_t)G + (uint32_t)bl;
+        const uint32_t f = b * (uint32_t)fb + (uint32_t)(lane - fl);
+        const bool inb = bl < G && b < A.nbatch;
+        uint32_t gb = kSpilled;
+        if (inb) gb = A.bsel[b];
+        const bool active = inb && gb != kSpilled && f < A.F;   // spilled warp-batches: fused kernel
+        int ncand = 0, reason = M3E_REASON_NONE;
+        uint32_t nst = 0;
+        if (active) {
+            const uint32_t w = A.sel[f];
+            ncand = (int)(w & 0xFFFFu);
+            reason = (int)(w >> 16);
+            nst = reason == M3E_REASON_NONE ? (uint32_t)ncand : 0u;
+        }
+        // first store entry of the frame: warp-batch base + prefix within the warp-batch
+        const uint32_t cex = warp_incl(nst) - nst;
+        const uint32_t cs = gb + cex - __shfl_sync(0xffffffffu, cex, fl);
+        // T: accepted tracks of the frame and their charges (candidate order)
+        int cnt = 0, nneg = 0, npos = 0;
+        for (uint32_t k = 0; k < nst; ++k) {
+            const m3e_track* r = A.fit_g + cs + k;
+            if (r->frame != kSpilled) {
+                const float kap = r->kappa;
+                nneg += (cnt < P.max_tracks && kap < 0.0f) ? 1 : 0;
+                npos += (cnt < P.max_tracks && kap > 0.0f) ? 1 : 0;
+                ++cnt;
+            }
+        }
+        if (active && reason == M3E_REASON_NONE && cnt > P.max_tracks) {
+            reason = M3E_REASON_TRACK_OVERFLOW;
+            nneg = 0;
+        }
+        const int ntrk = min(cnt, P.max_tracks + 1);
+        // V: frames with e+e+e- candidates, whole warp per frame
+        int ncomb = 0;
+        const bool need = active && reason == M3E_REASON_NONE && npos >= 2 && nneg >= 1;
+        for (unsigned todo = __ballot_sync(0xffffffffu, need); todo; todo &= todo - 1) {
+            const int j = __ffs(todo) - 1;
+            const uint32_t csj = __shfl_sync(0xffffffffu, cs, j), nj = __shfl_sync(0xffffffffu, nst, j);
+            const uint32_t fj = __shfl_sync(0xffffffffu, f, j);
+            int n = 0;
+            for (uint32_t k0 = 0; k0 < nj; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                const bool acc = k < nj && A.fit_g[csj + k].frame != kSpilled;
+                const unsigned m = __ballot_sync(0xffffffffu, acc);
+                const int pos = n + __popc(m & lt_mask);
+                if (acc && pos < P.max_tracks) {
+                    m3e_track t = A.fit_g[csj + k];
+                    pool[pos] = t;
+                }
+                n += __popc(m);
+            }
+            __syncwarp();
+            Frame Fv;
+            {
+                const uint4 o4 = *reinterpret_cast<const uint4*>(A.offsets + 4 * (size_t)fj);
+                const uint32_t o5 = A.offsets[4 * (size_t)fj + 4];
+                Fv.x = A.x + o4.x;
+                Fv.y = A.y + o4.x;
+                Fv.z = A.z + o4.x;
+                Fv.s[0] = 0;
+                Fv.s[1] = (int)(o4.y - o4.x);
+                Fv.s[2] = (int)(o4.z - o4.x);
+                Fv.s[3] = (int)(o4.w - o4.x);
+                Fv.n[0] = Fv.s[1];
+                Fv.n[1] = (int)(o4.z - o4.y);
+                Fv.n[2] = (int)(o4.w - o4.z);
+                Fv.n[3] = (int)(o5 - o4.w);
+            }
+            const VOut r = vertex_frame(&S.P, V, min(n, P.max_tracks), pool, Fv, fj, &V.vtx[j]);
+            if (lane == j) {
+                ncomb = r.ncomb;
+                nneg = r.nneg;
+                if (r.ncomb > P.max_combs) reason = M3E_REASON_COMB_OVERFLOW;
+                else if (r.vtx) reason = M3E_REASON_VERTEX;
+            }
+            __syncwarp();
+        }
+        // O: frame records in place (warp-batch relative offsets), tracks and kept
+        // frames staged, BatchStat per warp-batch
+        const bool kept = active && reason != M3E_REASON_NONE;
+        const bool has_tracks = active && reason != M3E_REASON_TRIPLET_OVERFLOW && reason != M3E_REASON_INVALID;
+        const uint32_t o_trk = has_tracks ? (uint32_t)min(ntrk, P.max_tracks) : 0u;
+        const uint32_t o_kept = kept ? 1u : 0u;
+        uint32_t o_hits = 0;
+        if (kept) o_hits = A.offsets[4 * (size_t)f + 4] - A.offsets[4 * (size_t)f];
+        const uint32_t i_trk = warp_incl(o_trk), i_kept = warp_incl(o_kept), i_hits = warp_incl(o_hits);
+        const uint32_t e_trk = i_trk - o_trk, e_kept = i_kept - o_kept, e_hits = i_hits - o_hits;
+        uint32_t s_trk = 0, s_kept = 0;
+        const uint32_t t_trk = __shfl_sync(0xffffffffu, i_trk, 31), t_kept = __shfl_sync(0xffffffffu, i_kept, 31);
+        if (lane == 0) {
+            if (t_trk && A.stage_trk) s_trk = atomicAdd(A.ticket + 1, t_trk);
+            if (t_kept) s_kept = atomicAdd(A.ticket + 2, t_kept);
+        }
+        s_trk = __shfl_sync(0xffffffffu, s_trk, 0);
+        s_kept = __shfl_sync(0xffffffffu, s_kept, 0);
+        const uint32_t b_trk = __shfl_sync(0xffffffffu, e_trk, fl), b_kept = __shfl_sync(0xffffffffu, e_kept, fl);
+        const uint32_t b_hits = __shfl_sync(0xffffffffu, e_hits, fl);
+        if (active) {
+            if (O.reason) O.reason[f] = (uint8_t)reason;
+            if (O.frames) {
+                m3e_frame_out fo;
+                fo.n_cand = (uint16_t)ncand;
+                fo.n_tracks = (uint16_t)ntrk;
+                fo.n_combs = (uint16_t)ncomb;
+                fo.reason = (uint8_t)reason;
+                fo.n_neg = (uint8_t)min(nneg, 255);
+                fo.track_first = e_trk - b_trk;
+                fo.kept_index = kept ? e_kept - b_kept : 0xFFFFFFFFu;
+                O.frames[f] = fo;
+            }
+            if (kept) {
+                const uint32_t k = s_kept + e_kept;
+                if (k < A.stage_kept_cap) {
+                    KeptRec kr;
+                    kr.frame = f;
+                    kr.pad = 0;
+                    if (reason == M3E_REASON_VERTEX) {
+                        kr.v = V.vtx[lane];
+                    } else {
+                        kr.v = m3e_vertex{};
+                        kr.v.frame = 0xFFFFFFFFu;
+                    }
+                    A.stage_kept[k] = kr;
+                } else {
+                    overflow = true;
+                }
+            }
+            if (o_trk && A.stage_trk) {   // the frame's first o_trk accepted tracks, in candidate order
+                uint32_t n = 0;
+                for (uint32_t k = 0; k < nst && n < o_trk; ++k) {
+                    m3e_track t = A.fit_g[cs + k];
+                    if (t.frame == kSpilled) continue;
+                    const uint32_t dst = s_trk + e_trk + n;
+                    if (dst < A.stage_trk_cap) A.stage_trk[dst] = t;
+                    else overflow = true;
+                    ++n;
+                }
+            }
+        }
+        // BatchStat of each fitted warp-batch (written by its first lane)
+        const int ll = fl + fb - 1;   // last lane of the warp-batch (frames past F are inactive: 0)
+        const uint32_t l_trk = __shfl_sync(0xffffffffu, i_trk, ll & 31), l_kept = __shfl_sync(0xffffffffu, i_kept, ll & 31);
+        const uint32_t l_hits = __shfl_sync(0xffffffffu, i_hits, ll & 31);
+        if (inb && gb != kSpilled && lane == fl) {
+            BatchStat bs;
+            bs.n_trk = l_trk - b_trk;
+            bs.n_kept = l_kept - b_kept;
+            bs.n_hits = l_hits - b_hits;
+            bs.s_trk = s_trk + b_trk;
+            bs.s_kept = s_kept + b_kept;
+            bs.nf = min(A.F - b * (uint32_t)fb, (uint32_t)fb);
+            bs.pad[0] = bs.pad[1] = 0;
+            A.bstat[b] = bs;
+        }
+        // run summary (per-warp counters in shared memory)
+        uint32_t kr[6];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) kr[r] = __popc(__ballot_sync(0xffffffffu, active && reason == r));
+        const uint32_t c_cand = warp_sum(nst), c_frames = __popc(__ballot_sync(0xffffffffu, active));
+        const uint32_t t_hits = __shfl_sync(0xffffffffu, i_hits, 31);
+        if (lane == 0) {
+            for (int r = 0; r < 6; ++r) S.acc[warp][r] += kr[r];
+            S.acc[warp][6] += c_cand;
+            S.acc[warp][7] += c_frames;
+            S.acc[warp][8] += t_trk;
+            S.acc[warp][9] += t_hits;
+        }
+        __syncwarp();
+    }
+    if (__any_sync(0xffffffffu, overflow) && lane == 0) S.acc[warp][10] = 1u;
+    __syncwarp();
+    if (lane == 0 && A.out.summary) flush_summary(A.out.summary, S.acc[warp]);
+}
+
+cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s) {
+    finish_kernel<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+int finish_blocks_per_sm() {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, finish_kernel, kThreads, 0) != cudaSuccess) return 1;
+    return n > 0 ? n : 1;
 }
 
 cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s) {

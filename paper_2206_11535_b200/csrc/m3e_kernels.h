@@ -17,11 +17,11 @@ constexpr int kHCap = 256;           // hits of a warp-batch staged in shared me
 constexpr int kMaxTracksCap = 128;   // upper bound accepted for params.max_tracks
 constexpr int kMaxCombsCap = 128;    // upper bound accepted for params.max_combs + 1
 constexpr int kMaxCutsCap = 1023;    // upper bound accepted for params.cuts_max
-constexpr size_t kVScratchBytes = 2048;   // >= sizeof(VScratch), checked in m3e_kernels.cu
+constexpr size_t kVScratchBytes = 4096;   // >= sizeof(VScratch), checked in m3e_kernels.cu
 
 // kModeSelectC: the Selection Cuts alone, candidates written compactly to the
-// candidate store (first kernel of the split production path); kModeFull then
-// reads them (A.presel) instead of selecting again
+// candidate store (first kernel of the split production path: select -> fit ->
+// finish -> fused kernel over the spilled warp-batches only -> pack)
 enum { kModeFull = 0, kModeSelect = 1, kModeFit = 2, kModeVertex = 3, kModePack = 4, kModeSelectC = 5 };
 constexpr uint32_t kSpilled = 0xFFFFFFFFu;   // bsel[] entry of a warp-batch whose candidates did not fit
 
@@ -61,10 +61,11 @@ struct KArgs {
     // workspace
     uint32_t* ticket;      // counters (zeroed before the launch): [0] select warp-batch ticket, [1] staged
                            // tracks, [2] staged kept frames, [3] pack-kernel tile ticket, [4] filter
-                           // warp-batch ticket, [6..7] candidate-store fill (u64)
+                           // warp-batch ticket, [5] spilled warp-batches, [6..7] candidate-store fill (u64)
     uint32_t* bticket;     // this launch's warp-batch ticket (ticket + 0 or ticket + 4)
-    // candidate store of the split path (kModeSelectC writes, kModeFull + presel reads)
-    int presel;            // kModeFull: take candidates from the store (batches not spilled)
+    // candidate store of the split path (kModeSelectC writes, fit_kernel / finish_kernel read)
+    uint32_t* spill_out;   // kModeSelectC: appends the warp-batches that did not fit (count in ticket[5])
+    uint32_t* spill_list;  // kModeFull, non-NULL: process only these warp-batches
     uint4* cand_g;         // {packed hit indices, r_tc bits, frame, 0}, warp-batch contiguous, frame
                            // order; frame = kSpilled marks an unused entry
     m3e_track* fit_g;      // fit of store entry c (fit_kernel); frame = kSpilled: not accepted
@@ -105,6 +106,8 @@ cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStre
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s);
 int fit_blocks_per_sm();
+cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s);
+int finish_blocks_per_sm();
 int blocks_per_sm(int mode, bool big);
 
 }  // namespace m3e

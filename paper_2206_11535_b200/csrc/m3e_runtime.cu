@@ -65,6 +65,7 @@ struct Workspace {
     uint32_t* sel = nullptr;            // per-frame selection words of the split path
     size_t sel_n = 0;
     uint32_t* bsel = nullptr;           // per-warp-batch store offsets of the split path
+    uint32_t* spill = nullptr;          // warp-batches the store could not take
     size_t bsel_n = 0;
     size_t bytes = 0;
 };
@@ -112,6 +113,7 @@ void free_ws(Workspace& w) {
     cudaFree(w.fit_g);
     cudaFree(w.sel);
     cudaFree(w.bsel);
+    cudaFree(w.spill);
     cudaFree(w.pair_scratch);
     cudaFree(w.vscratch);
     cudaFree(w.bstat);
@@ -277,10 +279,13 @@ int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame) 
     }
     if (w.bsel_n < nbatch) {
         cudaFree(w.bsel);
-        w.bytes -= w.bsel_n * sizeof(uint32_t);
+        cudaFree(w.spill);
+        w.bytes -= 2 * w.bsel_n * sizeof(uint32_t);
+        w.bsel_n = 0;
         CK(cudaMalloc(&w.bsel, nbatch * sizeof(uint32_t)));
+        CK(cudaMalloc(&w.spill, nbatch * sizeof(uint32_t)));
         w.bsel_n = nbatch;
-        w.bytes += nbatch * sizeof(uint32_t);
+        w.bytes += 2 * nbatch * sizeof(uint32_t);
     }
     return M3E_OK;
 }
@@ -323,14 +328,17 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     const uint64_t nbatch = (F + fb - 1) / fb;
     // big-frame variant (pair-factorised selection compiled in) for high occupancy
     const bool big = (mode == kModeFull || mode == kModeSelect) && (double)H > kBigMeanHits * (double)F;
-    // production path split in two kernels (Selection Cuts | fit, vertex, output)
-    // so that each keeps its hot code in the instruction cache
+    // production path split by stage (Selection Cuts | fit | tracks, vertex,
+    // output staging), each kernel with its hot code in the instruction cache and
+    // its own occupancy; the fused kernel then runs only the warp-batches whose
+    // candidates did not fit the store
     const bool split = mode == kModeFull && !big && ctx->split;
     const int bps = blocks_per_sm(mode, big);
     const int grid = (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * bps);
     const int sgrid = split ? (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * blocks_per_sm(kModeSelectC, false))
                             : 0;
-    rc = ensure_ws(ctx, w, nbatch, p, fb, std::max(grid, sgrid));
+    const int fgrid = split ? ctx->sms * finish_blocks_per_sm() : 0;
+    rc = ensure_ws(ctx, w, nbatch, p, fb, std::max(std::max(grid, sgrid), fgrid));
     if (rc) return rc;
     if (split) {
         rc = ensure_split(w, F, nbatch, ctx->cand_per_frame);
@@ -372,20 +380,23 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         sa.cand_cap = std::min<uint64_t>(w.cand_n, std::max<uint64_t>(ctx->cand_per_frame * F, 1u << 10));
         sa.sel = w.sel;
         sa.bsel = w.bsel;
+        sa.spill_out = w.spill;
         CK(launch_filter(kModeSelectC, false, sa, sgrid, s));
         if (tm) CK(cudaEventRecord(ev[1], s));
-        a.presel = 1;
         a.cand_g = w.cand_g;
         a.fit_g = w.fit_g;
         a.cand_cap = sa.cand_cap;
         a.sel = w.sel;
         a.bsel = w.bsel;
-        a.bticket = w.ticket + 4;
         CK(launch_fit(a, ctx->sms * fit_blocks_per_sm(), s));
+        if (tm) CK(cudaEventRecord(ev[2], s));
+        CK(launch_finish(a, fgrid, s));
+        a.spill_list = w.spill;   // the fused kernel takes only the spilled warp-batches
+        a.bticket = w.ticket + 4;
     } else if (tm) {
         CK(cudaEventRecord(ev[1], s));
+        CK(cudaEventRecord(ev[2], s));
     }
-    if (tm) CK(cudaEventRecord(ev[2], s));
     CK(launch_filter(mode, big, a, grid, s));
     if (tm) CK(cudaEventRecord(ev[3], s));
     if (packs) {
