@@ -540,7 +540,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                         c.x = cidx[e];
                         c.y = __float_as_uint(crt[e]);
                     }
-                    c.z = f0 + (uint32_t)find_frame(W.pref, nf, e);
+                    const int j = find_frame(W.pref, nf, e);
+                    c.z = f0 + (uint32_t)j;
+                    c.w = (uint32_t)j;   // frame within the warp-batch
                 }
                 A.cand_g[base + e] = c;
             }
@@ -1031,6 +1033,11 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
         t.cx = o.cx;
         t.cy = o.cy;
         A.fit_g[c] = t;
+        // code byte for the finish kernel: frame within the warp-batch << 3 |
+        // accepted | kappa < 0 | kappa > 0
+        const bool acc = o.status == 0;
+        A.code_g[c] = (uint8_t)((e.w << 3) | (acc ? 1u : 0u) | (acc && o.kappa < 0.0f ? 2u : 0u) |
+                                (acc && o.kappa > 0.0f ? 4u : 0u));
     }
 }
 
@@ -1053,6 +1060,7 @@ __device__ __forceinline__ uint32_t warp_incl(uint32_t v) {
 struct FinishSmem {
     DevParams P;
     uint32_t acc[kWarps][12];
+    int cnt[kWarps][33], neg[kWarps][33], pos[kWarps][33];   // per frame lane (+1 for invalid lanes)
 };
 
 #ifndef M3E_FINISH_MIN_BLOCKS
@@ -1095,17 +1103,43 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
         // first store entry of the frame: warp-batch base + prefix within the warp-batch
         const uint32_t cex = warp_incl(nst) - nst;
         const uint32_t cs = gb + cex - __shfl_sync(0xffffffffu, cex, fl);
-        // T: accepted tracks of the frame and their charges (candidate order)
-        int cnt = 0, nneg = 0, npos = 0;
-        for (uint32_t k = 0; k < nst; ++k) {
-            const m3e_track* r = A.fit_g + cs + k;
-            if (r->frame != kSpilled) {
-                const float kap = r->kappa;
-                nneg += (cnt < P.max_tracks && kap < 0.0f) ? 1 : 0;
-                npos += (cnt < P.max_tracks && kap > 0.0f) ? 1 : 0;
-                ++cnt;
+        // T: accepted tracks of each frame and their charges (candidate order):
+        // coalesced passes over each warp-batch's code bytes, one lane per candidate
+        S.cnt[warp][lane] = 0;
+        S.neg[warp][lane] = 0;
+        S.pos[warp][lane] = 0;
+        __syncwarp();
+        const uint32_t cin = cex + nst;   // inclusive prefix
+        for (int q = 0; q < G; ++q) {
+            const int ql = q * fb;
+            const uint32_t qb = __shfl_sync(0xffffffffu, gb, ql);
+            const uint32_t qn = __shfl_sync(0xffffffffu, cin, min(ql + fb, 32) - 1) -
+                                __shfl_sync(0xffffffffu, cex, ql);
+            if (qb == kSpilled || g * (uint32_t)G + (uint32_t)q >= A.nbatch) continue;
+            for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
+                const uint32_t e = e0 + lane;
+                const bool valid = e < qn;
+                const uint32_t code = valid ? A.code_g[qb + e] : 0u;
+                const int j = valid ? ql + (int)(code >> 3) : 32;
+                const unsigned grp = __match_any_sync(0xffffffffu, j);
+                const unsigned ma = __ballot_sync(0xffffffffu, code & 1u);
+                const int before = valid ? S.cnt[warp][j] : 0;
+                const int rank = before + __popc(ma & grp & lt_mask);
+                const bool st = (code & 1u) && rank < P.max_tracks;   // stored track
+                const unsigned mn = __ballot_sync(0xffffffffu, st && (code & 2u));
+                const unsigned mp = __ballot_sync(0xffffffffu, st && (code & 4u));
+                __syncwarp();
+                if (valid && lane == __ffs(grp) - 1) {
+                    S.cnt[warp][j] = before + __popc(ma & grp);
+                    S.neg[warp][j] += __popc(mn & grp);
+                    S.pos[warp][j] += __popc(mp & grp);
+                }
+                __syncwarp();
             }
         }
+        const int cnt = S.cnt[warp][lane];
+        int nneg = S.neg[warp][lane];
+        const int npos = S.pos[warp][lane];
         if (active && reason == M3E_REASON_NONE && cnt > P.max_tracks) {
             reason = M3E_REASON_TRACK_OVERFLOW;
             nneg = 0;
@@ -1206,15 +1240,43 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
                     overflow = true;
                 }
             }
-            if (o_trk && A.stage_trk) {   // the frame's first o_trk accepted tracks, in candidate order
-                uint32_t n = 0;
-                for (uint32_t k = 0; k < nst && n < o_trk; ++k) {
-                    m3e_track t = A.fit_g[cs + k];
-                    if (t.frame == kSpilled) continue;
-                    const uint32_t dst = s_trk + e_trk + n;
-                    if (dst < A.stage_trk_cap) A.stage_trk[dst] = t;
-                    else overflow = true;
-                    ++n;
+        }
+        // the first o_trk accepted tracks of each frame, in candidate order: second
+        // coalesced pass (codes from L1/L2), one lane per candidate
+        if (A.stage_trk && t_trk) {
+            S.cnt[warp][lane] = 0;
+            S.pos[warp][lane] = (int)(s_trk + e_trk);   // staging slot of the frame's first track
+            S.neg[warp][lane] = (int)o_trk;
+            __syncwarp();
+            for (int q = 0; q < G; ++q) {
+                const int ql = q * fb;
+                const uint32_t qb = __shfl_sync(0xffffffffu, gb, ql);
+                const uint32_t qn = __shfl_sync(0xffffffffu, cin, min(ql + fb, 32) - 1) -
+                                    __shfl_sync(0xffffffffu, cex, ql);
+                if (qb == kSpilled || g * (uint32_t)G + (uint32_t)q >= A.nbatch) continue;
+                for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
+                    const uint32_t e = e0 + lane;
+                    const bool valid = e < qn;
+                    const uint32_t code = valid ? A.code_g[qb + e] : 0u;
+                    const int j = valid ? ql + (int)(code >> 3) : 32;
+                    const unsigned grp = __match_any_sync(0xffffffffu, j);
+                    const unsigned ma = __ballot_sync(0xffffffffu, code & 1u);
+                    const int before = valid ? S.cnt[warp][j] : 0;
+                    const int rank = before + __popc(ma & grp & lt_mask);
+                    if ((code & 1u) && rank < S.neg[warp][j]) {
+                        const uint32_t dst = (uint32_t)S.pos[warp][j] + (uint32_t)rank;
+                        if (dst < A.stage_trk_cap) {
+                            const uint4* s4 = reinterpret_cast<const uint4*>(A.fit_g + qb + e);
+                            uint4* d4 = reinterpret_cast<uint4*>(A.stage_trk + dst);
+                            d4[0] = s4[0];
+                            d4[1] = s4[1];
+                        } else {
+                            overflow = true;
+                        }
+                    }
+                    __syncwarp();
+                    if (valid && lane == __ffs(grp) - 1) S.cnt[warp][j] = before + __popc(ma & grp);
+                    __syncwarp();
                 }
             }
         }

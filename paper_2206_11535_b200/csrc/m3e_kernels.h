@@ -69,6 +69,8 @@ struct KArgs {
     uint4* cand_g;         // {packed hit indices, r_tc bits, frame, 0}, warp-batch contiguous, frame
                            // order; frame = kSpilled marks an unused entry
     m3e_track* fit_g;      // fit of store entry c (fit_kernel); frame = kSpilled: not accepted
+    uint8_t* code_g;       // code of store entry c: frame within its warp-batch << 3 | accepted |
+                           // kappa < 0 (2) | kappa > 0 (4)
     uint64_t cand_cap;     // entries of cand_g (< 2^32)
     uint32_t* sel;         // [F] per frame: n_cand | reason << 16
     uint32_t* bsel;        // [nbatch] first store entry of the warp-batch, or kSpilled

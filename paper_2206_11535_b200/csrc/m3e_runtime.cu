@@ -61,6 +61,7 @@ struct Workspace {
     void* vscratch = nullptr;           // vertex-stage scratch, kVScratchBytes per warp
     uint4* cand_g = nullptr;            // candidate store of the split path
     m3e_track* fit_g = nullptr;         // fit records of the store entries
+    uint8_t* code_g = nullptr;          // their code bytes
     size_t cand_n = 0;
     uint32_t* sel = nullptr;            // per-frame selection words of the split path
     size_t sel_n = 0;
@@ -111,6 +112,7 @@ namespace {
 void free_ws(Workspace& w) {
     cudaFree(w.cand_g);
     cudaFree(w.fit_g);
+    cudaFree(w.code_g);
     cudaFree(w.sel);
     cudaFree(w.bsel);
     cudaFree(w.spill);
@@ -263,12 +265,14 @@ int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame) 
     if (w.cand_n < nc) {
         cudaFree(w.cand_g);
         cudaFree(w.fit_g);
-        w.bytes -= w.cand_n * (sizeof(uint4) + sizeof(m3e_track));
+        cudaFree(w.code_g);
+        w.bytes -= w.cand_n * (sizeof(uint4) + sizeof(m3e_track) + 1);
         w.cand_n = 0;
         CK(cudaMalloc(&w.cand_g, nc * sizeof(uint4)));
         CK(cudaMalloc(&w.fit_g, nc * sizeof(m3e_track)));
+        CK(cudaMalloc(&w.code_g, nc));
         w.cand_n = nc;
-        w.bytes += nc * (sizeof(uint4) + sizeof(m3e_track));
+        w.bytes += nc * (sizeof(uint4) + sizeof(m3e_track) + 1);
     }
     if (w.sel_n < F) {
         cudaFree(w.sel);
@@ -385,6 +389,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         if (tm) CK(cudaEventRecord(ev[1], s));
         a.cand_g = w.cand_g;
         a.fit_g = w.fit_g;
+        a.code_g = w.code_g;
         a.cand_cap = sa.cand_cap;
         a.sel = w.sel;
         a.bsel = w.bsel;
