@@ -117,41 +117,51 @@ __device__ __forceinline__ bool pass_rest(const DevParams& P, const Frame& F, in
     return ar >= P.rt_min && ar <= P.rt_max;
 }
 
-// Warp-cooperative enumeration of all n0 n1 n2 combinations of one frame in the
-// row-major order of Alg. 2 (i0 outer, i2 inner), 32 consecutive combinations per
-// step.  Two-level compaction: the Delta-lambda survivors (~7 % of combinations,
-// the cut that removes > 80 %, Fig. 4) are appended with ballot + popc to a
-// per-warp FIFO `q` (64 entries, shared memory); each full 32 of them is tested
-// for Phi_01, Phi_12, r_tc on all 32 lanes (no divergent tail) and the final
-// survivors are compacted again with ballot + popc, so stored candidates keep
-// the enumeration order.  Stops once more than cuts_max survive (R3).
+// r_tc window of Eq. 5 (the last of the Selection Cuts)
+__device__ __forceinline__ bool pass_rtc(const DevParams& P, const Frame& F, int i0, int i1, int i2, float& rt) {
+    const int g0 = F.s[0] + i0, g1 = F.s[1] + i1, g2 = F.s[2] + i2;
+    rt = circle_radius(make_float3(F.x[g0], F.y[g0], 0.0f), make_float3(F.x[g1], F.y[g1], 0.0f),
+                       make_float3(F.x[g2], F.y[g2], 0.0f));
+    const float ar = fabsf(rt);
+    return ar >= P.rt_min && ar <= P.rt_max;
+}
+
+// Warp-cooperative Selection Cuts of one frame, in the row-major (i0, i1, i2)
+// order of Alg. 2.  The cuts are factorised by the hits they depend on (Eq. 2-5):
+// Phi_01 by (i0, i1) alone, so
+//   1. the (i0, i1) pairs are tested for Phi_01, 32 per step, and the survivors
+//      (~22 %) appended with ballot + popc to the pair list `pl` (shared memory);
+//   2. the first K <= 32 listed pairs are expanded against every layer-2 hit,
+//      32 (k, i2) combinations per step in row-major order, and tested for
+//      Delta-lambda and Phi_12; survivors (~11 %) go to the FIFO `q`;
+//   3. each full 32 of the FIFO is tested for r_tc on all 32 lanes and the final
+//      survivors compacted again with ballot + popc,
+// so the stored candidates keep the enumeration order and the set is exactly the
+// conjunction of the four cuts.  Stops once more than cuts_max survive (R3).
 // emit(pos, packed, rt) is called for pos < cuts_max.  Returns min(#survivors,
 // cuts_max + 1) (warp-uniform).
 template <class Emit>
-__device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame& F, uint32_t* q, Emit emit) {
+__device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame& F, uint32_t* q, uint32_t* pl,
+                                                 Emit emit) {
     const int lane = threadIdx.x & 31;
     const int n0 = F.n[0], n1 = F.n[1], n2 = F.n[2];
-    const long long total = (long long)n0 * n1 * n2;
-    if (total == 0) return 0;
+    const int np = n0 * n1;
+    if (np == 0 || n2 == 0) return 0;
     const unsigned lt_mask = (1u << lane) - 1u;
-    // mixed-radix digits of the lane's first combination and of the step 32; the
-    // quotients of x < 64 by n are floor((x + 0.5) / n): >= 0.5/n away from an
-    // integer, far above the 1-ulp error of rcp (no integer division)
-    const int n12 = n1 * n2;
-    const float in12 = rcp((float)n12), in2 = rcp((float)n2);
-    int i0 = (int)(((float)lane + 0.5f) * in12), rem = lane - i0 * n12;
-    int i1 = (int)(((float)rem + 0.5f) * in2), i2 = rem - i1 * n2;
-    const int a = (int)(32.5f * in12), r32 = 32 - a * n12;
-    const int b = (int)(((float)r32 + 0.5f) * in2), c = r32 - b * n2;
-    int count = 0, qn = 0;
-    // test q[0..n) (n <= 32) for the remaining cuts; true once the frame overflows
+    // mixed-radix digits: quotients of x by n as floor((x + 0.5) / n), >= 0.5/n
+    // away from an integer for the x < 2^15 used here, far above the error of rcp
+    const float in1 = rcp((float)n1), in2 = rcp((float)n2);
+    int j0 = (int)(((float)lane + 0.5f) * in1), j1 = lane - j0 * n1;   // lane's first pair
+    const int a1 = (int)(32.5f * in1), b1 = 32 - a1 * n1;                // step of 32 pairs
+    int count = 0, qn = 0, pn = 0, pnext = 0;
+    // r_tc for q[0..n) (n <= 32); true once the frame overflows
     auto drain = [&](int n) -> bool {
         float rt = 0.0f;
         uint32_t pk = 0;
         bool pass = false;
         if (lane < n) {
             pk = q[lane];
-            pass = pass_rest(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
+            pass = pass_rtc(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
         }
         const unsigned m = __ballot_sync(0xffffffffu, pass);
         const int pos = count + __popc(m & lt_mask);
@@ -159,26 +169,58 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
         count += __popc(m);
         return count > P.cuts_max;
     };
-    for (long long base = 0; base < total; base += 32) {
-        const bool pass = i0 < n0 && pass_dlambda(P, F, i0, i1, i2);
-        const unsigned m = __ballot_sync(0xffffffffu, pass);
-        if (pass) q[qn + __popc(m & lt_mask)] = (uint32_t)i0 | ((uint32_t)i1 << 10) | ((uint32_t)i2 << 20);
-        qn += __popc(m);
-        if (qn >= 32) {
-            __syncwarp();
-            if (drain(32)) return P.cuts_max + 1;
-            const uint32_t v = lane < qn - 32 ? q[32 + lane] : 0u;
-            __syncwarp();
-            if (lane < qn - 32) q[lane] = v;
-            qn -= 32;
+    for (;;) {
+        // 1. refill the pair list to >= 32 Phi_01 survivors (or all pairs)
+        while (pn < 32 && pnext < np) {
+            bool pass = false;
+            if (j0 < n0) {
+                const int g0 = F.s[0] + j0, g1 = F.s[1] + j1;
+                pass = (F.x[g0] * F.x[g1] + F.y[g0] * F.y[g1]) * P.inv_r0r1 >= P.c01_min;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            if (pass) pl[pn + __popc(m & lt_mask)] = (uint32_t)j0 | ((uint32_t)j1 << 10);
+            pn += __popc(m);
+            pnext += 32;
+            j1 += b1;
+            if (j1 >= n1) { j1 -= n1; ++j0; }
+            j0 += a1;
+        }
+        if (pn == 0) break;
+        __syncwarp();
+        // 2. expand the first K listed pairs against layer 2
+        const int K = min(pn, 32), nk = K * n2;
+        for (int cb = 0; cb < nk; cb += 32) {
+            const int c = cb + lane;
+            const int k = (int)(((float)c + 0.5f) * in2), i2 = c - k * n2;
+            bool pass = false;
+            uint32_t pk = 0;
+            if (c < nk) {
+                pk = pl[k] | ((uint32_t)i2 << 20);
+                const int g0 = F.s[0] + (int)(pk & 1023u), g1 = F.s[1] + (int)((pk >> 10) & 1023u), g2 = F.s[2] + i2;
+                const float z1 = F.z[g1];
+                const float dl = (F.z[g2] - z1) * P.inv_dr12 - (z1 - F.z[g0]) * P.inv_dr01;
+                pass = fabsf(dl) <= P.dl_max &&
+                       (F.x[g1] * F.x[g2] + F.y[g1] * F.y[g2]) * P.inv_r1r2 >= P.c12_min;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            if (pass) q[qn + __popc(m & lt_mask)] = pk;
+            qn += __popc(m);
+            if (qn >= 32) {
+                __syncwarp();
+                if (drain(32)) return P.cuts_max + 1;
+                const uint32_t v = lane < qn - 32 ? q[32 + lane] : 0u;
+                __syncwarp();
+                if (lane < qn - 32) q[lane] = v;
+                qn -= 32;
+            }
             __syncwarp();
         }
-        // advance (i0, i1, i2) by 32 in radix (n0, n1, n2)
-        i2 += c;
-        if (i2 >= n2) { i2 -= n2; ++i1; }
-        i1 += b;
-        if (i1 >= n1) { i1 -= n1; ++i0; }
-        i0 += a;
+        // drop the K expanded pairs
+        const uint32_t v = lane < pn - K ? pl[K + lane] : 0u;
+        __syncwarp();
+        if (lane < pn - K) pl[lane] = v;
+        pn -= K;
+        __syncwarp();
     }
     __syncwarp();
     if (qn > 0 && drain(qn)) return P.cuts_max + 1;

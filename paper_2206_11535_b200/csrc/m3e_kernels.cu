@@ -122,7 +122,8 @@ struct __align__(16) WarpSmem {
     BatchState st;
     uint32_t pref[kFB + 1];          // candidates: exclusive prefix
     int npos[kFB];                   // stored positive tracks per frame (vertex gate)
-    uint32_t q[64];                  // Delta-lambda survivors (selection FIFO)
+    uint32_t q[64];                  // Delta-lambda + Phi_12 survivors (selection FIFO)
+    uint32_t pl[64];                 // Phi_01 pair list of the selection
     uint32_t acc[12];                // run summary: kept_by_reason[6], cand, frames, tracks, hits, overflow
 };
 
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                         count = select_frame_big(&S.P, Fv, W.q, A.pair_scratch + gwarp * kPairWords, sk, kPairCapG);
                         __syncwarp();
                     }
-                    if (count < 0) count = select_frame_warp(P, Fv, W.q, emit);
+                    if (count < 0) count = select_frame_warp(P, Fv, W.q, W.pl, emit);
                     __syncwarp();
                 }
                 const int r = inval ? M3E_REASON_INVALID
