@@ -1065,7 +1065,7 @@ struct FinishSmem {
 };
 
 #ifndef M3E_FINISH_MIN_BLOCKS
-#define M3E_FINISH_MIN_BLOCKS 4
+#define M3E_FINISH_MIN_BLOCKS 6   // latency bound: 48 warps/SM (measured 4: 4.6 ms, 6: 3.9 ms, 8: 4.0 ms)
 #endif
 __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel(const __grid_constant__ KArgs A) {
     __shared__ FinishSmem S;
@@ -1084,9 +1084,12 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
     const int bl = lane / fb;                   // this lane's warp-batch within the group
     const int fl = bl * fb;                     // its first lane
     const uint32_t ngroups = (A.nbatch + G - 1) / G;
-    const uint32_t nwarps = gridDim.x * kWarps;
     bool overflow = false;
-    for (uint32_t g = (uint32_t)gwarp; g < ngroups; g += nwarps) {
+    for (;;) {
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(A.ticket + 8, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= ngroups) break;
         const uint32_t b = g * (uint32_t)G + (uint32_t)bl;
         const uint32_t f = b * (uint32_t)fb + (uint32_t)(lane - fl);
         const bool inb = bl < G && b < A.nbatch;
@@ -1192,7 +1195,7 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
             __syncwarp();
         }
         // O: frame records in place (warp-batch relative offsets), tracks and kept
-        // frames staged, BatchStat per warp-batch
+        // frames staged, BatchStat per warp-batch for the pack kernel
         const bool kept = active && reason != M3E_REASON_NONE;
         const bool has_tracks = active && reason != M3E_REASON_TRIPLET_OVERFLOW && reason != M3E_REASON_INVALID;
         const uint32_t o_trk = has_tracks ? (uint32_t)min(ntrk, P.max_tracks) : 0u;
@@ -1201,8 +1204,9 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
         if (kept) o_hits = A.offsets[4 * (size_t)f + 4] - A.offsets[4 * (size_t)f];
         const uint32_t i_trk = warp_incl(o_trk), i_kept = warp_incl(o_kept), i_hits = warp_incl(o_hits);
         const uint32_t e_trk = i_trk - o_trk, e_kept = i_kept - o_kept, e_hits = i_hits - o_hits;
-        uint32_t s_trk = 0, s_kept = 0;
         const uint32_t t_trk = __shfl_sync(0xffffffffu, i_trk, 31), t_kept = __shfl_sync(0xffffffffu, i_kept, 31);
+        const uint32_t t_hits = __shfl_sync(0xffffffffu, i_hits, 31);
+        uint32_t s_trk = 0, s_kept = 0;
         if (lane == 0) {
             if (t_trk && A.stage_trk) s_trk = atomicAdd(A.ticket + 1, t_trk);
             if (t_kept) s_kept = atomicAdd(A.ticket + 2, t_kept);
@@ -1283,7 +1287,8 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
         }
         // BatchStat of each fitted warp-batch (written by its first lane)
         const int ll = fl + fb - 1;   // last lane of the warp-batch (frames past F are inactive: 0)
-        const uint32_t l_trk = __shfl_sync(0xffffffffu, i_trk, ll & 31), l_kept = __shfl_sync(0xffffffffu, i_kept, ll & 31);
+        const uint32_t l_trk = __shfl_sync(0xffffffffu, i_trk, ll & 31);
+        const uint32_t l_kept = __shfl_sync(0xffffffffu, i_kept, ll & 31);
         const uint32_t l_hits = __shfl_sync(0xffffffffu, i_hits, ll & 31);
         if (inb && gb != kSpilled && lane == fl) {
             BatchStat bs;
@@ -1301,7 +1306,6 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
 #pragma unroll
         for (int r = 0; r < 6; ++r) kr[r] = __popc(__ballot_sync(0xffffffffu, active && reason == r));
         const uint32_t c_cand = warp_sum(nst), c_frames = __popc(__ballot_sync(0xffffffffu, active));
-        const uint32_t t_hits = __shfl_sync(0xffffffffu, i_hits, 31);
         if (lane == 0) {
             for (int r = 0; r < 6; ++r) S.acc[warp][r] += kr[r];
             S.acc[warp][6] += c_cand;

@@ -61,7 +61,8 @@ struct KArgs {
     // workspace
     uint32_t* ticket;      // counters (zeroed before the launch): [0] select warp-batch ticket, [1] staged
                            // tracks, [2] staged kept frames, [3] pack-kernel tile ticket, [4] filter
-                           // warp-batch ticket, [5] spilled warp-batches, [6..7] candidate-store fill (u64)
+                           // warp-batch ticket, [5] spilled warp-batches, [6..7] candidate-store fill (u64),
+                           // [8] finish-kernel group ticket
     uint32_t* bticket;     // this launch's warp-batch ticket (ticket + 0 or ticket + 4)
     // candidate store of the split path (kModeSelectC writes, fit_kernel / finish_kernel read)
     uint32_t* spill_out;   // kModeSelectC: appends the warp-batches that did not fit (count in ticket[5])

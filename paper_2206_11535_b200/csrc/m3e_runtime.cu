@@ -203,8 +203,8 @@ int choose_fb(uint64_t F, uint64_t H) {
 
 int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p, int fb, int ctas) {
     if (!w.ticket) {
-        CK(cudaMalloc(&w.ticket, 8 * sizeof(uint32_t)));
-        w.bytes += 8 * sizeof(uint32_t);
+        CK(cudaMalloc(&w.ticket, 16 * sizeof(uint32_t)));
+        w.bytes += 16 * sizeof(uint32_t);
     }
     const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
     if (w.bstat_n < nbatch) {
@@ -373,7 +373,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         a.stage_kept = w.stage_kept;
         a.stage_kept_cap = a.out.kept_capacity;
     }
-    CK(cudaMemsetAsync(w.ticket, 0, 8 * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(w.ticket, 0, 16 * sizeof(uint32_t), s));
     if (a.out.summary) CK(cudaMemsetAsync(a.out.summary, 0, sizeof(m3e_summary), s));
     const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + 5 <= ctx->tev.size();
     cudaEvent_t* ev = tm ? &ctx->tev[ctx->tev_used] : nullptr;
