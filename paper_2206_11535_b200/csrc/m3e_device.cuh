@@ -141,7 +141,7 @@ __device__ __forceinline__ bool pass_rtc(const DevParams& P, const Frame& F, int
 // emit(pos, packed, rt) is called for pos < cuts_max.  Returns min(#survivors,
 // cuts_max + 1) (warp-uniform).
 template <class Emit>
-__device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame& F, uint32_t* q, uint32_t* pl,
+__device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame& F, uint32_t* q, uint2* pl,
                                                  Emit emit) {
     const int lane = threadIdx.x & 31;
     const int n0 = F.n[0], n1 = F.n[1], n2 = F.n[2];
@@ -173,12 +173,19 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
         // 1. refill the pair list to >= 32 Phi_01 survivors (or all pairs)
         while (pn < 32 && pnext < np) {
             bool pass = false;
+            int g0 = 0, g1 = 0;
             if (j0 < n0) {
-                const int g0 = F.s[0] + j0, g1 = F.s[1] + j1;
+                g0 = F.s[0] + j0;
+                g1 = F.s[1] + j1;
                 pass = (F.x[g0] * F.x[g1] + F.y[g0] * F.y[g1]) * P.inv_r0r1 >= P.c01_min;
             }
             const unsigned m = __ballot_sync(0xffffffffu, pass);
-            if (pass) pl[pn + __popc(m & lt_mask)] = (uint32_t)j0 | ((uint32_t)j1 << 10);
+            if (pass) {
+                // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
+                const float z1 = F.z[g1];
+                const float u = z1 * P.inv_dr12 + (z1 - F.z[g0]) * P.inv_dr01;
+                pl[pn + __popc(m & lt_mask)] = make_uint2((uint32_t)j0 | ((uint32_t)j1 << 10), __float_as_uint(u));
+            }
             pn += __popc(m);
             pnext += 32;
             j1 += b1;
@@ -195,12 +202,12 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
             bool pass = false;
             uint32_t pk = 0;
             if (c < nk) {
-                pk = pl[k] | ((uint32_t)i2 << 20);
-                const int g0 = F.s[0] + (int)(pk & 1023u), g1 = F.s[1] + (int)((pk >> 10) & 1023u), g2 = F.s[2] + i2;
-                const float z1 = F.z[g1];
-                const float dl = (F.z[g2] - z1) * P.inv_dr12 - (z1 - F.z[g0]) * P.inv_dr01;
-                pass = fabsf(dl) <= P.dl_max &&
-                       (F.x[g1] * F.x[g2] + F.y[g1] * F.y[g2]) * P.inv_r1r2 >= P.c12_min;
+                const uint2 pe = pl[k];
+                pk = pe.x | ((uint32_t)i2 << 20);
+                const int g1 = F.s[1] + (int)(pe.x >> 10), g2 = F.s[2] + i2;
+                const float dl = fmaf(F.z[g2], P.inv_dr12, -__uint_as_float(pe.y));
+                const float c12 = (F.x[g1] * F.x[g2] + F.y[g1] * F.y[g2]) * P.inv_r1r2;
+                pass = (fabsf(dl) <= P.dl_max) & (c12 >= P.c12_min);
             }
             const unsigned m = __ballot_sync(0xffffffffu, pass);
             if (pass) q[qn + __popc(m & lt_mask)] = pk;
@@ -216,7 +223,7 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
             __syncwarp();
         }
         // drop the K expanded pairs
-        const uint32_t v = lane < pn - K ? pl[K + lane] : 0u;
+        const uint2 v = lane < pn - K ? pl[K + lane] : make_uint2(0u, 0u);
         __syncwarp();
         if (lane < pn - K) pl[lane] = v;
         pn -= K;

@@ -123,7 +123,7 @@ struct __align__(16) WarpSmem {
     uint32_t pref[kFB + 1];          // candidates: exclusive prefix
     int npos[kFB];                   // stored positive tracks per frame (vertex gate)
     uint32_t q[64];                  // Delta-lambda + Phi_12 survivors (selection FIFO)
-    uint32_t pl[64];                 // Phi_01 pair list of the selection
+    uint2 pl[64];                    // Phi_01 pair list of the selection: {i0 | i1 << 10, u(i0, i1)}
     uint32_t acc[12];                // run summary: kept_by_reason[6], cand, frames, tracks, hits, overflow
 };
 
@@ -479,7 +479,20 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                         count = select_frame_big(&S.P, Fv, W.q, A.pair_scratch + gwarp * kPairWords, sk, kPairCapG);
                         __syncwarp();
                     }
-                    if (count < 0) count = select_frame_warp(P, Fv, W.q, W.pl, emit);
+                    if (count < 0) {
+                        const uint32_t g = W.offs[buf][4 * j];
+                        if (MODE == kModeSelectC && g >= W.b_winlo[buf] && W.offs[buf][4 * j + 4] <= W.b_winhi[buf]) {
+                            // staged frame: the same walk with shared-memory addressing
+                            Frame Fs = Fv;
+                            const uint32_t d = g - W.b_winlo[buf];
+                            Fs.x = W.hx[buf] + d;
+                            Fs.y = W.hy[buf] + d;
+                            Fs.z = W.hz[buf] + d;
+                            count = select_frame_warp(P, Fs, W.q, W.pl, emit);
+                        } else {
+                            count = select_frame_warp(P, Fv, W.q, W.pl, emit);
+                        }
+                    }
                     __syncwarp();
                 }
                 const int r = inval ? M3E_REASON_INVALID
