@@ -62,6 +62,7 @@ struct DevParams {
     float inv_dr01, inv_dr12;   // 1/(R1-R0), 1/(R2-R1)         (Eq. 2)
     float inv_r0r1, inv_r1r2;   // 1/(R0 R1), 1/(R1 R2)         (Eq. 4)
     float dl_max, c01_min, c12_min, rt_min, rt_max;
+    float rt_min2, rt_max2;   // squared r_t window (selection kernel: no square roots)
     float chl;                  // sigma_MS = chl * k  (Highland at p = ptb / k, R7)
     float chi2_max;
     float R3sq;                 // layer-3 radius squared
@@ -126,6 +127,19 @@ __device__ __forceinline__ bool pass_rtc(const DevParams& P, const Frame& F, int
     return ar >= P.rt_min && ar <= P.rt_max;
 }
 
+// the same window without r_tc itself: r_tc^2 = d01^2 d12^2 d20^2 / (2 cz)^2
+// (collinear, cz = 0: fails, as r_tc = inf does)
+__device__ __forceinline__ bool pass_rtc_sq(const DevParams& P, const Frame& F, int i0, int i1, int i2) {
+    const int g0 = F.s[0] + i0, g1 = F.s[1] + i1, g2 = F.s[2] + i2;
+    const float x1 = F.x[g1], y1 = F.y[g1];
+    const float ax = F.x[g0] - x1, ay = F.y[g0] - y1, bx = F.x[g2] - x1, by = F.y[g2] - y1;
+    const float cx = bx - ax, cy = by - ay;
+    const float cz = ax * by - ay * bx;
+    const float num = (ax * ax + ay * ay) * (bx * bx + by * by) * (cx * cx + cy * cy);
+    const float den = 4.0f * cz * cz;
+    return cz != 0.0f && num >= den * P.rt_min2 && num <= den * P.rt_max2;
+}
+
 // Warp-cooperative Selection Cuts of one frame, in the row-major (i0, i1, i2)
 // order of Alg. 2.  The cuts are factorised by the hits they depend on (Eq. 2-5):
 // Phi_01 by (i0, i1) alone, so
@@ -138,9 +152,10 @@ __device__ __forceinline__ bool pass_rtc(const DevParams& P, const Frame& F, int
 //      survivors compacted again with ballot + popc,
 // so the stored candidates keep the enumeration order and the set is exactly the
 // conjunction of the four cuts.  Stops once more than cuts_max survive (R3).
-// emit(pos, packed, rt) is called for pos < cuts_max.  Returns min(#survivors,
+// emit(pos, packed, rt) is called for pos < cuts_max (rt = r_tc if kRt, else 0:
+// the split path's fit kernel recomputes it).  Returns min(#survivors,
 // cuts_max + 1) (warp-uniform).
-template <class Emit>
+template <bool kRt, class Emit>
 __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame& F, uint32_t* q, uint2* pl,
                                                  Emit emit) {
     const int lane = threadIdx.x & 31;
@@ -161,7 +176,8 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
         bool pass = false;
         if (lane < n) {
             pk = q[lane];
-            pass = pass_rtc(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
+            if constexpr (kRt) pass = pass_rtc(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
+            else pass = pass_rtc_sq(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u);
         }
         const unsigned m = __ballot_sync(0xffffffffu, pass);
         const int pos = count + __popc(m & lt_mask);

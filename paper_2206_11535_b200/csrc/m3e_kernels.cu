@@ -488,9 +488,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                             Fs.x = W.hx[buf] + d;
                             Fs.y = W.hy[buf] + d;
                             Fs.z = W.hz[buf] + d;
-                            count = select_frame_warp(P, Fs, W.q, W.pl, emit);
+                            count = select_frame_warp<MODE != kModeSelectC>(P, Fs, W.q, W.pl, emit);
                         } else {
-                            count = select_frame_warp(P, Fv, W.q, W.pl, emit);
+                            count = select_frame_warp<MODE != kModeSelectC>(P, Fv, W.q, W.pl, emit);
                         }
                     }
                     __syncwarp();
@@ -1033,8 +1033,10 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
         F.n[2] = (int)(o4.w - o4.z);
         F.n[3] = (int)(o5 - o4.w);
         const uint32_t pk = e.x;
-        const FitOut o = fit_candidate(A.P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u,
-                                       __uint_as_float(e.y));
+        const int i0 = (int)(pk & 1023u), i1 = (int)((pk >> 10) & 1023u), i2 = (int)((pk >> 20) & 1023u);
+        // r_tc of the selection (Eq. 5, same fp32 code as the selection's)
+        const float rtc = circle_radius(hit(F, 0, i0), hit(F, 1, i1), hit(F, 2, i2));
+        const FitOut o = fit_candidate(A.P, F, i0, i1, i2, rtc);
         m3e_track t;
         t.frame = o.status == 0 ? e.z : kSpilled;
         t.hit[0] = (uint16_t)(pk & 1023u);

@@ -171,6 +171,8 @@ DevParams make_dev_params(const m3e_params* p) {
     d.c12_min = (float)p->cos_phi12_min;
     d.rt_min = (float)p->rt_min;
     d.rt_max = (float)p->rt_max;
+    d.rt_min2 = d.rt_min * d.rt_min;
+    d.rt_max2 = d.rt_max * d.rt_max;
     const double X = p->x_over_x0;
     // Highland (R7): sigma = 13.6 MeV / p * sqrt(X) (1 + 0.038 ln X), p = PT_CONV B / k
     const double chl = 13.6 * std::sqrt(X) * (1.0 + 0.038 * std::log(X)) / (kPtConv * p->b_field);
