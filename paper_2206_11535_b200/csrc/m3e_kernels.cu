@@ -817,7 +817,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                 bs.s_trk = s_trk;
                 bs.s_kept = s_kept;
                 bs.nf = nf;
-                bs.pad[0] = bs.pad[1] = 0;
+                bs.c_base = 0;
+                bs.c_n = 0;
                 A.bstat[b] = bs;
             }
             // run summary: per-warp counters in shared memory, flushed once at the end
@@ -914,7 +915,29 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const KArgs A) {
             uint32_t g_hits = __shfl_sync(0xffffffffu, eb_hits, src);
             const uint32_t f0 = bb * (uint32_t)A.fb;
             // tracks
-            if (O.tracks && A.stage_trk) {
+            const uint32_t c_base = __shfl_sync(0xffffffffu, bs.c_base, src);
+            const uint32_t c_n = __shfl_sync(0xffffffffu, bs.c_n, src);
+            if (O.tracks && A.stage_trk && s_trk == kSpilled) {
+                // straight from the fit records: the warp-batch's accepted store entries, in order
+                uint32_t n = 0;
+                for (uint32_t e0 = 0; e0 < c_n; e0 += 32) {
+                    const uint32_t e = e0 + lane;
+                    const bool acc = e < c_n && (A.code_g[c_base + e] & 1u);
+                    const unsigned m = __ballot_sync(0xffffffffu, acc);
+                    if (acc) {
+                        const uint32_t dst = g_trk + n + __popc(m & ((1u << lane) - 1u));
+                        if (dst < O.track_capacity) {
+                            const uint4* s4 = reinterpret_cast<const uint4*>(A.fit_g + c_base + e);
+                            uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst);
+                            d4[0] = s4[0];
+                            d4[1] = s4[1];
+                        } else {
+                            overflow = true;
+                        }
+                    }
+                    n += __popc(m);
+                }
+            } else if (O.tracks && A.stage_trk) {
                 for (uint32_t e = lane; e < n_trk; e += 32) {
                     const uint32_t dst = g_trk + e;
                     if (dst < O.track_capacity && s_trk + e < A.stage_trk_cap) {
@@ -1221,9 +1244,17 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
         const uint32_t e_trk = i_trk - o_trk, e_kept = i_kept - o_kept, e_hits = i_hits - o_hits;
         const uint32_t t_trk = __shfl_sync(0xffffffffu, i_trk, 31), t_kept = __shfl_sync(0xffffffffu, i_kept, 31);
         const uint32_t t_hits = __shfl_sync(0xffffffffu, i_hits, 31);
+        // a warp-batch without track-overflow frame outputs exactly its accepted
+        // store entries: the pack kernel copies them from the fit records; only
+        // the others stage their (capped) tracks here
+        const unsigned m_tov = __ballot_sync(0xffffffffu, active && reason == M3E_REASON_TRACK_OVERFLOW);
+        const bool staged = ((m_tov >> fl) & ((1u << fb) - 1u)) != 0u;
+        const uint32_t so_trk = staged ? o_trk : 0u;
+        const uint32_t si_trk = warp_incl(so_trk), se_trk = si_trk - so_trk;
+        const uint32_t st_trk = __shfl_sync(0xffffffffu, si_trk, 31);
         uint32_t s_trk = 0, s_kept = 0;
         if (lane == 0) {
-            if (t_trk && A.stage_trk) s_trk = atomicAdd(A.ticket + 1, t_trk);
+            if (st_trk && A.stage_trk) s_trk = atomicAdd(A.ticket + 1, st_trk);
             if (t_kept) s_kept = atomicAdd(A.ticket + 2, t_kept);
         }
         s_trk = __shfl_sync(0xffffffffu, s_trk, 0);
@@ -1261,15 +1292,16 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
                 }
             }
         }
-        // the first o_trk accepted tracks of each frame, in candidate order: second
-        // coalesced pass (codes from L1/L2), one lane per candidate
-        if (A.stage_trk && t_trk) {
+        // staged warp-batches: the first o_trk accepted tracks of each frame, in
+        // candidate order (second pass over the codes, one lane per candidate)
+        if (A.stage_trk && st_trk) {
             S.cnt[warp][lane] = 0;
-            S.pos[warp][lane] = (int)(s_trk + e_trk);   // staging slot of the frame's first track
-            S.neg[warp][lane] = (int)o_trk;
+            S.pos[warp][lane] = (int)(s_trk + se_trk);   // staging slot of the frame's first track
+            S.neg[warp][lane] = (int)so_trk;
             __syncwarp();
             for (int q = 0; q < G; ++q) {
                 const int ql = q * fb;
+                if (!__shfl_sync(0xffffffffu, staged, ql)) continue;
                 const uint32_t qb = __shfl_sync(0xffffffffu, gb, ql);
                 const uint32_t qn = __shfl_sync(0xffffffffu, cin, min(ql + fb, 32) - 1) -
                                     __shfl_sync(0xffffffffu, cex, ql);
@@ -1305,15 +1337,19 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
         const uint32_t l_trk = __shfl_sync(0xffffffffu, i_trk, ll & 31);
         const uint32_t l_kept = __shfl_sync(0xffffffffu, i_kept, ll & 31);
         const uint32_t l_hits = __shfl_sync(0xffffffffu, i_hits, ll & 31);
+        const uint32_t l_cand = __shfl_sync(0xffffffffu, cin, ll & 31);
+        const uint32_t b_cand = __shfl_sync(0xffffffffu, cex, fl);
+        const uint32_t b_strk = __shfl_sync(0xffffffffu, se_trk, fl);
         if (inb && gb != kSpilled && lane == fl) {
             BatchStat bs;
             bs.n_trk = l_trk - b_trk;
             bs.n_kept = l_kept - b_kept;
             bs.n_hits = l_hits - b_hits;
-            bs.s_trk = s_trk + b_trk;
+            bs.s_trk = staged ? s_trk + b_strk : kSpilled;   // kSpilled: tracks = accepted store entries
             bs.s_kept = s_kept + b_kept;
             bs.nf = min(A.F - b * (uint32_t)fb, (uint32_t)fb);
-            bs.pad[0] = bs.pad[1] = 0;
+            bs.c_base = gb;
+            bs.c_n = l_cand - b_cand;
             A.bstat[b] = bs;
         }
         // run summary (per-warp counters in shared memory)

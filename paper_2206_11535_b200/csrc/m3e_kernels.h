@@ -37,9 +37,10 @@ constexpr int kPackTile = 256;       // warp-batches per CTA of the pack kernel 
 // consumed by the pack kernel (32 B)
 struct BatchStat {
     uint32_t n_trk, n_kept, n_hits;  // tracks, kept frames, hits of kept frames
-    uint32_t s_trk, s_kept;          // staging offsets of its tracks / kept-frame records
+    uint32_t s_trk, s_kept;          // staging offsets of its tracks / kept-frame records; s_trk =
+                                     // kSpilled: its tracks are its accepted store entries
     uint32_t nf;                     // frames in the warp-batch
-    uint32_t pad[2];
+    uint32_t c_base, c_n;            // its store entries (split path)
 };
 
 // kept-frame record staged by the filter kernel (64 B)
