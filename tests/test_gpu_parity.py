@@ -257,6 +257,27 @@ def test_full_parity(ctx, gp, P, name, n, seed):
         assert np.all(np.diff(tracks_np["frame"].astype(np.int64)) >= 0)
 
 
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_track_overflow_parity(cfg, monkeypatch, fused):
+    """max_tracks = 2: most frames with tracks overflow (R3), so the capped
+    track lists go through the staged path of the finish and pack kernels."""
+    c2 = dict(cfg, max_tracks=2)
+    gp2, P2 = m3e.make_params(c2), oracle.make_params(c2)
+    monkeypatch.setenv("M3E_FUSED", fused)
+    c = m3e.Context(0)
+    n = 3000
+    d, fr, df = _gen("phase1_sig", n, 801)
+    res = m3e.run_filter(c, gp2, df)
+    torch.cuda.synchronize()
+    sm = res.summary_np()
+    assert int(sm["overflow"]) == 0
+    frames_np = res.frames_np(n)
+    assert int(np.count_nonzero(frames_np["reason"] == m3e.REASON_TRACK_OVERFLOW)) > n // 4
+    explained = _compare_full(P2, fr, None, frames_np, res.tracks_np(int(sm["tracks"])), n)
+    assert len(explained) <= max(1, 2e-3 * n)
+    c.close()
+
+
 def _outputs(res, n):
     sm = res.summary_np()
     T, K = int(sm["tracks"]), int(sum(sm["kept_by_reason"][1:]))
