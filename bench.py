@@ -358,7 +358,7 @@ def main():
                          "kernels_ms": {"select": round(ms_select, 4), "fit": round(ms_fit, 4),
                                         "finish": round(ms_filter, 4), "pack": round(ms_pack, 4)},
                          "candidates_per_frame": round(cand / F, 3)},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (4 if split else 2) * a.steps, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 if split else 2) * a.steps, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
