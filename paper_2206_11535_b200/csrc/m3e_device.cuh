@@ -188,13 +188,9 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
     for (;;) {
         // 1. refill the pair list to >= 32 Phi_01 survivors (or all pairs)
         while (pn < 32 && pnext < np) {
-            bool pass = false;
-            int g0 = 0, g1 = 0;
-            if (j0 < n0) {
-                g0 = F.s[0] + j0;
-                g1 = F.s[1] + j1;
-                pass = (F.x[g0] * F.x[g1] + F.y[g0] * F.y[g1]) * P.inv_r0r1 >= P.c01_min;
-            }
+            // branch-free: lanes past the last pair test a clamped (valid) one
+            const int g0 = F.s[0] + min(j0, n0 - 1), g1 = F.s[1] + j1;
+            const bool pass = (j0 < n0) & ((F.x[g0] * F.x[g1] + F.y[g0] * F.y[g1]) * P.inv_r0r1 >= P.c01_min);
             const unsigned m = __ballot_sync(0xffffffffu, pass);
             if (pass) {
                 // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
@@ -213,18 +209,15 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
         // 2. expand the first K listed pairs against layer 2
         const int K = min(pn, 32), nk = K * n2;
         for (int cb = 0; cb < nk; cb += 32) {
-            const int c = cb + lane;
+            // branch-free: lanes past the end evaluate a clamped (valid) combination
+            const int c = min(cb + lane, nk - 1);
             const int k = (int)(((float)c + 0.5f) * in2), i2 = c - k * n2;
-            bool pass = false;
-            uint32_t pk = 0;
-            if (c < nk) {
-                const uint2 pe = pl[k];
-                pk = pe.x | ((uint32_t)i2 << 20);
-                const int g1 = F.s[1] + (int)(pe.x >> 10), g2 = F.s[2] + i2;
-                const float dl = fmaf(F.z[g2], P.inv_dr12, -__uint_as_float(pe.y));
-                const float c12 = (F.x[g1] * F.x[g2] + F.y[g1] * F.y[g2]) * P.inv_r1r2;
-                pass = (fabsf(dl) <= P.dl_max) & (c12 >= P.c12_min);
-            }
+            const uint2 pe = pl[k];
+            const uint32_t pk = pe.x | ((uint32_t)i2 << 20);
+            const int g1 = F.s[1] + (int)(pe.x >> 10), g2 = F.s[2] + i2;
+            const float dl = fmaf(F.z[g2], P.inv_dr12, -__uint_as_float(pe.y));
+            const float c12 = (F.x[g1] * F.x[g2] + F.y[g1] * F.y[g2]) * P.inv_r1r2;
+            const bool pass = (cb + lane < nk) & (fabsf(dl) <= P.dl_max) & (c12 >= P.c12_min);
             const unsigned m = __ballot_sync(0xffffffffu, pass);
             if (pass) q[qn + __popc(m & lt_mask)] = pk;
             qn += __popc(m);
