@@ -170,15 +170,13 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
     const int a1 = (int)(32.5f * in1), b1 = 32 - a1 * n1;                // step of 32 pairs
     int count = 0, qn = 0, pn = 0, pnext = 0;
     // r_tc for q[0..n) (n <= 32); true once the frame overflows
-    auto drain = [&](int n) -> bool {
+    auto drain = [&](int n) -> bool {   // branch-free: lanes >= n test a clamped entry
         float rt = 0.0f;
-        uint32_t pk = 0;
-        bool pass = false;
-        if (lane < n) {
-            pk = q[lane];
-            if constexpr (kRt) pass = pass_rtc(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
-            else pass = pass_rtc_sq(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u);
-        }
+        const uint32_t pk = q[min(lane, n - 1)];
+        bool pass;
+        if constexpr (kRt) pass = pass_rtc(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
+        else pass = pass_rtc_sq(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u);
+        pass = pass && lane < n;
         const unsigned m = __ballot_sync(0xffffffffu, pass);
         const int pos = count + __popc(m & lt_mask);
         if (pass && pos < P.cuts_max) emit(pos, pk, rt);
@@ -192,12 +190,10 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
             const int g0 = F.s[0] + min(j0, n0 - 1), g1 = F.s[1] + j1;
             const bool pass = (j0 < n0) & ((F.x[g0] * F.x[g1] + F.y[g0] * F.y[g1]) * P.inv_r0r1 >= P.c01_min);
             const unsigned m = __ballot_sync(0xffffffffu, pass);
-            if (pass) {
-                // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
-                const float z1 = F.z[g1];
-                const float u = z1 * P.inv_dr12 + (z1 - F.z[g0]) * P.inv_dr01;
-                pl[pn + __popc(m & lt_mask)] = make_uint2((uint32_t)j0 | ((uint32_t)j1 << 10), __float_as_uint(u));
-            }
+            // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
+            const float z1 = F.z[g1];
+            const float u = z1 * P.inv_dr12 + (z1 - F.z[g0]) * P.inv_dr01;
+            if (pass) pl[pn + __popc(m & lt_mask)] = make_uint2((uint32_t)j0 | ((uint32_t)j1 << 10), __float_as_uint(u));
             pn += __popc(m);
             pnext += 32;
             j1 += b1;
