@@ -530,15 +530,26 @@ M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet&
     const float hh = sqrtf(hh2);
     const float cux = cx * iC, cuy = cy * iC;
     const float ax = h2.x - cx, ay = h2.y - cy;
-    float best = 1e30f, bx = 0.0f, by = 0.0f;
+    // first crossing in the direction of motion: the smaller positive turning
+    // angle from h2, compared on a monotone pseudo-angle of (cross, dot) in
+    // (-2, 2] (no trigonometry); one atan2 for the chosen crossing's angle
+    float bestp = 1e30f, bx = 0.0f, by = 0.0f, bcr = 0.0f, bdt = 0.0f;
 #pragma unroll
     for (int s = -1; s <= 1; s += 2) {
         const float px = a * cux - s * hh * cuy, py = a * cuy + s * hh * cux;
         const float qx = px - cx, qy = py - cy;
-        // turning angle from h2 to p in the direction of motion, in [0, 2 pi)
-        float t = -T.q * atan2f(ax * qy - ay * qx, ax * qx + ay * qy);
-        if (t < 0.0f) t += 2.0f * kPiF;
-        if (t > 0.0f && t < best) { best = t; bx = px; by = py; }
+        const float cr = ax * qy - ay * qx, dt = ax * qx + ay * qy;
+        const float r = cr * rcp(fabsf(dt) + fabsf(cr));
+        float t = -T.q * (dt >= 0.0f ? r : (cr >= 0.0f ? 2.0f - r : -2.0f - r));
+        if (t < 0.0f) t += 4.0f;
+        if (t > 0.0f && t < bestp) { bestp = t; bx = px; by = py; bcr = cr; bdt = dt; }
+    }
+    // turning angle from h2 to the crossing in the direction of motion, in (0, 2 pi)
+    // (no crossing ahead, both at h2 itself: degenerate, as before 1e30)
+    float best = 1e30f;
+    if (bestp < 1e30f) {
+        best = -T.q * atan2f(bcr, bdt);
+        if (best < 0.0f) best += 2.0f * kPiF;
     }
     out = make_float3(bx, by, h2.z + cth * ik * best);
     return true;
