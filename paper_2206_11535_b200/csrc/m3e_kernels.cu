@@ -30,6 +30,9 @@
 #ifndef M3E_MIN_BLOCKS
 #define M3E_MIN_BLOCKS 4   // CTAs per SM the register allocation targets (64 regs: 32 warps/SM)
 #endif
+#ifndef M3E_NO_FLAT_SELECT
+#define M3E_NO_FLAT_SELECT 0   // 1: the selection kernel walks frame by frame (select_frame_warp) only
+#endif
 #ifndef M3E_MIN_BLOCKS_SEL
 #define M3E_MIN_BLOCKS_SEL 4   // same for the selection kernel of the split path
 #endif
@@ -102,6 +105,16 @@ struct BatchState {
 constexpr int kNBuf = 1;
 constexpr int kCandSmem = 256;   // candidates of a warp-batch kept in shared memory
 
+// Shared state of select_batch_flat (one warp-batch, frames j < kFB)
+struct FlatSel {
+    uint4 pl[64];      // Phi_01 pair list {g0 | g1 << 8 | s2 << 16 | j << 24, u bits, n2, 0} (g = staging-window
+                       // index); after the walk: per-frame table {list start, store prefix, s0 | s1 << 8 |
+                       // s2 << 16, stored}
+    uint4 rec[kFB];    // frames with pairs, by rank: {pair prefix, s0 | s1 << 8 | s2 << 16 | j << 24,
+                       // n1 | n2 << 8, 1/n1 bits}
+    int cnt[kFB];      // Selection-Cut survivors per frame
+};
+
 // Cold vertex-stage scratch of one warp, in global memory (L1/L2 resident;
 // touched for ~1.5% of frames), so that it does not cost shared memory.
 struct VScratch {
@@ -117,13 +130,18 @@ struct __align__(16) WarpSmem {
     uint32_t offs[kNBuf][4 * kFB + 4];
     uint64_t bar[kNBuf];
     uint32_t b_batch[kNBuf], b_winlo[kNBuf], b_winhi[kNBuf];
-    uint32_t cidx[kCandSmem];        // candidates (flat warp-batch index < kCandSmem), FULL mode
-    float crt[kCandSmem];
+    uint32_t cidx[kCandSmem];        // candidates (flat warp-batch index < kCandSmem)
+    union {
+        struct {                     // per-frame selection (select_frame_warp) and the fused stages
+            float crt[kCandSmem];
+            uint2 pl[64];            // Phi_01 pair list: {i0 | i1 << 10, u(i0, i1)}
+        };
+        FlatSel fl;                  // warp-batch-flat selection (select_batch_flat)
+    };
     BatchState st;
     uint32_t pref[kFB + 1];          // candidates: exclusive prefix
     int npos[kFB];                   // stored positive tracks per frame (vertex gate)
     uint32_t q[64];                  // Delta-lambda + Phi_12 survivors (selection FIFO)
-    uint2 pl[64];                    // Phi_01 pair list of the selection: {i0 | i1 << 10, u(i0, i1)}
     uint32_t acc[12];                // run summary: kept_by_reason[6], cand, frames, tracks, hits, overflow
 };
 
@@ -206,6 +224,17 @@ __device__ __forceinline__ void warp_scan(uint32_t* v, int n) {
     __syncwarp();
 }
 
+// inclusive warp prefix sum
+__device__ __forceinline__ uint32_t warp_incl(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
 // largest j in [0, n) with pref[j] <= e (pref non-decreasing, pref[0] = 0)
 __device__ __forceinline__ int find_frame(const uint32_t* pref, int n, uint32_t e) {
     int lo = 0, hi = n - 1;
@@ -255,6 +284,196 @@ __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) 
     }
     if (lane == 0) st_volatile_v4(A.status + b, make_uint4(tagI, ex.x + agg.x, ex.y + agg.y, ex.z + agg.z));
     return ex;
+}
+
+// Selection Cuts (Alg. 2, Eq. 2-5) of a whole staged warp-batch as ONE flat walk
+// (production path, SELECT_C): the (i0, i1) pairs of all frames of the
+// warp-batch are enumerated as one index space, 32 per step, frame after frame
+// and row-major inside a frame, so no lane idles at a frame boundary (phase-I
+// frames have ~40 pairs: one warp per frame leaves most lanes idle).  Factorised
+// by hit dependence as select_frame_warp: Phi_01 on pairs -> ballot pair list;
+// Delta-lambda + Phi_12 on listed pairs x layer-2 hits (again flat over the
+// pairs of up to 32 list entries) -> FIFO; r_tc window on full warps of the FIFO.
+// The element -> (frame, pair) lookup is a ballot search: the segments starting
+// inside the step's 32 elements set one bit each (redux.or), a lane's segment is
+// the popcount of the bits at or below it.  Survivors keep the order (frame, i0,
+// i1, i2) of Alg. 2, are counted per frame (match_any) and capped at cuts_max
+// (R3: n_cand = min(#survivors, cuts_max + 1); overflow frames store nothing),
+// then written to the candidate store at one atomicAdd per warp-batch.
+// Eligible warp-batches: all frames inside the staging window and every frame
+// with n0 n1 n2 <= kBigCombos (so the walk of an overflowing frame is bounded);
+// returns false, having written nothing, for the others (per-frame path).
+__device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, uint32_t b, uint32_t f0, int nf,
+                                                  uint32_t* gl) {
+    const DevParams& P = A.P;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u, le = lt | (1u << lane);
+    if (W.offs[0][4 * nf] > W.b_winhi[0]) return false;   // warp-batch larger than the window
+    FlatSel& S = W.fl;
+    const float* hx = W.hx[0];
+    const float* hy = W.hy[0];
+    const float* hz = W.hz[0];
+    // lane j = frame j: window-relative layer starts and counts
+    const bool isf = lane < nf;
+    const uint32_t* o = W.offs[0] + 4 * (isf ? lane : 0);
+    const uint32_t wlo = W.b_winlo[0];
+    const int s0 = (int)(o[0] - wlo), s1 = (int)(o[1] - wlo), s2 = (int)(o[2] - wlo);
+    const int n0 = isf ? (int)(o[1] - o[0]) : 0, n1 = (int)(o[2] - o[1]), n2 = (int)(o[3] - o[2]);
+    if (__any_sync(0xffffffffu, n0 * n1 * n2 > (int)kBigCombos)) return false;
+    const int np = n2 > 0 ? n0 * n1 : 0;
+    const uint32_t pa_i = warp_incl((uint32_t)np);
+    const uint32_t NP = __shfl_sync(0xffffffffu, pa_i, 31);
+    const unsigned nem = __ballot_sync(0xffffffffu, np > 0);
+    const uint32_t sp = (uint32_t)s0 | ((uint32_t)s1 << 8) | ((uint32_t)s2 << 16);
+    if (np > 0)
+        S.rec[__popc(nem & lt)] = make_uint4(pa_i - (uint32_t)np, sp | ((uint32_t)lane << 24),
+                                             (uint32_t)n1 | ((uint32_t)n2 << 8), __float_as_uint(rcp((float)n1)));
+    if (lane < kFB) S.cnt[lane] = 0;
+    __syncwarp();
+    // segment starts held by lane = rank (no bit for lanes past the last segment)
+    const uint32_t PAr = lane < __popc(nem) ? S.rec[lane].x : 0xFFFFFFFFu;
+
+    int pn = 0, qn = 0, L = 0, cbA = 0;
+    uint32_t pnext = 0;
+    // r_tc window (on squares, as pass_rtc_sq) for q[0..n); survivors counted per
+    // frame and appended to the warp-batch list
+    auto drain = [&](int n) {
+        const uint32_t pk = W.q[min(lane, n - 1)];
+        const int g0 = (int)(pk & 255u), g1 = (int)((pk >> 8) & 255u), g2 = (int)((pk >> 16) & 255u);
+        const int j = (int)(pk >> 24);
+        const float x1 = hx[g1], y1 = hy[g1];
+        const float ax = hx[g0] - x1, ay = hy[g0] - y1, bx = hx[g2] - x1, by = hy[g2] - y1;
+        const float cx = bx - ax, cy = by - ay;
+        const float cz = ax * by - ay * bx;
+        const float num = (ax * ax + ay * ay) * (bx * bx + by * by) * (cx * cx + cy * cy);
+        const float den = 4.0f * cz * cz;
+        const bool pass = (lane < n) & (cz != 0.0f) & (num >= den * P.rt_min2) & (num <= den * P.rt_max2);
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        const unsigned grp = __match_any_sync(0xffffffffu, j);
+        const int cj = S.cnt[j];
+        const bool keep = pass && cj + __popc(m & grp & lt) < P.cuts_max;
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int idx = L + __popc(mk & lt);
+            if (idx < kCandSmem) W.cidx[idx] = pk; else gl[idx] = pk;
+        }
+        __syncwarp();
+        if (lane == __ffs(grp) - 1) S.cnt[j] = cj + __popc(m & grp);
+        __syncwarp();
+        L += __popc(mk);
+    };
+    for (;;) {
+        // 1. refill the pair list to >= 32 Phi_01 survivors (or all pairs)
+        while (pn < 32 && pnext < NP) {
+            const uint32_t bit = PAr - pnext < 32u ? 1u << (PAr - pnext) : 0u;
+            const unsigned M = __reduce_or_sync(0xffffffffu, bit);
+            const uint4 rc = S.rec[cbA + __popc(M & le) - 1];
+            cbA += __popc(M);
+            const uint32_t e = pnext + lane;
+            const int r = (int)(e - rc.x);
+            // (i0, i1) = divmod(r, n1): floor((r + 0.5) / n1), exact for r < 2^15 (see select_frame_warp)
+            const int i0 = (int)(((float)r + 0.5f) * __uint_as_float(rc.w));
+            const int i1 = r - i0 * (int)(rc.z & 255u);
+            const int g0 = (int)(rc.y & 255u) + i0, g1 = (int)((rc.y >> 8) & 255u) + i1;
+            const float x1 = hx[g1], y1 = hy[g1];
+            const bool pass = (e < NP) & ((hx[g0] * x1 + hy[g0] * y1) * P.inv_r0r1 >= P.c01_min);
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            if (pass) {
+                // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
+                const float z1 = hz[g1];
+                const float u = z1 * P.inv_dr12 + (z1 - hz[g0]) * P.inv_dr01;
+                S.pl[pn + __popc(m & lt)] = make_uint4((uint32_t)g0 | ((uint32_t)g1 << 8) | (rc.y & 0xFFFF0000u),
+                                                       __float_as_uint(u), rc.z >> 8, 0u);
+            }
+            pn += __popc(m);
+            pnext += 32;
+        }
+        if (pn == 0) break;
+        __syncwarp();
+        // 2. the first K listed pairs x their frame's layer-2 hits, flat
+        const int K = min(pn, 32);
+        const uint32_t w = lane < K ? S.pl[lane].z : 0u;
+        const uint32_t pb_i = warp_incl(w), PB = pb_i - w;
+        const int WT = (int)__shfl_sync(0xffffffffu, pb_i, 31);
+        const uint32_t PBr = lane < K ? PB : 0xFFFFFFFFu;
+        int cbB = 0;
+        for (int base = 0; base < WT; base += 32) {
+            const uint32_t bit = PBr - (uint32_t)base < 32u ? 1u << (PBr - (uint32_t)base) : 0u;
+            const unsigned M = __reduce_or_sync(0xffffffffu, bit);
+            const int kk = cbB + __popc(M & le) - 1;
+            cbB += __popc(M);
+            const uint4 pe = S.pl[kk];
+            const int e = base + lane;
+            const int g2 = (int)((pe.x >> 16) & 255u) + (e - (int)__shfl_sync(0xffffffffu, PB, kk));
+            const int g1 = (int)((pe.x >> 8) & 255u);
+            const float dl = fmaf(hz[g2], P.inv_dr12, -__uint_as_float(pe.y));
+            const float c12 = (hx[g1] * hx[g2] + hy[g1] * hy[g2]) * P.inv_r1r2;
+            const bool pass = (e < WT) & (fabsf(dl) <= P.dl_max) & (c12 >= P.c12_min);
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            if (pass) W.q[qn + __popc(m & lt)] = (pe.x & 0xFF00FFFFu) | ((uint32_t)g2 << 16);
+            qn += __popc(m);
+            if (qn >= 32) {
+                __syncwarp();
+                drain(32);
+                const uint32_t v = lane < qn - 32 ? W.q[32 + lane] : 0u;
+                __syncwarp();
+                if (lane < qn - 32) W.q[lane] = v;
+                qn -= 32;
+            }
+            __syncwarp();
+        }
+        // drop the K expanded pairs
+        const uint4 v = lane < pn - K ? S.pl[K + lane] : make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+        if (lane < pn - K) S.pl[lane] = v;
+        pn -= K;
+        __syncwarp();
+    }
+    if (qn > 0) drain(qn);
+    __syncwarp();
+
+    // per-frame results (lane j): n_cand, reason, list start, store prefix
+    const int c = isf ? S.cnt[lane] : 0;
+    const int count = min(c, P.cuts_max + 1);
+    const int reason = count > P.cuts_max ? M3E_REASON_TRIPLET_OVERFLOW : M3E_REASON_NONE;
+    const uint32_t ns = reason == M3E_REASON_NONE ? (uint32_t)c : 0u;
+    const uint32_t lc = (uint32_t)min(c, P.cuts_max);
+    const uint32_t ls = warp_incl(lc) - lc;
+    const uint32_t sp_i = warp_incl(ns);
+    const uint32_t tot = __shfl_sync(0xffffffffu, sp_i, 31);
+    if (isf) {
+        A.sel[f0 + lane] = (uint32_t)count | ((uint32_t)reason << 16);
+        S.pl[lane] = make_uint4(ls, sp_i - ns, sp, ns);
+    }
+    unsigned long long base = 0;
+    if (lane == 0 && tot) base = atomicAdd(reinterpret_cast<unsigned long long*>(A.ticket + 6), tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const bool fits = base + tot <= A.cand_cap;
+    __syncwarp();
+    if (fits) {
+        // list entry e of frame j -> store entry base + store prefix + (e - list start);
+        // entries of overflow frames are dropped
+        for (int e = lane; e < L; e += 32) {
+            const uint32_t pk = e < kCandSmem ? W.cidx[e] : gl[e];
+            const uint32_t j = pk >> 24;
+            const uint4 ft = S.pl[j];
+            if (ft.w) {
+                const uint32_t i0 = (pk & 255u) - (ft.z & 255u), i1 = ((pk >> 8) & 255u) - ((ft.z >> 8) & 255u),
+                               i2 = ((pk >> 16) & 255u) - ((ft.z >> 16) & 255u);
+                A.cand_g[base + ft.y + ((uint32_t)e - ft.x)] =
+                    make_uint4(i0 | (i1 << 10) | (i2 << 20), 0u, f0 + j, j);
+            }
+        }
+    } else {
+        // a warp-batch that does not fit leaves its (partial) range marked unused
+        const uint32_t nw = base < A.cand_cap ? (uint32_t)(A.cand_cap - base) : 0u;
+        for (uint32_t e = lane; e < nw; e += 32) A.cand_g[base + e] = make_uint4(0u, 0u, kSpilled, 0u);
+    }
+    if (lane == 0) {
+        A.bsel[b] = fits ? (uint32_t)base : kSpilled;
+        if (!fits) A.spill_out[atomicAdd(A.ticket + 5, 1u)] = b;   // for the fused kernel
+    }
+    return true;
 }
 
 // Vertex selection of frame j (Sec. IV-C, Alg. 4; whole warp), out of line: it
@@ -443,7 +662,12 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
         m3e_track* ctrk = ctrk_base;
 
         // ---------------------------------------------------- S: Selection Cuts
+        // production path: the whole warp-batch as one flat walk (eligible
+        // warp-batches; the per-frame walk below handles the others)
+        bool flat_done = false;
+        if constexpr (MODE == kModeSelectC && !M3E_NO_FLAT_SELECT) flat_done = select_batch_flat(A, W, b, f0, nf, cidx);
         if constexpr (MODE == kModeFull || MODE == kModeSelect || MODE == kModeSelectC) {
+          if (!flat_done) {
             uint32_t cbase = 0;   // flat: candidate index of frame j's first candidate
             for (int j = 0; j < nf; ++j) {
                 const Frame Fv = frame_view(A, W, buf, j);
@@ -504,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
                 }
                 cbase += r == M3E_REASON_NONE ? (uint32_t)count : 0u;
             }
+          }
         } else if constexpr (MODE == kModeFit) {
             for (int j = lane; j < nf; j += 32) {
                 const int n = A.s_ncand[f0 + j];
@@ -530,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
         }
         __syncwarp();
 
-        if constexpr (MODE == kModeSelectC) {   // candidates -> store, warp-batch contiguous
+        if (MODE == kModeSelectC && !flat_done) {   // candidates -> store, warp-batch contiguous
             for (int j = lane; j < nf; j += 32) {
                 A.sel[f0 + j] = (uint32_t)B.ncand[j] | ((uint32_t)B.reason[j] << 16);
                 W.pref[j] = (uint32_t)B.nstored[j];
@@ -1086,15 +1311,6 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
 // every global round trip serves up to 32 frames.  Results are identical to the
 // fused kernel's stages T, V and O (frame records warp-batch relative, tracks
 // and kept-frame records staged, BatchStat per warp-batch for the pack kernel).
-__device__ __forceinline__ uint32_t warp_incl(uint32_t v) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
-    }
-    return v;
-}
 
 struct FinishSmem {
     DevParams P;

@@ -311,6 +311,72 @@ def test_split_spill_and_fused_agree(gp, monkeypatch, store):
             assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("cuts_max", [3, 8, 40])
+def test_flat_selection_cap(cfg, monkeypatch, cuts_max):
+    """The production selection walks each warp-batch flat across frames and caps
+    survivors per frame (R3).  With a small cuts_max many phase-I frames overflow
+    inside one warp-batch, next to frames that do not: outputs must be
+    byte-identical to the fused kernel's frame-by-frame walk and match the oracle
+    run with the same cap."""
+    c2 = dict(cfg, cuts_max=cuts_max)
+    gp2, P2 = m3e.make_params(c2), oracle.make_params(c2)
+    n = 4000
+    d, fr, df = _gen("phase1_sig", n, 900 + cuts_max)
+    outs = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("M3E_FUSED", fused)
+        c = m3e.Context(0)
+        res = m3e.run_filter(c, gp2, df)
+        torch.cuda.synchronize()
+        outs.append(_outputs(res, n))
+        if fused == "0":
+            sm = res.summary_np()
+            frames_np = res.frames_np(n)
+            n_ov = int(np.count_nonzero(frames_np["reason"] == m3e.REASON_TRIPLET_OVERFLOW))
+            if cuts_max < 10:
+                assert n_ov > n // 20
+            assert np.all(frames_np["n_cand"] <= cuts_max + 1)
+            explained = _compare_full(P2, fr, None, frames_np, res.tracks_np(int(sm["tracks"])), n)
+            assert len(explained) <= max(1, 2e-3 * n)
+        c.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+
+
+def test_flat_selection_dense_frame(ctx, gp, P, cfg):
+    """A dense frame (11 hits per layer on one helix bundle: > cuts_max survivors
+    among <= 4096 combinations) inside a warp-batch of ordinary frames: the flat
+    walk marks it TRIPLET_OVERFLOW, keeps n_cand = cuts_max + 1 and leaves the
+    neighbours' candidates untouched."""
+    n = 48
+    d = synth.generate(synth.preset("phase1_sig", seed=931), n)
+    R = cfg["layer_r"]
+    rng = np.random.default_rng(5)
+    off = d["offsets"].astype(np.int64)
+    xs, ys, zs, noff = [], [], [], [0]
+    for f in range(n):
+        for layer in range(4):
+            lo, hi = off[4 * f + layer], off[4 * f + layer + 1]
+            if f == 7:
+                for _ in range(11):
+                    a = 0.3 + R[layer] / 160 + rng.normal() * 1e-3
+                    xs.append(R[layer] * math.cos(a)); ys.append(R[layer] * math.sin(a)); zs.append(rng.normal() * 0.5)
+            else:
+                xs.extend(d["x"][lo:hi]); ys.extend(d["y"][lo:hi]); zs.extend(d["z"][lo:hi])
+            noff.append(len(xs))
+    d2 = {"x": np.array(xs, np.float32), "y": np.array(ys, np.float32), "z": np.array(zs, np.float32),
+          "offsets": np.array(noff, np.uint32)}
+    res = m3e.run_filter(ctx, gp, m3e.DeviceFrames(d2))
+    torch.cuda.synchronize()
+    fo = res.frames_np(n)
+    assert int(fo["reason"][7]) == m3e.REASON_TRIPLET_OVERFLOW
+    assert int(fo["n_cand"][7]) == P.cuts_max + 1
+    fr2 = oracle.Frames(d2)
+    sm = res.summary_np()
+    explained = _compare_full(P, fr2, None, fo, res.tracks_np(int(sm["tracks"])), n)
+    assert len(explained) <= 1
+
+
 def test_host_path_matches_device(ctx, gp):
     """m3e_filter_host (chunked, two streams) == m3e_filter on the same frames."""
     n = 5000
