@@ -46,6 +46,18 @@ M3E_HD float rcp(float x) {
     return 1.0f / x;
 #endif
 }
+// sqrt: one MUFU.SQRT (sqrt.approx.ftz, ~1 ulp) instead of the IEEE-rounded
+// sequence with its slow-path branch: the fit is compared at 1e-4 and the
+// Selection Cuts' decisions at 1e-5 relative of a threshold
+M3E_HD float fsqrt(float x) {
+#ifdef __CUDA_ARCH__
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+#else
+    return sqrtf(x);
+#endif
+}
 // sin / cos of 0 <= x <= pi/2 by Taylor polynomials of degree 11 / 12
 // (truncation < 6e-8 absolute on the interval; no range reduction needed).
 M3E_HD void sincos_half(float x, float& s, float& c) {
@@ -94,7 +106,7 @@ M3E_HD float circle_radius(float3 h0, float3 h1, float3 h2) {
     float cz = ax * by - ay * bx;
     if (cz == 0.0f) return kInfF;
     float cx = h2.x - h0.x, cy = h2.y - h0.y;
-    float d01 = sqrtf(ax * ax + ay * ay), d12 = sqrtf(bx * bx + by * by), d20 = sqrtf(cx * cx + cy * cy);
+    float d01 = fsqrt(ax * ax + ay * ay), d12 = fsqrt(bx * bx + by * by), d20 = fsqrt(cx * cx + cy * cy);
     return d01 * d12 * d20 * rcp(2.0f * cz);
 }
 
@@ -430,15 +442,15 @@ M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
         const float dx = H[a + 1].x - H[a].x, dy = H[a + 1].y - H[a].y, z = H[a + 1].z - H[a].z;
-        const float d = sqrtf(dx * dx + dy * dy);
+        const float d = fsqrt(dx * dx + dy * dy);
         float s = d * (0.5f * ir);
         s = fminf(s, 1.0f);
         const float phc = 2.0f * asinf(s);
-        const float den = sqrtf(r * r * phc * phc + z * z);
+        const float den = fsqrt(r * r * phc * phc + z * z);
         const float iden = rcp(den);
         const float kc = phc * iden;
         const float cth = z * iden, sth = r * phc * iden;
-        const float ch = sqrtf(fmaxf(0.0f, 1.0f - s * s));     // cos(Phi_C / 2)
+        const float ch = fsqrt(fmaxf(0.0f, 1.0f - s * s));     // cos(Phi_C / 2)
         // dPhi/dk = (2/k^3) / (d^2 cos(Phi/2) / (4 sin^3(Phi/2)) + 2 z^2/Phi^3), sin(Phi_C/2) = d/(2r)
         const float iphc = rcp(phc), ikc = rcp(kc);
         const float dphi = 2.0f * ikc * ikc * ikc * rcp(r * r * ch * rcp(s) + 2.0f * z * z * iphc * iphc * iphc);
@@ -507,12 +519,12 @@ M3E_HD_CALL bool arc_phi(float d, float z, float k, float start, float& phi) {
 M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet& T, float3& out) {
     const float k = T.khat;
     const float dx = h2.x - h1.x, dy = h2.y - h1.y, z = h2.z - h1.z;
-    const float d = sqrtf(dx * dx + dy * dy);
+    const float d = fsqrt(dx * dx + dy * dy);
     float phi;
     if (!arc_phi(d, z, k, T.phc[1] + T.dphi[1] * (k - T.kc[1]), phi)) return false;
     const float ik = rcp(k);
     const float cth = fminf(fmaxf(z * k * rcp(phi), -1.0f), 1.0f);
-    const float rt = sqrtf(1.0f - cth * cth) * ik;
+    const float rt = fsqrt(1.0f - cth * cth) * ik;
     // heading at h2 = chord direction turned by -q phi/2 (a clockwise arc turns by -phi)
     float sh, ch;
     sincos_half(0.5f * phi, sh, ch);
@@ -520,14 +532,14 @@ M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet&
     const float ex = ux * ch + T.q * uy * sh, ey = uy * ch - T.q * ux * sh;
     // centre: clockwise (q = +1) to the right of the heading
     const float cx = h2.x + T.q * rt * ey, cy = h2.y - T.q * rt * ex;
-    const float C2 = cx * cx + cy * cy, C = sqrtf(C2);
+    const float C2 = cx * cx + cy * cy, C = fsqrt(C2);
     if (C == 0.0f) return false;
     // crossings of |p| = r3 and |p - c| = rt: p = a c^ +- hh n^ (no trigonometry)
     const float iC = rcp(C);
     const float a = (P.R3sq - rt * rt + C2) * 0.5f * iC;
     const float hh2 = P.R3sq - a * a;
     if (hh2 < 0.0f) return false;                    // the helix never reaches layer 3
-    const float hh = sqrtf(hh2);
+    const float hh = fsqrt(hh2);
     const float cux = cx * iC, cuy = cy * iC;
     const float ax = h2.x - cx, ay = h2.y - cy;
     // first crossing in the direction of motion: the smaller positive turning
@@ -599,12 +611,12 @@ M3E_HD FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, 
     const float k = fabsf(kb);
     const int q = kb > 0.0f ? 1 : -1;
     const float dx = h1.x - h0.x, dy = h1.y - h0.y, z01 = h1.z - h0.z;
-    const float d01 = sqrtf(dx * dx + dy * dy);
+    const float d01 = fsqrt(dx * dx + dy * dy);
     float phi01;
     if (!arc_phi(d01, z01, k, T1.phc[0] + T1.dphi[0] * (k - T1.kc[0]), phi01)) { o.status = 6; return o; }
     const float cth = fminf(fmaxf(z01 * k * rcp(phi01), -1.0f), 1.0f);
-    const float rt = sqrtf(1.0f - cth * cth) * rcp(k);
-    const float off = sqrtf(fmaxf(0.0f, rt * rt - 0.25f * d01 * d01));
+    const float rt = fsqrt(1.0f - cth * cth) * rcp(k);
+    const float off = fsqrt(fmaxf(0.0f, rt * rt - 0.25f * d01 * d01));
     const float id01 = rcp(d01);
     const float ux = dx * id01, uy = dy * id01;
     o.cth01 = cth;
@@ -702,18 +714,27 @@ static __device__ __noinline__ VResult vertex_triple(const DevParams* __restrict
         }
         if (npt[pi] == 0) return best;
     }
+    // Eq. 10 (R13) weight of every intersection point, once per point (the
+    // choice loop below combines them 2^3 ways)
+    double s2p[3][2];
+    for (int pi = 0; pi < 3; ++pi) {
+        const VTrk& A = T[pr[pi][0]];
+        const VTrk& B = T[pr[pi][1]];
+        for (int s = 0; s < npt[pi]; ++s) {
+            const double px = pts[pi][s][0], py = pts[pi][s][1];
+            const double sa = A.rt * fabs(turn_to_h0(A, px, py));
+            const double sb = B.rt * fabs(turn_to_h0(B, px, py));
+            s2p[pi][s] = 0.5 * (A.sms * A.sms * sa * sa + B.sms * B.sms * sb * sb) + P.sig_pix2;
+        }
+    }
     for (int s0 = 0; s0 < npt[0]; ++s0)
         for (int s1 = 0; s1 < npt[1]; ++s1)
             for (int s2 = 0; s2 < npt[2]; ++s2) {
                 const int sel[3] = {s0, s1, s2};
                 double mx = 0.0, my = 0.0, ws = 0.0;
-                for (int pi = 0; pi < 3; ++pi) {                           // Eq. 10 (R13), Eq. 9
+                for (int pi = 0; pi < 3; ++pi) {                           // Eq. 9
                     const double px = pts[pi][sel[pi]][0], py = pts[pi][sel[pi]][1];
-                    const VTrk& A = T[pr[pi][0]];
-                    const VTrk& B = T[pr[pi][1]];
-                    const double sa = A.rt * fabs(turn_to_h0(A, px, py));
-                    const double sb = B.rt * fabs(turn_to_h0(B, px, py));
-                    const double s2v = 0.5 * (A.sms * A.sms * sa * sa + B.sms * B.sms * sb * sb) + P.sig_pix2;
+                    const double s2v = s2p[pi][sel[pi]];
                     mx += px / s2v; my += py / s2v; ws += 1.0 / s2v;
                 }
                 mx /= ws; my /= ws;
