@@ -228,7 +228,7 @@ def main():
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize(dev)
-    ctx.set_timing(True)   # CUDA events around each of the two kernels, on the launch stream
+    ctx.set_timing(True)   # CUDA events around each kernel of the path, on the launch stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     if world > 1:
         dist.barrier()
@@ -243,7 +243,7 @@ def main():
         dist.barrier()
     ms = [s.elapsed_time(e) for s, e in ev]
     ms_step = statistics.mean(ms)
-    ms_select, ms_fit, ms_filter, ms_pack = ctx.kernel_times()
+    ms_select, ms_fit, ms_tracks, ms_vertex, ms_filter, ms_pack = ctx.kernel_times()
     sm = res.summary_np()
     kept = int(sum(sm["kept_by_reason"][1:]))
     assert int(sm["frames"]) == F and not int(sm["overflow"]), "output capacity exceeded"
@@ -318,8 +318,10 @@ def main():
         # algorithmic bytes per launch:
         #   selection kernel: hit stream in, selection words (4 B/frame) + store entries (16 B) out
         #   fit kernel: store entries + the candidates' frames (hit stream) in, fit records (32 B) out
-        #   finish kernel (+ the fused kernel over spilled warp-batches, ~0): offsets +
-        #   selection words + fit records in, per-frame outputs, tracks, kept records out
+        #   tracks kernel: selection words + code bytes (1 B per entry) in, track words out
+        #   vertex kernel: the listed frames' fit records + hits in (~1% of frames), small
+        #   finish kernel (+ the fused kernel over spilled warp-batches, ~0): selection
+        #   and track words in, per-frame outputs, kept records out
         #   (fused path: one kernel, hit stream in + outputs)
         split = ms_select > 0
         cand = int(sm["candidates"])
@@ -327,7 +329,8 @@ def main():
         if split:
             kernels = [("m3e::filter_kernel<SELECT_C, BIG=false>", ms_select, in_bytes + 4 * F + 16 * cand),
                        ("m3e::fit_kernel", ms_fit, in_bytes + 16 * cand + 32 * cand),
-                       ("m3e::finish_kernel", ms_filter, 16 * F + 4 * F + 32 * cand + out_bytes)]
+                       ("m3e::tracks_kernel", ms_tracks, 4 * F + cand + 4 * F),
+                       ("m3e::finish_kernel", ms_filter, 8 * F + F * (1 + 16) + kept * 64)]
         else:
             kernels = [("m3e::filter_kernel<FULL, BIG=%s>" % ("true" if big else "false"), ms_filter,
                         in_bytes + out_bytes)]
@@ -356,9 +359,10 @@ def main():
                          "kernel": kname, "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms_step, 4),
                          "algorithmic_bytes_per_launch": int(alg_bytes),
                          "kernels_ms": {"select": round(ms_select, 4), "fit": round(ms_fit, 4),
+                                        "tracks": round(ms_tracks, 4), "vertex": round(ms_vertex, 4),
                                         "finish": round(ms_filter, 4), "pack": round(ms_pack, 4)},
                          "candidates_per_frame": round(cand / F, 3)},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 if split else 2) * a.steps, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (7 if split else 2) * a.steps, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

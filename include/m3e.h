@@ -149,7 +149,12 @@ const char* m3e_version(void);
 const char* m3e_last_error(void);
 
 /* Opaque context: device workspace, streams, CUDA graph, pinned staging.
- * max_frames / max_hits bound one call (device side); device = CUDA ordinal. */
+ * max_frames / max_hits bound one call (device side); device = CUDA ordinal.
+ * Environment read here (testing knobs, results never change): M3E_FUSED=1 runs
+ * the single fused filter kernel; M3E_CAND_STORE=n sizes the candidate store at
+ * n entries per frame (warp-batches that do not fit are re-selected by the fused
+ * kernel); M3E_TRI_CAP=n caps the vertex stage's triple list (frames whose
+ * triples do not fit are decided in place). */
 typedef struct m3e_context m3e_context;
 int m3e_create(m3e_context** ctx, int device, uint64_t max_frames, uint64_t max_hits);
 int m3e_destroy(m3e_context* ctx);
@@ -159,13 +164,15 @@ uint64_t m3e_workspace_bytes(const m3e_context* ctx);
  * stream around each of its kernels (up to 1024 calls); m3e_kernel_times()
  * waits for them and returns the MEAN durations in ms over those calls, then
  * resets the record:
- *   ms[0] selection kernel, ms[1] fit kernel (both 0 when the call ran the
- *   single fused filter kernel), ms[2] filter kernel (vertex selection and
- *   output staging; the whole path on the fused variant), ms[3] pack kernel.
+ *   ms[0] selection kernel, ms[1] fit kernel, ms[2] track kernel, ms[3] vertex
+ *   kernel (all four 0 when the call ran the single fused filter kernel),
+ *   ms[4] output-staging kernel plus the fused filter kernel over warp-batches the
+ *   candidate store could not take (the whole path on the fused variant),
+ *   ms[5] pack kernel.
  * The split path is the default; M3E_FUSED=1 in the environment at m3e_create
  * selects the single fused kernel (same results). */
 int m3e_set_timing(m3e_context* ctx, int enable);
-int m3e_kernel_times(m3e_context* ctx, float ms[4]);
+int m3e_kernel_times(m3e_context* ctx, float ms[6]);
 
 /* Full hot path on device-resident input (the call bench.py times):
  * select -> fit -> vertex -> pack for frames [0, F).  Outputs [dev]. */

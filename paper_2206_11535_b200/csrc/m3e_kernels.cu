@@ -1305,157 +1305,416 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
     }
 }
 
-// --------------------------------------------------------- finish kernel ----
-// Split path, T + V + O for the warp-batches fitted by fit_kernel: one warp
-// takes G = 32 / fb consecutive warp-batches at a time, one lane per frame, so
-// every global round trip serves up to 32 frames.  Results are identical to the
-// fused kernel's stages T, V and O (frame records warp-batch relative, tracks
-// and kept-frame records staged, BatchStat per warp-batch for the pack kernel).
+// ------------------------------------------- tracks / vertex / finish kernels ----
+// Split path, T + V + O for the warp-batches fitted by fit_kernel, as three
+// kernels so that each has no out-of-line call (no ABI register saves in its
+// loop) and its hot code in the instruction cache:
+//   tracks_kernel  T: one warp takes G = 32 / fb consecutive warp-batches at a
+//                  time, one lane per frame: accepted tracks and charges from the
+//                  code bytes, track-overflow decision; frames with e+ e+ e-
+//                  candidates are listed for the vertex stage;
+//   vertex_kernel  V: one warp per listed frame, fp64 (Alg. 4);
+//   finish_kernel  O: frame records in place (warp-batch relative offsets),
+//                  kept-frame records and the tracks of warp-batches with a
+//                  track-overflow frame staged, BatchStat per warp-batch.
+// Results are identical to the fused kernel's stages T, V and O.
 
-struct FinishSmem {
-    DevParams P;
-    uint32_t acc[kWarps][12];
-    int cnt[kWarps][33], neg[kWarps][33], pos[kWarps][33];   // per frame lane (+1 for invalid lanes)
+// group of G warp-batches of one warp, lane = frame (shared by T and O)
+struct Group {
+    uint32_t g, b, f, gb, cex, cin, nst;
+    int ncand, reason;
+    bool inb, active;
 };
 
-#ifndef M3E_FINISH_MIN_BLOCKS
-#define M3E_FINISH_MIN_BLOCKS 6   // latency bound: 48 warps/SM (measured 4: 4.6 ms, 6: 3.9 ms, 8: 4.0 ms)
-#endif
-__global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel(const __grid_constant__ KArgs A) {
-    __shared__ FinishSmem S;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+__device__ __forceinline__ Group load_group(const KArgs& A, uint32_t g, int fb, int G, int bl, int fl) {
+    const int lane = threadIdx.x & 31;
+    Group q;
+    q.g = g;
+    q.b = g * (uint32_t)G + (uint32_t)bl;
+    q.f = q.b * (uint32_t)fb + (uint32_t)(lane - fl);
+    q.inb = bl < G && q.b < A.nbatch;
+    q.gb = kSpilled;
+    if (q.inb) q.gb = A.bsel[q.b];
+    q.active = q.inb && q.gb != kSpilled && q.f < A.F;   // spilled warp-batches: fused kernel
+    q.ncand = 0;
+    q.reason = M3E_REASON_NONE;
+    q.nst = 0;
+    if (q.active) {
+        const uint32_t w = A.sel[q.f];
+        q.ncand = (int)(w & 0xFFFFu);
+        q.reason = (int)(w >> 16);
+        q.nst = q.reason == M3E_REASON_NONE ? (uint32_t)q.ncand : 0u;
+    }
+    // store entries of the frame: warp-batch base + prefix within the warp-batch
+    q.cex = warp_incl(q.nst) - q.nst;
+    q.cin = q.cex + q.nst;
+    return q;
+}
+
+// One pass over the code bytes of the group's warp-batches (coalesced, one lane
+// per candidate, candidate order): per frame lane, cnt = accepted tracks so far.
+// STAGE = false: also counts the stored tracks' charges into neg / pos.
+// STAGE = true: copies the first lim[j] accepted fit records of frame lane j to
+// stage_trk[dst[j] + rank] (warp-batches flagged in `which` only).
+template <bool STAGE>
+__device__ __forceinline__ bool code_pass(const KArgs& A, const Group& q, int fb, int G, int* cnt, int* neg, int* pos,
+                                          unsigned which) {
+    const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    const DevParams& P = A.P;
-    const size_t gwarp = (size_t)blockIdx.x * kWarps + warp;
-    VScratch& V = reinterpret_cast<VScratch*>(A.vscratch)[gwarp];
-    m3e_track* pool = A.pool_trk + gwarp * A.trk_stride;   // tracks of the frame under vertex selection
-    if (tid == 0) S.P = A.P;
-    if (lane < 12) S.acc[warp][lane] = 0u;
-    __syncthreads();
-    const m3e_outputs& O = A.out;
-    const int fb = A.fb;
-    const int G = 32 / fb;                      // warp-batches per group (fb <= kFB <= 16)
-    const int bl = lane / fb;                   // this lane's warp-batch within the group
-    const int fl = bl * fb;                     // its first lane
-    const uint32_t ngroups = (A.nbatch + G - 1) / G;
     bool overflow = false;
+    for (int qq = 0; qq < G; ++qq) {
+        const int ql = qq * fb;
+        if (STAGE && !((which >> ql) & 1u)) continue;
+        const uint32_t qb = __shfl_sync(0xffffffffu, q.gb, ql);
+        const uint32_t qn = __shfl_sync(0xffffffffu, q.cin, min(ql + fb, 32) - 1) - __shfl_sync(0xffffffffu, q.cex, ql);
+        if (qb == kSpilled || q.g * (uint32_t)G + (uint32_t)qq >= A.nbatch) continue;
+        for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            const bool valid = e < qn;
+            const uint32_t code = valid ? A.code_g[qb + e] : 0u;
+            const int j = valid ? ql + (int)(code >> 3) : 32;
+            const unsigned grp = __match_any_sync(0xffffffffu, j);
+            const unsigned ma = __ballot_sync(0xffffffffu, code & 1u);
+            const int before = valid ? cnt[j] : 0;
+            const int rank = before + __popc(ma & grp & lt_mask);
+            if constexpr (STAGE) {
+                if ((code & 1u) && rank < neg[j]) {
+                    const uint32_t dst = (uint32_t)pos[j] + (uint32_t)rank;
+                    if (dst < A.stage_trk_cap) {
+                        const uint4* s4 = reinterpret_cast<const uint4*>(A.fit_g + qb + e);
+                        uint4* d4 = reinterpret_cast<uint4*>(A.stage_trk + dst);
+                        d4[0] = s4[0];
+                        d4[1] = s4[1];
+                    } else {
+                        overflow = true;
+                    }
+                }
+                __syncwarp();
+                if (valid && lane == __ffs(grp) - 1) cnt[j] = before + __popc(ma & grp);
+            } else {
+                const bool st = (code & 1u) && rank < A.P.max_tracks;   // stored track
+                const unsigned mn = __ballot_sync(0xffffffffu, st && (code & 2u));
+                const unsigned mp = __ballot_sync(0xffffffffu, st && (code & 4u));
+                __syncwarp();
+                if (valid && lane == __ffs(grp) - 1) {
+                    cnt[j] = before + __popc(ma & grp);
+                    neg[j] += __popc(mn & grp);
+                    pos[j] += __popc(mp & grp);
+                }
+            }
+            __syncwarp();
+        }
+    }
+    return overflow;
+}
+
+#ifndef M3E_TRACKS_MIN_BLOCKS
+#define M3E_TRACKS_MIN_BLOCKS 6
+#endif
+__global__ void __launch_bounds__(kThreads, M3E_TRACKS_MIN_BLOCKS) tracks_kernel(const __grid_constant__ KArgs A) {
+    __shared__ int s_cnt[kWarps][33], s_neg[kWarps][33], s_pos[kWarps][33];   // per frame lane (+1: invalid lanes)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int fb = A.fb, G = 32 / fb, bl = lane / fb, fl = bl * fb;
+    const uint32_t ngroups = (A.nbatch + G - 1) / G;
+    int* cnt = s_cnt[warp];
+    int* neg = s_neg[warp];
+    int* pos = s_pos[warp];
     for (;;) {
         uint32_t g = 0;
         if (lane == 0) g = atomicAdd(A.ticket + 8, 1u);
         g = __shfl_sync(0xffffffffu, g, 0);
         if (g >= ngroups) break;
-        const uint32_t b = g * (uint32_t)G + (uint32_t)bl;
-        const uint32_t f = b * (uint32_t)fb + (uint32_t)(lane - fl);
-        const bool inb = bl < G && b < A.nbatch;
-        uint32_t gb = kSpilled;
-        if (inb) gb = A.bsel[b];
-        const bool active = inb && gb != kSpilled && f < A.F;   // spilled warp-batches: fused kernel
-        int ncand = 0, reason = M3E_REASON_NONE;
-        uint32_t nst = 0;
-        if (active) {
-            const uint32_t w = A.sel[f];
-            ncand = (int)(w & 0xFFFFu);
-            reason = (int)(w >> 16);
-            nst = reason == M3E_REASON_NONE ? (uint32_t)ncand : 0u;
-        }
-        // first store entry of the frame: warp-batch base + prefix within the warp-batch
-        const uint32_t cex = warp_incl(nst) - nst;
-        const uint32_t cs = gb + cex - __shfl_sync(0xffffffffu, cex, fl);
-        // T: accepted tracks of each frame and their charges (candidate order):
-        // coalesced passes over each warp-batch's code bytes, one lane per candidate
-        S.cnt[warp][lane] = 0;
-        S.neg[warp][lane] = 0;
-        S.pos[warp][lane] = 0;
+        const Group q = load_group(A, g, fb, G, bl, fl);
+        cnt[lane] = 0;
+        neg[lane] = 0;
+        pos[lane] = 0;
         __syncwarp();
-        const uint32_t cin = cex + nst;   // inclusive prefix
-        for (int q = 0; q < G; ++q) {
-            const int ql = q * fb;
-            const uint32_t qb = __shfl_sync(0xffffffffu, gb, ql);
-            const uint32_t qn = __shfl_sync(0xffffffffu, cin, min(ql + fb, 32) - 1) -
-                                __shfl_sync(0xffffffffu, cex, ql);
-            if (qb == kSpilled || g * (uint32_t)G + (uint32_t)q >= A.nbatch) continue;
-            for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
-                const uint32_t e = e0 + lane;
-                const bool valid = e < qn;
-                const uint32_t code = valid ? A.code_g[qb + e] : 0u;
-                const int j = valid ? ql + (int)(code >> 3) : 32;
-                const unsigned grp = __match_any_sync(0xffffffffu, j);
-                const unsigned ma = __ballot_sync(0xffffffffu, code & 1u);
-                const int before = valid ? S.cnt[warp][j] : 0;
-                const int rank = before + __popc(ma & grp & lt_mask);
-                const bool st = (code & 1u) && rank < P.max_tracks;   // stored track
-                const unsigned mn = __ballot_sync(0xffffffffu, st && (code & 2u));
-                const unsigned mp = __ballot_sync(0xffffffffu, st && (code & 4u));
-                __syncwarp();
-                if (valid && lane == __ffs(grp) - 1) {
-                    S.cnt[warp][j] = before + __popc(ma & grp);
-                    S.neg[warp][j] += __popc(mn & grp);
-                    S.pos[warp][j] += __popc(mp & grp);
-                }
-                __syncwarp();
-            }
-        }
-        const int cnt = S.cnt[warp][lane];
-        int nneg = S.neg[warp][lane];
-        const int npos = S.pos[warp][lane];
-        if (active && reason == M3E_REASON_NONE && cnt > P.max_tracks) {
+        code_pass<false>(A, q, fb, G, cnt, neg, pos, 0u);
+        const int c = cnt[lane];
+        int nneg = neg[lane];
+        const int npos = pos[lane];
+        int reason = q.reason;
+        if (q.active && reason == M3E_REASON_NONE && c > A.P.max_tracks) {
             reason = M3E_REASON_TRACK_OVERFLOW;
             nneg = 0;
         }
-        const int ntrk = min(cnt, P.max_tracks + 1);
-        // V: frames with e+e+e- candidates, whole warp per frame
+        const int ntrk = min(c, A.P.max_tracks + 1);
+        if (q.active) A.fw[q.f] = (uint32_t)ntrk | ((uint32_t)min(nneg, 255) << 8) | ((uint32_t)reason << 24);
+        // frames for the vertex stage (Alg. 4 needs two e+ and one e-)
+        const bool need = q.active && reason == M3E_REASON_NONE && npos >= 2 && nneg >= 1;
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (m) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(A.ticket + 9, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const uint32_t cs = q.gb + q.cex - __shfl_sync(0xffffffffu, q.cex, fl);
+            if (need) A.vlist[base + __popc(m & lt_mask)] = make_uint2(q.f, cs);
+        }
+        __syncwarp();
+    }
+}
+
+// V, three kernels over the frames the track stage listed (Alg. 4,
+// Sec. IV-C; same arithmetic and order as vertex_frame):
+//   vertex_kernel  one warp per listed frame: its first max_tracks accepted tracks
+//                  (candidate order), charge lists, phase 1 (energy window over
+//                  (e+_a < e+_b, e-) in row-major order, ballot-compacted, capped
+//                  at max_combs); the passing triples are appended to a global
+//                  triple list (one atomicAdd per frame);
+//   triple_kernel  phase 2, one THREAD per listed triple (dense lanes across
+//                  frames: a frame has ~2 triples, so a lane per triple inside one
+//                  frame's warp leaves most lanes idle);
+//   vpost_kernel   one thread per listed frame: the passing triple with the
+//                  smallest chi2 (earliest on ties) is the frame's vertex.
+// A frame whose triples do not fit the list runs vertex_frame in place.
+struct VRes {
+    double x, y, z, chi2, tdist, ptot;
+    int pass, pad;
+};
+
+struct VertexSmem {
+    DevParams P;                          // for the out-of-line routines
+    uint32_t ent[kWarps][2][kMaxTracksCap];   // charge lists: store offset | track index << 16
+    double en[kWarps][2][kMaxTracksCap];      // their energies
+    uint2 cmb[kWarps][kMaxCombsCap];          // passing triples: {offsets a | b << 10 | e << 20, a | b << 8 | e << 16}
+};
+
+__global__ void __launch_bounds__(kThreads, 4) vertex_kernel(const __grid_constant__ KArgs A) {
+    extern __shared__ __align__(16) uint8_t vsm_raw[];
+    VertexSmem& S = *reinterpret_cast<VertexSmem*>(vsm_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    if (tid == 0) S.P = A.P;
+    __syncthreads();
+    const DevParams& P = A.P;
+    const size_t gwarp = (size_t)blockIdx.x * kWarps + warp;
+    const uint32_t n = *reinterpret_cast<const volatile uint32_t*>(A.ticket + 9);
+    uint32_t* ep = S.ent[warp][0];
+    uint32_t* en_ = S.ent[warp][1];
+    double* Ep = S.en[warp][0];
+    double* En = S.en[warp][1];
+    uint2* cmb = S.cmb[warp];
+    for (uint32_t k = (uint32_t)gwarp; k < n; k += gridDim.x * kWarps) {
+        const uint2 e = A.vlist[k];
+        const uint32_t f = e.x, cs = e.y;
+        const uint32_t nj = A.sel[f] & 0xFFFFu;
+        // accepted tracks (track index = rank among the frame's accepted entries,
+        // the first max_tracks only) split by charge, in track order
+        int nt = 0, npos = 0, nneg = 0;
+        for (uint32_t k0 = 0; k0 < nj && nt < P.max_tracks; k0 += 32) {
+            const uint32_t c = k0 + lane;
+            float kap = 0.0f;
+            bool acc = false;
+            if (c < nj) {
+                const m3e_track* t = A.fit_g + cs + c;
+                acc = t->frame != kSpilled;
+                kap = t->kappa;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, acc);
+            const int ti = nt + __popc(m & lt_mask);
+            acc = acc && ti < P.max_tracks;
+            const bool ispos = acc && kap > 0.0f, isneg = acc && kap < 0.0f;
+            const unsigned mp = __ballot_sync(0xffffffffu, ispos);
+            const unsigned mn = __ballot_sync(0xffffffffu, isneg);
+            const uint32_t code = c | ((uint32_t)ti << 16);
+            if (ispos) {
+                const int p = npos + __popc(mp & lt_mask);
+                ep[p] = code;
+                Ep[p] = track_energy(P, kap);
+            }
+            if (isneg) {
+                const int p = nneg + __popc(mn & lt_mask);
+                en_[p] = code;
+                En[p] = track_energy(P, kap);
+            }
+            nt += __popc(m);
+            npos += __popc(mp);
+            nneg += __popc(mn);
+        }
+        __syncwarp();
+        // Alg. 4 phase 1 (the track stage listed the frame: npos >= 2, nneg >= 1)
+        const int tot = npos * npos * nneg;
         int ncomb = 0;
-        const bool need = active && reason == M3E_REASON_NONE && npos >= 2 && nneg >= 1;
-        for (unsigned todo = __ballot_sync(0xffffffffu, need); todo; todo &= todo - 1) {
-            const int j = __ffs(todo) - 1;
-            const uint32_t csj = __shfl_sync(0xffffffffu, cs, j), nj = __shfl_sync(0xffffffffu, nst, j);
-            const uint32_t fj = __shfl_sync(0xffffffffu, f, j);
-            int n = 0;
-            for (uint32_t k0 = 0; k0 < nj; k0 += 32) {
-                const uint32_t k = k0 + lane;
-                const bool acc = k < nj && A.fit_g[csj + k].frame != kSpilled;
-                const unsigned m = __ballot_sync(0xffffffffu, acc);
-                const int pos = n + __popc(m & lt_mask);
-                if (acc && pos < P.max_tracks) {
-                    m3e_track t = A.fit_g[csj + k];
-                    pool[pos] = t;
+        for (int base = 0; base < tot; base += 32) {
+            const int t = base + lane;
+            bool pass = false;
+            uint2 cc = make_uint2(0u, 0u);
+            if (t < tot) {
+                const int ia = t / (npos * nneg), rem = t - ia * npos * nneg;
+                const int ib = rem / nneg, ie = rem - ib * nneg;
+                if (ia < ib) {
+                    const double dE = Ep[ia] + Ep[ib] + En[ie] - kMuMass;
+                    pass = fabs(dE) <= P.e_window;
+                    const uint32_t a = ep[ia], bb = ep[ib], ee = en_[ie];
+                    cc = make_uint2((a & 0xFFFFu) | ((bb & 0xFFFFu) << 10) | ((ee & 0xFFFFu) << 20),
+                                    (a >> 16) | ((bb >> 16) << 8) | ((ee >> 16) << 16));
                 }
-                n += __popc(m);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            const int pos = ncomb + __popc(m & lt_mask);
+            if (pass && pos < P.max_combs) cmb[pos] = cc;
+            ncomb += __popc(m);
+            if (ncomb > P.max_combs) break;
+        }
+        __syncwarp();
+        uint32_t tb = 0;
+        bool inplace = false;
+        if (ncomb > P.max_combs) {
+            ncomb = P.max_combs + 1;
+        } else if (ncomb > 0) {
+            if (lane == 0) tb = atomicAdd(A.ticket + 11, (uint32_t)ncomb);
+            tb = __shfl_sync(0xffffffffu, tb, 0);
+            inplace = tb + (uint32_t)ncomb > A.tri_cap;
+            if (!inplace)
+                for (int c = lane; c < ncomb; c += 32) A.tri[tb + c] = make_uint4(k, cmb[c].x, cmb[c].y, 0u);
+        }
+        int reason = ncomb > P.max_combs ? M3E_REASON_COMB_OVERFLOW : M3E_REASON_NONE;
+        if (inplace) {   // triple list full: the whole vertex selection of this frame here
+            VScratch& V = reinterpret_cast<VScratch*>(A.vscratch)[gwarp];
+            m3e_track* pool = A.pool_trk + gwarp * A.trk_stride;
+            int m_ = 0;
+            for (uint32_t k0 = 0; k0 < nj; k0 += 32) {
+                const uint32_t c = k0 + lane;
+                const bool acc = c < nj && A.fit_g[cs + c].frame != kSpilled;
+                const unsigned m = __ballot_sync(0xffffffffu, acc);
+                const int p = m_ + __popc(m & lt_mask);
+                if (acc && p < P.max_tracks) pool[p] = A.fit_g[cs + c];
+                m_ += __popc(m);
             }
             __syncwarp();
             Frame Fv;
-            {
-                const uint4 o4 = *reinterpret_cast<const uint4*>(A.offsets + 4 * (size_t)fj);
-                const uint32_t o5 = A.offsets[4 * (size_t)fj + 4];
-                Fv.x = A.x + o4.x;
-                Fv.y = A.y + o4.x;
-                Fv.z = A.z + o4.x;
-                Fv.s[0] = 0;
-                Fv.s[1] = (int)(o4.y - o4.x);
-                Fv.s[2] = (int)(o4.z - o4.x);
-                Fv.s[3] = (int)(o4.w - o4.x);
-                Fv.n[0] = Fv.s[1];
-                Fv.n[1] = (int)(o4.z - o4.y);
-                Fv.n[2] = (int)(o4.w - o4.z);
-                Fv.n[3] = (int)(o5 - o4.w);
-            }
-            const VOut r = vertex_frame(&S.P, V, min(n, P.max_tracks), pool, Fv, fj, &V.vtx[j]);
-            if (lane == j) {
-                ncomb = r.ncomb;
-                nneg = r.nneg;
-                if (r.ncomb > P.max_combs) reason = M3E_REASON_COMB_OVERFLOW;
-                else if (r.vtx) reason = M3E_REASON_VERTEX;
-            }
-            __syncwarp();
+            const uint4 o4 = *reinterpret_cast<const uint4*>(A.offsets + 4 * (size_t)f);
+            const uint32_t o5 = A.offsets[4 * (size_t)f + 4];
+            Fv.x = A.x + o4.x;
+            Fv.y = A.y + o4.x;
+            Fv.z = A.z + o4.x;
+            Fv.s[0] = 0;
+            Fv.s[1] = (int)(o4.y - o4.x);
+            Fv.s[2] = (int)(o4.z - o4.x);
+            Fv.s[3] = (int)(o4.w - o4.x);
+            Fv.n[0] = Fv.s[1];
+            Fv.n[1] = (int)(o4.z - o4.y);
+            Fv.n[2] = (int)(o4.w - o4.z);
+            Fv.n[3] = (int)(o5 - o4.w);
+            const VOut r = vertex_frame(&S.P, V, min(m_, P.max_tracks), pool, Fv, f, A.vrec + k);
+            reason = r.ncomb > P.max_combs ? M3E_REASON_COMB_OVERFLOW : (r.vtx ? M3E_REASON_VERTEX : M3E_REASON_NONE);
         }
-        // O: frame records in place (warp-batch relative offsets), tracks and kept
-        // frames staged, BatchStat per warp-batch for the pack kernel
-        const bool kept = active && reason != M3E_REASON_NONE;
-        const bool has_tracks = active && reason != M3E_REASON_TRIPLET_OVERFLOW && reason != M3E_REASON_INVALID;
+        if (lane == 0) {
+            A.fw[f] = (A.fw[f] & 0xFFu) | ((uint32_t)min(nneg, 255) << 8) | ((uint32_t)ncomb << 16) |
+                      ((uint32_t)reason << 24);
+            if (reason == M3E_REASON_VERTEX) A.vk[f] = k;
+            // triples for phase 2 (count 0: none; in place: already decided)
+            A.vtr[k] = make_uint2(tb, (reason == M3E_REASON_NONE && !inplace) ? (uint32_t)ncomb : 0u);
+        }
+        __syncwarp();
+    }
+}
+
+// phase 2: one thread per listed triple
+__global__ void __launch_bounds__(kThreads, 2) triple_kernel(const __grid_constant__ KArgs A) {
+    __shared__ DevParams SP;
+    if (threadIdx.x == 0) SP = A.P;
+    __syncthreads();
+    const uint32_t n0 = *reinterpret_cast<const volatile uint32_t*>(A.ticket + 11);
+    const uint32_t n = n0 < A.tri_cap ? n0 : (uint32_t)A.tri_cap;
+    for (uint32_t t = blockIdx.x * kThreads + threadIdx.x; t < n; t += gridDim.x * kThreads) {
+        const uint4 e = A.tri[t];
+        if (e.x >= *reinterpret_cast<const volatile uint32_t*>(A.ticket + 9)) continue;   // never (guard)
+        const uint2 v = A.vlist[e.x];
+        const uint32_t g0 = A.offsets[4 * (size_t)v.x];
+        Frame Fv;
+        Fv.x = A.x + g0;
+        Fv.y = A.y + g0;
+        Fv.z = A.z + g0;
+        Fv.s[0] = 0;
+        VTrk T[3];
+        T[0] = make_vtrk(SP, A.fit_g[v.y + (e.y & 1023u)], Fv);
+        T[1] = make_vtrk(SP, A.fit_g[v.y + ((e.y >> 10) & 1023u)], Fv);
+        T[2] = make_vtrk(SP, A.fit_g[v.y + ((e.y >> 20) & 1023u)], Fv);
+        const VResult r = vertex_triple(&SP, T);
+        VRes o;
+        o.x = r.x; o.y = r.y; o.z = r.z;
+        o.chi2 = r.chi2;
+        o.tdist = r.tdist;
+        o.ptot = r.ptot;
+        o.pass = r.pass;
+        o.pad = 0;
+        A.tres[t] = o;
+    }
+}
+
+// phase 3: one thread per listed frame
+__global__ void __launch_bounds__(kThreads) vpost_kernel(const __grid_constant__ KArgs A) {
+    const uint32_t n = *reinterpret_cast<const volatile uint32_t*>(A.ticket + 9);
+    for (uint32_t k = blockIdx.x * kThreads + threadIdx.x; k < n; k += gridDim.x * kThreads) {
+        const uint2 r = A.vtr[k];
+        if (r.y == 0u) continue;
+        double bchi = 1e300;
+        uint32_t bi = 0xFFFFFFFFu;
+        for (uint32_t t = r.x; t < r.x + r.y; ++t) {
+            const VRes& o = A.tres[t];
+            if (o.pass && o.chi2 < bchi) { bchi = o.chi2; bi = t; }
+        }
+        if (bi == 0xFFFFFFFFu) continue;
+        const uint32_t f = A.vlist[k].x;
+        const VRes o = A.tres[bi];
+        const uint32_t code = A.tri[bi].z;
+        m3e_vertex v;
+        v.frame = f;
+        v.track[0] = (uint16_t)(code & 255u);
+        v.track[1] = (uint16_t)((code >> 8) & 255u);
+        v.track[2] = (uint16_t)((code >> 16) & 255u);
+        v.pad = 0;
+        v.pad2 = 0;
+        v.x = o.x; v.y = o.y; v.z = o.z;
+        v.chi2 = o.chi2;
+        v.target_dist = (float)o.tdist;
+        v.p_total = (float)o.ptot;
+        A.vrec[k] = v;
+        A.fw[f] = (A.fw[f] & 0x00FFFFFFu) | ((uint32_t)M3E_REASON_VERTEX << 24);
+        A.vk[f] = k;
+    }
+}
+
+struct FinishSmem {
+    uint32_t acc[kWarps][12];
+    int cnt[kWarps][33], lim[kWarps][33], dst[kWarps][33];   // per frame lane (+1 for invalid lanes)
+};
+
+#ifndef M3E_FINISH_MIN_BLOCKS
+#define M3E_FINISH_MIN_BLOCKS 6
+#endif
+__global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel(const __grid_constant__ KArgs A) {
+    __shared__ FinishSmem S;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const DevParams& P = A.P;
+    if (lane < 12) S.acc[warp][lane] = 0u;
+    __syncwarp();
+    const m3e_outputs& O = A.out;
+    const int fb = A.fb, G = 32 / fb, bl = lane / fb, fl = bl * fb;
+    const uint32_t ngroups = (A.nbatch + G - 1) / G;
+    bool overflow = false;
+    for (;;) {
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(A.ticket + 10, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= ngroups) break;
+        const Group q = load_group(A, g, fb, G, bl, fl);
+        int ntrk = 0, nneg = 0, ncomb = 0, reason = q.reason;
+        if (q.active) {
+            const uint32_t w = A.fw[q.f];
+            ntrk = (int)(w & 0xFFu);
+            nneg = (int)((w >> 8) & 0xFFu);
+            ncomb = (int)((w >> 16) & 0xFFu);
+            reason = (int)(w >> 24);
+        }
+        const bool kept = q.active && reason != M3E_REASON_NONE;
+        const bool has_tracks = q.active && reason != M3E_REASON_TRIPLET_OVERFLOW && reason != M3E_REASON_INVALID;
         const uint32_t o_trk = has_tracks ? (uint32_t)min(ntrk, P.max_tracks) : 0u;
         const uint32_t o_kept = kept ? 1u : 0u;
         uint32_t o_hits = 0;
-        if (kept) o_hits = A.offsets[4 * (size_t)f + 4] - A.offsets[4 * (size_t)f];
+        if (kept) o_hits = A.offsets[4 * (size_t)q.f + 4] - A.offsets[4 * (size_t)q.f];
         const uint32_t i_trk = warp_incl(o_trk), i_kept = warp_incl(o_kept), i_hits = warp_incl(o_hits);
         const uint32_t e_trk = i_trk - o_trk, e_kept = i_kept - o_kept, e_hits = i_hits - o_hits;
         const uint32_t t_trk = __shfl_sync(0xffffffffu, i_trk, 31), t_kept = __shfl_sync(0xffffffffu, i_kept, 31);
@@ -1463,7 +1722,7 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
         // a warp-batch without track-overflow frame outputs exactly its accepted
         // store entries: the pack kernel copies them from the fit records; only
         // the others stage their (capped) tracks here
-        const unsigned m_tov = __ballot_sync(0xffffffffu, active && reason == M3E_REASON_TRACK_OVERFLOW);
+        const unsigned m_tov = __ballot_sync(0xffffffffu, q.active && reason == M3E_REASON_TRACK_OVERFLOW);
         const bool staged = ((m_tov >> fl) & ((1u << fb) - 1u)) != 0u;
         const uint32_t so_trk = staged ? o_trk : 0u;
         const uint32_t si_trk = warp_incl(so_trk), se_trk = si_trk - so_trk;
@@ -1477,27 +1736,27 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
         s_kept = __shfl_sync(0xffffffffu, s_kept, 0);
         const uint32_t b_trk = __shfl_sync(0xffffffffu, e_trk, fl), b_kept = __shfl_sync(0xffffffffu, e_kept, fl);
         const uint32_t b_hits = __shfl_sync(0xffffffffu, e_hits, fl);
-        if (active) {
-            if (O.reason) O.reason[f] = (uint8_t)reason;
+        if (q.active) {
+            if (O.reason) O.reason[q.f] = (uint8_t)reason;
             if (O.frames) {
                 m3e_frame_out fo;
-                fo.n_cand = (uint16_t)ncand;
+                fo.n_cand = (uint16_t)q.ncand;
                 fo.n_tracks = (uint16_t)ntrk;
                 fo.n_combs = (uint16_t)ncomb;
                 fo.reason = (uint8_t)reason;
-                fo.n_neg = (uint8_t)min(nneg, 255);
+                fo.n_neg = (uint8_t)nneg;
                 fo.track_first = e_trk - b_trk;
                 fo.kept_index = kept ? e_kept - b_kept : 0xFFFFFFFFu;
-                O.frames[f] = fo;
+                O.frames[q.f] = fo;
             }
             if (kept) {
                 const uint32_t k = s_kept + e_kept;
                 if (k < A.stage_kept_cap) {
                     KeptRec kr;
-                    kr.frame = f;
+                    kr.frame = q.f;
                     kr.pad = 0;
                     if (reason == M3E_REASON_VERTEX) {
-                        kr.v = V.vtx[lane];
+                        kr.v = A.vrec[A.vk[q.f]];
                     } else {
                         kr.v = m3e_vertex{};
                         kr.v.frame = 0xFFFFFFFFu;
@@ -1509,70 +1768,40 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
             }
         }
         // staged warp-batches: the first o_trk accepted tracks of each frame, in
-        // candidate order (second pass over the codes, one lane per candidate)
+        // candidate order (a pass over their code bytes)
         if (A.stage_trk && st_trk) {
             S.cnt[warp][lane] = 0;
-            S.pos[warp][lane] = (int)(s_trk + se_trk);   // staging slot of the frame's first track
-            S.neg[warp][lane] = (int)so_trk;
+            S.dst[warp][lane] = (int)(s_trk + se_trk);   // staging slot of the frame's first track
+            S.lim[warp][lane] = (int)so_trk;
             __syncwarp();
-            for (int q = 0; q < G; ++q) {
-                const int ql = q * fb;
-                if (!__shfl_sync(0xffffffffu, staged, ql)) continue;
-                const uint32_t qb = __shfl_sync(0xffffffffu, gb, ql);
-                const uint32_t qn = __shfl_sync(0xffffffffu, cin, min(ql + fb, 32) - 1) -
-                                    __shfl_sync(0xffffffffu, cex, ql);
-                if (qb == kSpilled || g * (uint32_t)G + (uint32_t)q >= A.nbatch) continue;
-                for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
-                    const uint32_t e = e0 + lane;
-                    const bool valid = e < qn;
-                    const uint32_t code = valid ? A.code_g[qb + e] : 0u;
-                    const int j = valid ? ql + (int)(code >> 3) : 32;
-                    const unsigned grp = __match_any_sync(0xffffffffu, j);
-                    const unsigned ma = __ballot_sync(0xffffffffu, code & 1u);
-                    const int before = valid ? S.cnt[warp][j] : 0;
-                    const int rank = before + __popc(ma & grp & lt_mask);
-                    if ((code & 1u) && rank < S.neg[warp][j]) {
-                        const uint32_t dst = (uint32_t)S.pos[warp][j] + (uint32_t)rank;
-                        if (dst < A.stage_trk_cap) {
-                            const uint4* s4 = reinterpret_cast<const uint4*>(A.fit_g + qb + e);
-                            uint4* d4 = reinterpret_cast<uint4*>(A.stage_trk + dst);
-                            d4[0] = s4[0];
-                            d4[1] = s4[1];
-                        } else {
-                            overflow = true;
-                        }
-                    }
-                    __syncwarp();
-                    if (valid && lane == __ffs(grp) - 1) S.cnt[warp][j] = before + __popc(ma & grp);
-                    __syncwarp();
-                }
-            }
+            const unsigned which = __ballot_sync(0xffffffffu, staged);
+            overflow |= code_pass<true>(A, q, fb, G, S.cnt[warp], S.lim[warp], S.dst[warp], which);
         }
         // BatchStat of each fitted warp-batch (written by its first lane)
         const int ll = fl + fb - 1;   // last lane of the warp-batch (frames past F are inactive: 0)
         const uint32_t l_trk = __shfl_sync(0xffffffffu, i_trk, ll & 31);
         const uint32_t l_kept = __shfl_sync(0xffffffffu, i_kept, ll & 31);
         const uint32_t l_hits = __shfl_sync(0xffffffffu, i_hits, ll & 31);
-        const uint32_t l_cand = __shfl_sync(0xffffffffu, cin, ll & 31);
-        const uint32_t b_cand = __shfl_sync(0xffffffffu, cex, fl);
+        const uint32_t l_cand = __shfl_sync(0xffffffffu, q.cin, ll & 31);
+        const uint32_t b_cand = __shfl_sync(0xffffffffu, q.cex, fl);
         const uint32_t b_strk = __shfl_sync(0xffffffffu, se_trk, fl);
-        if (inb && gb != kSpilled && lane == fl) {
+        if (q.inb && q.gb != kSpilled && lane == fl) {
             BatchStat bs;
             bs.n_trk = l_trk - b_trk;
             bs.n_kept = l_kept - b_kept;
             bs.n_hits = l_hits - b_hits;
             bs.s_trk = staged ? s_trk + b_strk : kSpilled;   // kSpilled: tracks = accepted store entries
             bs.s_kept = s_kept + b_kept;
-            bs.nf = min(A.F - b * (uint32_t)fb, (uint32_t)fb);
-            bs.c_base = gb;
+            bs.nf = min(A.F - q.b * (uint32_t)fb, (uint32_t)fb);
+            bs.c_base = q.gb;
             bs.c_n = l_cand - b_cand;
-            A.bstat[b] = bs;
+            A.bstat[q.b] = bs;
         }
         // run summary (per-warp counters in shared memory)
         uint32_t kr[6];
 #pragma unroll
-        for (int r = 0; r < 6; ++r) kr[r] = __popc(__ballot_sync(0xffffffffu, active && reason == r));
-        const uint32_t c_cand = warp_sum(nst), c_frames = __popc(__ballot_sync(0xffffffffu, active));
+        for (int r = 0; r < 6; ++r) kr[r] = __popc(__ballot_sync(0xffffffffu, q.active && reason == r));
+        const uint32_t c_cand = warp_sum(q.nst), c_frames = __popc(__ballot_sync(0xffffffffu, q.active));
         if (lane == 0) {
             for (int r = 0; r < 6; ++r) S.acc[warp][r] += kr[r];
             S.acc[warp][6] += c_cand;
@@ -1590,6 +1819,38 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
 cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s) {
     finish_kernel<<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_tracks(const KArgs& a, int grid, cudaStream_t s) {
+    tracks_kernel<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+int tracks_blocks_per_sm() {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tracks_kernel, kThreads, 0) != cudaSuccess) return 1;
+    return n > 0 ? n : 1;
+}
+
+cudaError_t launch_vertex(const KArgs& a, int grid, int sms, cudaStream_t s) {
+    const size_t smem = sizeof(VertexSmem);
+    cudaError_t e = cudaFuncSetAttribute(vertex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    vertex_kernel<<<grid, kThreads, smem, s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    triple_kernel<<<sms * 4, kThreads, 0, s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    vpost_kernel<<<sms * 2, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+int vertex_blocks_per_sm() {
+    int n = 0;
+    const size_t smem = sizeof(VertexSmem);
+    if (cudaFuncSetAttribute(vertex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vertex_kernel, kThreads, smem) != cudaSuccess) return 1;
+    return n > 0 ? n : 1;
 }
 
 int finish_blocks_per_sm() {
@@ -1665,3 +1926,4 @@ int blocks_per_sm(int mode, bool big) {
 }  // namespace m3e
 
 static_assert(sizeof(m3e::VScratch) <= m3e::kVScratchBytes, "kVScratchBytes too small");
+static_assert(sizeof(m3e::VRes) == m3e::kVResBytes, "kVResBytes");

@@ -18,6 +18,7 @@ constexpr int kMaxTracksCap = 128;   // upper bound accepted for params.max_trac
 constexpr int kMaxCombsCap = 128;    // upper bound accepted for params.max_combs + 1
 constexpr int kMaxCutsCap = 1023;    // upper bound accepted for params.cuts_max
 constexpr size_t kVScratchBytes = 4096;   // >= sizeof(VScratch), checked in m3e_kernels.cu
+constexpr size_t kVResBytes = 56;         // sizeof(VRes) (phase-2 vertex result), checked in m3e_kernels.cu
 
 // kModeSelectC: the Selection Cuts alone, candidates written compactly to the
 // candidate store (first kernel of the split production path: select -> fit ->
@@ -63,7 +64,8 @@ struct KArgs {
     uint32_t* ticket;      // counters (zeroed before the launch): [0] select warp-batch ticket, [1] staged
                            // tracks, [2] staged kept frames, [3] pack-kernel tile ticket, [4] filter
                            // warp-batch ticket, [5] spilled warp-batches, [6..7] candidate-store fill (u64),
-                           // [8] finish-kernel group ticket
+                           // [8] tracks-kernel group ticket, [9] vertex-list fill, [10] finish-kernel
+                           // group ticket, [11] triple-list fill
     uint32_t* bticket;     // this launch's warp-batch ticket (ticket + 0 or ticket + 4)
     // candidate store of the split path (kModeSelectC writes, fit_kernel / finish_kernel read)
     uint32_t* spill_out;   // kModeSelectC: appends the warp-batches that did not fit (count in ticket[5])
@@ -75,6 +77,16 @@ struct KArgs {
                            // kappa < 0 (2) | kappa > 0 (4)
     uint64_t cand_cap;     // entries of cand_g (< 2^32)
     uint32_t* sel;         // [F] per frame: n_cand | reason << 16
+    uint32_t* fw;          // [F] per frame after the track stage: n_tracks | n_neg << 8 | n_combs << 16 |
+                           // reason << 24 (tracks_kernel writes, vertex_kernel updates, finish_kernel reads)
+    uint32_t* vk;          // [F] vertex_kernel: list position of a frame's vertex (reason VERTEX only)
+    uint2* vlist;          // frames for the vertex stage {frame, first store entry}, count in ticket[9]
+    m3e_vertex* vrec;      // vertex of vlist entry k
+    uint2* vtr;            // [vlist] its triples {first, count} in tri (count 0: decided without phase 2)
+    uint4* tri;            // listed e+e+e- triples {vlist entry, store offsets a | b << 10 | e << 20,
+                           // track indices a | b << 8 | e << 16, 0}, count in ticket[11]
+    struct VRes* tres;     // phase-2 result of each listed triple
+    uint64_t tri_cap;      // entries of tri / tres
     uint32_t* bsel;        // [nbatch] first store entry of the warp-batch, or kSpilled
     uint4* status;         // pack-kernel decoupled look-back, one 16 B word per tile
     uint32_t epoch;        // launch epoch tag of the status words (never 0)
@@ -112,6 +124,10 @@ cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s);
 int fit_blocks_per_sm();
 cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s);
 int finish_blocks_per_sm();
+cudaError_t launch_tracks(const KArgs& a, int grid, cudaStream_t s);
+int tracks_blocks_per_sm();
+cudaError_t launch_vertex(const KArgs& a, int grid, int sms, cudaStream_t s);
+int vertex_blocks_per_sm();
 int blocks_per_sm(int mode, bool big);
 
 }  // namespace m3e

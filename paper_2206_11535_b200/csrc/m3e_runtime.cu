@@ -64,6 +64,14 @@ struct Workspace {
     uint8_t* code_g = nullptr;          // their code bytes
     size_t cand_n = 0;
     uint32_t* sel = nullptr;            // per-frame selection words of the split path
+    uint32_t* fw = nullptr;             // per-frame track/vertex words of the split path
+    uint32_t* vk = nullptr;             // per-frame vertex list position
+    uint2* vlist = nullptr;             // frames for the vertex stage
+    m3e_vertex* vrec = nullptr;         // their vertices
+    uint2* vtr = nullptr;               // their triple ranges
+    uint4* tri = nullptr;               // listed e+e+e- triples
+    void* tres = nullptr;               // their phase-2 results
+    size_t tri_n = 0;
     size_t sel_n = 0;
     uint32_t* bsel = nullptr;           // per-warp-batch store offsets of the split path
     uint32_t* spill = nullptr;          // warp-batches the store could not take
@@ -91,6 +99,8 @@ struct Chunk {
 
 }  // namespace
 
+constexpr int kNEv = 7;   // timing events per m3e_filter call (6 kernel intervals)
+
 struct m3e_context {
     int device = 0;
     int sms = 148;
@@ -102,7 +112,8 @@ struct m3e_context {
     bool timing = false;
     bool split = true;              // two-kernel production path (M3E_FUSED=1 in the environment: one kernel)
     uint64_t cand_per_frame = 16;   // candidate-store entries per frame (M3E_CAND_STORE; tests force spills)
-    std::vector<cudaEvent_t> tev;   // 5 events per timed m3e_filter call
+    uint64_t tri_cap = 0;           // vertex-stage triple list entries (M3E_TRI_CAP; 0: one per frame)
+    std::vector<cudaEvent_t> tev;   // kNEv events per timed m3e_filter call
     size_t tev_used = 0;
     size_t tev_split = 0;           // timed calls that ran the split path
 };
@@ -114,6 +125,13 @@ void free_ws(Workspace& w) {
     cudaFree(w.fit_g);
     cudaFree(w.code_g);
     cudaFree(w.sel);
+    cudaFree(w.fw);
+    cudaFree(w.vk);
+    cudaFree(w.vlist);
+    cudaFree(w.vrec);
+    cudaFree(w.vtr);
+    cudaFree(w.tri);
+    cudaFree(w.tres);
     cudaFree(w.bsel);
     cudaFree(w.spill);
     cudaFree(w.pair_scratch);
@@ -277,11 +295,30 @@ int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame) 
         w.bytes += nc * (sizeof(uint4) + sizeof(m3e_track) + 1);
     }
     if (w.sel_n < F) {
-        cudaFree(w.sel);
-        w.bytes -= w.sel_n * sizeof(uint32_t);
+        constexpr size_t per = 3 * sizeof(uint32_t) + 2 * sizeof(uint2) + sizeof(m3e_vertex);
+        cudaFree(w.sel); cudaFree(w.fw); cudaFree(w.vk); cudaFree(w.vlist); cudaFree(w.vrec); cudaFree(w.vtr);
+        w.bytes -= w.sel_n * per;
+        w.sel_n = 0;
         CK(cudaMalloc(&w.sel, F * sizeof(uint32_t)));
+        CK(cudaMalloc(&w.fw, F * sizeof(uint32_t)));
+        CK(cudaMalloc(&w.vk, F * sizeof(uint32_t)));
+        CK(cudaMalloc(&w.vlist, F * sizeof(uint2)));
+        CK(cudaMalloc(&w.vrec, F * sizeof(m3e_vertex)));
+        CK(cudaMalloc(&w.vtr, F * sizeof(uint2)));
         w.sel_n = F;
-        w.bytes += F * sizeof(uint32_t);
+        w.bytes += F * per;
+    }
+    // e+e+e- triples of the vertex stage: one per frame on average (phase I: ~0.04);
+    // frames whose triples do not fit run the vertex selection in place
+    const uint64_t nt = std::max<uint64_t>(F, 4096);
+    if (w.tri_n < nt) {
+        cudaFree(w.tri); cudaFree(w.tres);
+        w.bytes -= w.tri_n * (sizeof(uint4) + kVResBytes);
+        w.tri_n = 0;
+        CK(cudaMalloc(&w.tri, nt * sizeof(uint4)));
+        CK(cudaMalloc(&w.tres, nt * kVResBytes));
+        w.tri_n = nt;
+        w.bytes += nt * (sizeof(uint4) + kVResBytes);
     }
     if (w.bsel_n < nbatch) {
         cudaFree(w.bsel);
@@ -344,7 +381,9 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     const int sgrid = split ? (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * blocks_per_sm(kModeSelectC, false))
                             : 0;
     const int fgrid = split ? ctx->sms * finish_blocks_per_sm() : 0;
-    rc = ensure_ws(ctx, w, nbatch, p, fb, std::max(std::max(grid, sgrid), fgrid));
+    const int tgrid = split ? ctx->sms * tracks_blocks_per_sm() : 0;
+    const int vgrid = split ? ctx->sms * vertex_blocks_per_sm() : 0;   // its warps own vscratch / pool slots
+    rc = ensure_ws(ctx, w, nbatch, p, fb, std::max(std::max(grid, sgrid), vgrid));
     if (rc) return rc;
     if (split) {
         rc = ensure_split(w, F, nbatch, ctx->cand_per_frame);
@@ -377,7 +416,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     }
     CK(cudaMemsetAsync(w.ticket, 0, 16 * sizeof(uint32_t), s));
     if (a.out.summary) CK(cudaMemsetAsync(a.out.summary, 0, sizeof(m3e_summary), s));
-    const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + 5 <= ctx->tev.size();
+    const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + kNEv <= ctx->tev.size();
     cudaEvent_t* ev = tm ? &ctx->tev[ctx->tev_used] : nullptr;
     if (tm) CK(cudaEventRecord(ev[0], s));
     if (split) {
@@ -395,25 +434,36 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         a.cand_cap = sa.cand_cap;
         a.sel = w.sel;
         a.bsel = w.bsel;
+        a.fw = w.fw;
+        a.vk = w.vk;
+        a.vlist = w.vlist;
+        a.vrec = w.vrec;
+        a.vtr = w.vtr;
+        a.tri = w.tri;
+        a.tres = reinterpret_cast<VRes*>(w.tres);
+        a.tri_cap = ctx->tri_cap ? std::min<uint64_t>(ctx->tri_cap, w.tri_n) : w.tri_n;
         CK(launch_fit(a, ctx->sms * fit_blocks_per_sm(), s));
         if (tm) CK(cudaEventRecord(ev[2], s));
+        CK(launch_tracks(a, tgrid, s));
+        if (tm) CK(cudaEventRecord(ev[3], s));
+        CK(launch_vertex(a, vgrid, ctx->sms, s));
+        if (tm) CK(cudaEventRecord(ev[4], s));
         CK(launch_finish(a, fgrid, s));
         a.spill_list = w.spill;   // the fused kernel takes only the spilled warp-batches
         a.bticket = w.ticket + 4;
     } else if (tm) {
-        CK(cudaEventRecord(ev[1], s));
-        CK(cudaEventRecord(ev[2], s));
+        for (int k = 1; k <= 4; ++k) CK(cudaEventRecord(ev[k], s));
     }
     CK(launch_filter(mode, big, a, grid, s));
-    if (tm) CK(cudaEventRecord(ev[3], s));
+    if (tm) CK(cudaEventRecord(ev[5], s));
     if (packs) {
         const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
         const int pgrid = (int)std::min<uint64_t>(ntiles, (uint64_t)ctx->sms * 8);
         CK(launch_pack(a, pgrid, s));
     }
     if (tm) {
-        CK(cudaEventRecord(ev[4], s));
-        ctx->tev_used += 5;
+        CK(cudaEventRecord(ev[6], s));
+        ctx->tev_used += kNEv;
         ctx->tev_split += split ? 1 : 0;
     }
     return M3E_OK;
@@ -444,6 +494,7 @@ int m3e_create(m3e_context** out, int device, uint64_t max_frames, uint64_t max_
     c->split = !(fused && fused[0] == '1');
     if (const char* cs = std::getenv("M3E_CAND_STORE")) c->cand_per_frame = std::strtoull(cs, nullptr, 10);
     else c->cand_per_frame = kCandPerFrame;
+    if (const char* tc = std::getenv("M3E_TRI_CAP")) c->tri_cap = std::strtoull(tc, nullptr, 10);
     for (int i = 0; i < 2; ++i) {
         if (cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) != cudaSuccess) {
             delete c;
@@ -474,7 +525,7 @@ int m3e_set_timing(m3e_context* c, int enable) {
     if (!c) return fail(M3E_ERR_INVALID_ARGUMENT, "ctx is NULL");
     CK(cudaSetDevice(c->device));
     if (enable && c->tev.empty()) {
-        c->tev.resize(5 * 1024);   // up to 1024 timed calls between two m3e_kernel_times()
+        c->tev.resize(kNEv * 1024);   // up to 1024 timed calls between two m3e_kernel_times()
         for (auto& e : c->tev) CK(cudaEventCreate(&e));
     }
     c->timing = enable != 0;
@@ -483,21 +534,21 @@ int m3e_set_timing(m3e_context* c, int enable) {
     return M3E_OK;
 }
 
-int m3e_kernel_times(m3e_context* c, float ms[4]) {
+int m3e_kernel_times(m3e_context* c, float ms[6]) {
     if (!c || !ms) return fail(M3E_ERR_INVALID_ARGUMENT, "NULL argument");
     if (c->tev_used == 0) return fail(M3E_ERR_INVALID_ARGUMENT, "no timed call since the last reset");
-    double acc[4] = {0, 0, 0, 0};
-    const size_t n = c->tev_used / 5;
+    double acc[kNEv - 1] = {};
+    const size_t n = c->tev_used / kNEv;
     for (size_t i = 0; i < n; ++i) {
-        CK(cudaEventSynchronize(c->tev[5 * i + 4]));
-        for (int k = 0; k < 4; ++k) {
+        CK(cudaEventSynchronize(c->tev[kNEv * i + kNEv - 1]));
+        for (int k = 0; k < kNEv - 1; ++k) {
             float t = 0;
-            CK(cudaEventElapsedTime(&t, c->tev[5 * i + k], c->tev[5 * i + k + 1]));
+            CK(cudaEventElapsedTime(&t, c->tev[kNEv * i + k], c->tev[kNEv * i + k + 1]));
             acc[k] += t;
         }
     }
-    for (int k = 0; k < 4; ++k) ms[k] = (float)(acc[k] / n);
-    if (c->tev_split == 0) ms[0] = ms[1] = 0.0f;   // fused path: no selection / fit kernel ran
+    for (int k = 0; k < kNEv - 1; ++k) ms[k] = (float)(acc[k] / n);
+    if (c->tev_split == 0) ms[0] = ms[1] = ms[2] = ms[3] = 0.0f;   // fused path: only the filter kernel ran
     c->tev_used = 0;
     c->tev_split = 0;
     return M3E_OK;

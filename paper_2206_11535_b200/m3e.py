@@ -164,10 +164,11 @@ class Context:
         _check(lib().m3e_set_timing(self._h, int(enable)))
 
     def kernel_times(self):
-        """Mean (selection, fit, filter, pack) kernel ms over the m3e_filter calls
-        since the last reset; selection and fit are 0 on the single-kernel
-        (M3E_FUSED=1) path, where the filter kernel runs every stage."""
-        ms = (ctypes.c_float * 4)()
+        """Mean (selection, fit, tracks, vertex, finish, pack) kernel ms over the
+        m3e_filter calls since the last reset (include/m3e.h m3e_kernel_times);
+        the first four are 0 on the single-kernel (M3E_FUSED=1) path, where the
+        filter kernel ("finish") runs every stage."""
+        ms = (ctypes.c_float * 6)()
         _check(lib().m3e_kernel_times(self._h, ms))
         return tuple(float(v) for v in ms)
 

@@ -285,6 +285,30 @@ def _outputs(res, n):
             res.kept_frame.cpu().numpy()[:K].copy(), res.vertices_np(K).copy(), sm.copy())
 
 
+def test_vertex_triple_list_full(gp, monkeypatch):
+    """The split path's vertex stage lists e+e+e- triples for a dense phase-2
+    kernel; frames whose triples do not fit the list (M3E_TRI_CAP, read at
+    m3e_create) run the whole vertex selection in place.  Both must give the
+    fused kernel's outputs byte for byte."""
+    n = 3000
+    d, fr, df = _gen("signal_only", n, 711)
+    outs = []
+    for env in [{}, {"M3E_TRI_CAP": "40"}, {"M3E_FUSED": "1"}]:
+        for k in ["M3E_TRI_CAP", "M3E_FUSED"]:
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        c = m3e.Context(0)
+        res = m3e.run_filter(c, gp, df)
+        torch.cuda.synchronize()
+        outs.append(_outputs(res, n))
+        c.close()
+    assert int(np.count_nonzero(outs[0][0] == m3e.REASON_VERTEX)) > n // 10
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("store", ["0", "2"])
 def test_split_spill_and_fused_agree(gp, monkeypatch, store):
     """The production path runs the Selection Cuts in their own kernel and
