@@ -24,6 +24,10 @@
 #define M3E_HD_CALL __host__ __device__ inline
 #endif
 
+#ifndef M3E_NEWTON_IT
+#define M3E_NEWTON_IT 2   // Newton steps of arc_phi (host study: 1, 2, 3 give identical decisions and hit3)
+#endif
+
 namespace m3e {
 
 constexpr float kInfF = __builtin_huge_valf();
@@ -500,7 +504,7 @@ M3E_HD_CALL bool arc_phi(float d, float z, float k, float start, float& phi) {
     if (R2 < d2 + z2 * (1.0f / (kPiF * kPiF))) return false;
     float p = fminf(fmaxf(start, 1e-6f), kPiF);
 #pragma unroll 1
-    for (int it = 0; it < 3; ++it) {   // quadratic convergence from the linearised start
+    for (int it = 0; it < M3E_NEWTON_IT; ++it) {   // quadratic convergence from the linearised start
         float sh, ch;
         sincos_half(0.5f * p, sh, ch);
         const float is = rcp(sh), ip = rcp(p);

@@ -86,6 +86,9 @@ __device__ __forceinline__ uint4 ld_volatile_v4(const uint4* p) {
                  : "memory");
     return v;
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -1130,6 +1133,22 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const KArgs A) {
         for (int src = 0; src < 32; ++src) {
             const uint32_t bb = t * kPackTile + warp * 32 + src;
             if (bb >= A.nbatch) break;
+            {   // L2 prefetch of the warp-batch two ahead: its fit records, code bytes and
+                // frame records (the walk is a chain of dependent loads per warp-batch)
+                const int pf = src + 2;
+                const uint32_t pc_base = __shfl_sync(0xffffffffu, bs.c_base, pf & 31);
+                const uint32_t pc_n = __shfl_sync(0xffffffffu, bs.c_n, pf & 31);
+                const uint32_t ps_trk = __shfl_sync(0xffffffffu, bs.s_trk, pf & 31);
+                if (pf < 32 && bb + 2 < A.nbatch) {
+                    if (ps_trk == kSpilled && pc_n) {
+                        const char* fr = reinterpret_cast<const char*>(A.fit_g + pc_base);
+                        const uint32_t nl = (pc_n * 32u + 127u) / 128u + 1u;
+                        if ((uint32_t)lane < nl) prefetch_l2(fr + 128 * lane);
+                        if (lane == 31) prefetch_l2(A.code_g + pc_base);
+                    }
+                    if (lane == 30 && O.frames) prefetch_l2(O.frames + (size_t)(bb + 2) * A.fb);
+                }
+            }
             const uint32_t n_trk = __shfl_sync(0xffffffffu, bs.n_trk, src);
             const uint32_t n_kept = __shfl_sync(0xffffffffu, bs.n_kept, src);
             const uint32_t s_trk = __shfl_sync(0xffffffffu, bs.s_trk, src);
@@ -1263,8 +1282,13 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
     const unsigned long long filled = *reinterpret_cast<const volatile unsigned long long*>(A.ticket + 6);
     const uint64_t n = filled < A.cand_cap ? filled : A.cand_cap;
     const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-    for (uint64_t c = (uint64_t)blockIdx.x * kThreads + threadIdx.x; c < n; c += stride) {
-        const uint4 e = A.cand_g[c];
+    uint64_t c = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+    uint4 en = c < n ? A.cand_g[c] : make_uint4(0u, 0u, kSpilled, 0u);
+    for (; c < n; c += stride) {
+        // the next entry is loaded while this one is fitted (one dependent global
+        // round trip less per candidate)
+        const uint4 e = en;
+        en = c + stride < n ? A.cand_g[c + stride] : make_uint4(0u, 0u, kSpilled, 0u);
         if (e.z == kSpilled) continue;
         const uint4 o4 = *reinterpret_cast<const uint4*>(A.offsets + 4 * (size_t)e.z);
         const uint32_t o5 = A.offsets[4 * (size_t)e.z + 4];
