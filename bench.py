@@ -106,19 +106,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def load_traffic(workload: str, frames: int, seed: int, kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture of this
-    exact configuration (profiles/*_bench_traffic.json), else None."""
+def load_profile(workload: str, frames: int, seed: int):
+    """Per-kernel ncu counters (DRAM bytes, executed warp instructions per launch)
+    of the committed capture of this exact configuration
+    (profiles/*_bench_traffic.json), else {}."""
     import glob
     for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_bench_traffic.json")), reverse=True):
         try:
             t = json.load(open(fn))
         except Exception:
             continue
-        if (t.get("workload") == workload and t.get("frames") == frames and t.get("seed") == seed
-                and t.get("kernel") == kernel):
-            return t["dram_read_bytes"] + t["dram_write_bytes"]
-    return None
+        if t.get("workload") == workload and t.get("frames") == frames and t.get("seed") == seed:
+            return t.get("kernels", {})
+    return {}
 
 
 def load_peaks():
@@ -337,6 +337,23 @@ def main():
         kname, kms, alg_bytes = max(kernels, key=lambda k: k[1])
         achieved = alg_bytes / (kms / 1e3) / 1e9
         clocks = clk.summary()
+        prof = load_profile(a.workload, F, a.seed)
+        kp = prof.get(kname, {})
+        traffic = (kp["dram_read_bytes"] + kp["dram_write_bytes"]) if "dram_read_bytes" in kp else None
+        # instruction-issue roofline of the two issue-bound kernels:
+        # warp instructions per launch (ncu, committed capture of this configuration) over
+        # the live kernel time, against 148 SMs x 4 schedulers x 1 warp-instruction/cycle
+        # at the sampled SM clock
+        sm_mhz = clocks.get("sm_mhz") or 1965.0
+        issue_peak = 148 * 4 * sm_mhz * 1e6 / 1e9   # G warp-instructions/s
+        issue = {}
+        for key, kn, kt in (("select", "m3e::filter_kernel<SELECT_C, BIG=false>", ms_select),
+                            ("fit", "m3e::fit_kernel", ms_fit)):
+            ie = prof.get(kn, {}).get("inst_executed")
+            if ie and kt > 0:
+                ach = ie / (kt / 1e3) / 1e9
+                issue[key] = {"warp_inst_per_launch": int(ie), "achieved": round(ach, 1), "peak": round(issue_peak, 1),
+                              "unit": "G warp-inst/s", "frac": round(ach / issue_peak, 4)}
         line = {
             "metric": METRIC, "value": round(gbps_equiv(fps, rate), 3), "unit": "Gbps", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max, 4),
@@ -355,14 +372,14 @@ def main():
                        "parallelism": f"frame-sharded dp{world}", "generation_s": round(t_gen, 1)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
-                         "traffic": load_traffic(a.workload, F, a.seed, kname), "peak_kind": peak_kind,
+                         "traffic": traffic, "peak_kind": peak_kind, "issue": issue or None,
                          "kernel": kname, "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms_step, 4),
                          "algorithmic_bytes_per_launch": int(alg_bytes),
                          "kernels_ms": {"select": round(ms_select, 4), "fit": round(ms_fit, 4),
                                         "tracks": round(ms_tracks, 4), "vertex": round(ms_vertex, 4),
                                         "finish": round(ms_filter, 4), "pack": round(ms_pack, 4)},
                          "candidates_per_frame": round(cand / F, 3)},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (7 if split else 2) * a.steps, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (9 if split else 2) * a.steps, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -214,10 +214,13 @@ DevParams make_dev_params(const m3e_params* p) {
 }
 
 // frames per warp-batch: keep a batch's hits within the shared-memory window
+#ifndef M3E_FB_SLACK
+#define M3E_FB_SLACK 1.3   // frames per warp-batch = window / (slack x mean hits): measured 1.0 / 1.15 / 1.3 -> 12.81 / 12.58 / 12.48 ms
+#endif
 int choose_fb(uint64_t F, uint64_t H) {
     if (F == 0) return kFB;
     const double mean = (double)H / (double)F;
-    int fb = (int)((double)kHCap / (1.15 * std::max(mean, 1.0)));
+    int fb = (int)((double)kHCap / (M3E_FB_SLACK * std::max(mean, 1.0)));
     return std::max(1, std::min(kFB, fb));
 }
 
