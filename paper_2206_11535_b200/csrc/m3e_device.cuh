@@ -62,6 +62,42 @@ M3E_HD float fsqrt(float x) {
     return sqrtf(x);
 #endif
 }
+#ifndef M3E_FAST_TRIG
+#define M3E_FAST_TRIG 1   // 0: CUDA asinf / atan2f in the fit
+#endif
+// asin of 0 <= x <= 1: odd minimax polynomial on [0, 1/2] (Cephes asinf
+// coefficients, ~1 ulp), asin x = pi/2 - 2 asin(sqrt((1 - x)/2)) above; branch-free
+M3E_HD float fasin(float x) {
+#if M3E_FAST_TRIG
+    const bool big = x > 0.5f;
+    const float z = big ? 0.5f * (1.0f - x) : x * x;
+    const float t = big ? fsqrt(z) : x;
+    const float p = ((((4.2163199048e-2f * z + 2.4181311049e-2f) * z + 4.5470025998e-2f) * z + 7.4953002686e-2f) * z +
+                     1.6666752422e-1f) * z * t + t;
+    return big ? 1.57079632679f - 2.0f * p : p;
+#else
+    return asinf(x);
+#endif
+}
+// atan2: octant reduction to [0, 1], then tan(pi/8) reduction and the Cephes atanf
+// polynomial (~2 ulp); atan2(0, 0) = 0; branch-free
+M3E_HD float fatan2(float y, float x) {
+#if M3E_FAST_TRIG
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float t = mx > 0.0f ? mn * rcp(mx) : 0.0f;
+    const bool r = t > 0.41421356237f;
+    const float tt = r ? (t - 1.0f) * rcp(t + 1.0f) : t;
+    const float z = tt * tt;
+    float a = (((8.05374449538e-2f * z - 1.38776856032e-1f) * z + 1.99777106478e-1f) * z - 3.33329491539e-1f) * z * tt + tt;
+    a = r ? a + 0.78539816340f : a;
+    a = ay > ax ? 1.57079632679f - a : a;
+    a = x < 0.0f ? 3.14159265359f - a : a;
+    return copysignf(a, y);
+#else
+    return atan2f(y, x);
+#endif
+}
 // sin / cos of 0 <= x <= pi/2 by Taylor polynomials of degree 11 / 12
 // (truncation < 6e-8 absolute on the interval; no range reduction needed).
 M3E_HD void sincos_half(float x, float& s, float& c) {
@@ -449,7 +485,7 @@ M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2
         const float d = fsqrt(dx * dx + dy * dy);
         float s = d * (0.5f * ir);
         s = fminf(s, 1.0f);
-        const float phc = 2.0f * asinf(s);
+        const float phc = 2.0f * fasin(s);
         const float den = fsqrt(r * r * phc * phc + z * z);
         const float iden = rcp(den);
         const float kc = phc * iden;
@@ -473,7 +509,7 @@ M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2
     T.al_phi = 0.25f * T.q * dk * (T.dphi[0] - T.dphi[1]);
     T.b_th = dth[1] - dth[0];
     // theta_12 - theta_01 (both in (0, pi)) with one atan2
-    const float dtheta = atan2f(sthv[1] * cthv[0] - cthv[1] * sthv[0], cthv[1] * cthv[0] + sthv[1] * sthv[0]);
+    const float dtheta = fatan2(sthv[1] * cthv[0] - cthv[1] * sthv[0], cthv[1] * cthv[0] + sthv[1] * sthv[0]);
     T.al_th = dtheta - 0.5f * dk * (dth[1] + dth[0]);
     const float sig = P.chl * T.kref;
     T.w_th = rcp(sig * sig);
@@ -564,7 +600,7 @@ M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet&
     // (no crossing ahead, both at h2 itself: degenerate, as before 1e30)
     float best = 1e30f;
     if (bestp < 1e30f) {
-        best = -T.q * atan2f(bcr, bdt);
+        best = -T.q * fatan2(bcr, bdt);
         if (best < 0.0f) best += 2.0f * kPiF;
     }
     out = make_float3(bx, by, h2.z + cth * ik * best);
