@@ -289,23 +289,29 @@ __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) 
     return ex;
 }
 
-// Selection Cuts (Alg. 2, Eq. 2-5) of a whole staged warp-batch as ONE flat walk
-// (production path, SELECT_C): the (i0, i1) pairs of all frames of the
-// warp-batch are enumerated as one index space, 32 per step, frame after frame
-// and row-major inside a frame, so no lane idles at a frame boundary (phase-I
-// frames have ~40 pairs: one warp per frame leaves most lanes idle).  Factorised
-// by hit dependence as select_frame_warp: Phi_01 on pairs -> ballot pair list;
-// Delta-lambda + Phi_12 on listed pairs x layer-2 hits (again flat over the
-// pairs of up to 32 list entries) -> FIFO; r_tc window on full warps of the FIFO.
-// The element -> (frame, pair) lookup is a ballot search: the segments starting
-// inside the step's 32 elements set one bit each (redux.or), a lane's segment is
-// the popcount of the bits at or below it.  Survivors keep the order (frame, i0,
-// i1, i2) of Alg. 2, are counted per frame (match_any) and capped at cuts_max
-// (R3: n_cand = min(#survivors, cuts_max + 1); overflow frames store nothing),
-// then written to the candidate store at one atomicAdd per warp-batch.
-// Eligible warp-batches: all frames inside the staging window and every frame
-// with n0 n1 n2 <= kBigCombos (so the walk of an overflowing frame is bounded);
-// returns false, having written nothing, for the others (per-frame path).
+// Selection Cuts (Alg. 2, Eq. 2-5) of a whole staged warp-batch (production
+// path, SELECT_C), factorised by the hits each cut depends on and walked with
+// one lane per ROW of a bit matrix across all frames of the warp-batch:
+//   A. one lane per (frame, i0) row: the row's Phi_01 mask over the frame's
+//      layer-1 hits (bit i1), a loop over n1 <= 32;
+//   B. the set bits, in (frame, i0, i1) order, go to the pair list with the
+//      pair's Delta-lambda offset u(i0, i1); one lane per listed pair computes the
+//      Delta-lambda + Phi_12 mask over the frame's layer-2 hits (bit i2);
+//   C. those set bits, in (frame, i0, i1, i2) order, go to the FIFO; each full 32
+//      of it is tested for the r_t window on all lanes, and the survivors are
+//      counted per frame (match_any) and capped at cuts_max (R3).
+// Bits leave a mask in order through bounded ordered emission (warp prefix of
+// popcounts, lower lanes first), so a dense frame never overruns the lists.
+// Rows / pairs map to lanes by a ballot search over segment starts (redux.or).
+// Compared with one lane per (i0, i1) or (pair, i2) element this drops the
+// per-element index arithmetic: ~130 instead of ~300 warp instructions per
+// phase-I frame.  Survivor set and order are those of Alg. 2; n_cand =
+// min(#survivors, cuts_max + 1), overflow frames store nothing; candidates are
+// written to the store at one atomicAdd per warp-batch.
+// Eligible warp-batches: all frames inside the staging window, every frame with
+// n1, n2 <= 32 and n0 n1 n2 <= kBigCombos (so the walk of an overflowing frame is
+// bounded); returns false, having written nothing, for the others (per-frame
+// walk).
 __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, uint32_t b, uint32_t f0, int nf,
                                                   uint32_t* gl) {
     const DevParams& P = A.P;
@@ -322,23 +328,23 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
     const uint32_t wlo = W.b_winlo[0];
     const int s0 = (int)(o[0] - wlo), s1 = (int)(o[1] - wlo), s2 = (int)(o[2] - wlo);
     const int n0 = isf ? (int)(o[1] - o[0]) : 0, n1 = (int)(o[2] - o[1]), n2 = (int)(o[3] - o[2]);
-    if (__any_sync(0xffffffffu, n0 * n1 * n2 > (int)kBigCombos)) return false;
-    const int np = n2 > 0 ? n0 * n1 : 0;
-    const uint32_t pa_i = warp_incl((uint32_t)np);
-    const uint32_t NP = __shfl_sync(0xffffffffu, pa_i, 31);
-    const unsigned nem = __ballot_sync(0xffffffffu, np > 0);
+    if (__any_sync(0xffffffffu, isf && (n1 > 32 || n2 > 32 || n0 * n1 * n2 > (int)kBigCombos))) return false;
+    // rows of frames with pairs to test
+    const int nr = (n1 > 0 && n2 > 0) ? n0 : 0;
+    const uint32_t ra_i = warp_incl((uint32_t)nr);
+    const uint32_t NR = __shfl_sync(0xffffffffu, ra_i, 31);
+    const unsigned nem = __ballot_sync(0xffffffffu, nr > 0);
     const uint32_t sp = (uint32_t)s0 | ((uint32_t)s1 << 8) | ((uint32_t)s2 << 16);
-    if (np > 0)
-        S.rec[__popc(nem & lt)] = make_uint4(pa_i - (uint32_t)np, sp | ((uint32_t)lane << 24),
-                                             (uint32_t)n1 | ((uint32_t)n2 << 8), __float_as_uint(rcp((float)n1)));
+    if (nr > 0)
+        S.rec[__popc(nem & lt)] = make_uint4(ra_i - (uint32_t)nr, sp | ((uint32_t)lane << 24),
+                                             (uint32_t)n1 | ((uint32_t)n2 << 8), 0u);
     if (lane < kFB) S.cnt[lane] = 0;
     __syncwarp();
     // segment starts held by lane = rank (no bit for lanes past the last segment)
-    const uint32_t PAr = lane < __popc(nem) ? S.rec[lane].x : 0xFFFFFFFFu;
+    const uint32_t RAr = lane < __popc(nem) ? S.rec[lane].x : 0xFFFFFFFFu;
 
-    int pn = 0, qn = 0, L = 0, cbA = 0;
-    uint32_t pnext = 0;
-    // r_tc window (on squares, as pass_rtc_sq) for q[0..n); survivors counted per
+    int pn = 0, qn = 0, L = 0, cb = 0;
+    // C. r_t window (on squares, as pass_rtc_sq) for q[0..n); survivors counted per
     // frame and appended to the warp-batch list
     auto drain = [&](int n) {
         const uint32_t pk = W.q[min(lane, n - 1)];
@@ -365,73 +371,93 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
         __syncwarp();
         L += __popc(mk);
     };
-    for (;;) {
-        // 1. refill the pair list to >= 32 Phi_01 survivors (or all pairs)
-        while (pn < 32 && pnext < NP) {
-            const uint32_t bit = PAr - pnext < 32u ? 1u << (PAr - pnext) : 0u;
-            const unsigned M = __reduce_or_sync(0xffffffffu, bit);
-            const uint4 rc = S.rec[cbA + __popc(M & le) - 1];
-            cbA += __popc(M);
-            const uint32_t e = pnext + lane;
-            const int r = (int)(e - rc.x);
-            // (i0, i1) = divmod(r, n1): floor((r + 0.5) / n1), exact for r < 2^15 (see select_frame_warp)
-            const int i0 = (int)(((float)r + 0.5f) * __uint_as_float(rc.w));
-            const int i1 = r - i0 * (int)(rc.z & 255u);
-            const int g0 = (int)(rc.y & 255u) + i0, g1 = (int)((rc.y >> 8) & 255u) + i1;
-            const float x1 = hx[g1], y1 = hy[g1];
-            const bool pass = (e < NP) & ((hx[g0] * x1 + hy[g0] * y1) * P.inv_r0r1 >= P.c01_min);
-            const unsigned m = __ballot_sync(0xffffffffu, pass);
-            if (pass) {
-                // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
-                const float z1 = hz[g1];
-                const float u = z1 * P.inv_dr12 + (z1 - hz[g0]) * P.inv_dr01;
-                S.pl[pn + __popc(m & lt)] = make_uint4((uint32_t)g0 | ((uint32_t)g1 << 8) | (rc.y & 0xFFFF0000u),
-                                                       __float_as_uint(u), rc.z >> 8, 0u);
+    // B + C for the K = pn <= 32 listed pairs: one lane per pair, its mask over
+    // layer 2, ordered emission into the FIFO, full 32s drained
+    auto expand = [&]() {
+        const int K = pn;
+        uint4 pe = make_uint4(0u, 0u, 0u, 0u);
+        uint32_t rem = 0;
+        if (lane < K) {
+            pe = S.pl[lane];
+            const int g1 = (int)((pe.x >> 8) & 255u), t2 = (int)((pe.x >> 16) & 255u), m2 = (int)pe.z;
+            const float x1 = hx[g1], y1 = hy[g1];   // same expressions as select_frame_warp
+            const float u = __uint_as_float(pe.y);
+            for (int k = 0; k < m2; ++k) {
+                const float dl = fmaf(hz[t2 + k], P.inv_dr12, -u);
+                const float c12 = (x1 * hx[t2 + k] + y1 * hy[t2 + k]) * P.inv_r1r2;
+                rem |= ((fabsf(dl) <= P.dl_max) & (c12 >= P.c12_min) ? 1u : 0u) << k;
             }
-            pn += __popc(m);
-            pnext += 32;
         }
-        if (pn == 0) break;
         __syncwarp();
-        // 2. the first K listed pairs x their frame's layer-2 hits, flat
-        const int K = min(pn, 32);
-        const uint32_t w = lane < K ? S.pl[lane].z : 0u;
-        const uint32_t pb_i = warp_incl(w), PB = pb_i - w;
-        const int WT = (int)__shfl_sync(0xffffffffu, pb_i, 31);
-        const uint32_t PBr = lane < K ? PB : 0xFFFFFFFFu;
-        int cbB = 0;
-        for (int base = 0; base < WT; base += 32) {
-            const uint32_t bit = PBr - (uint32_t)base < 32u ? 1u << (PBr - (uint32_t)base) : 0u;
-            const unsigned M = __reduce_or_sync(0xffffffffu, bit);
-            const int kk = cbB + __popc(M & le) - 1;
-            cbB += __popc(M);
-            const uint4 pe = S.pl[kk];
-            const int e = base + lane;
-            const int g2 = (int)((pe.x >> 16) & 255u) + (e - (int)__shfl_sync(0xffffffffu, PB, kk));
-            const int g1 = (int)((pe.x >> 8) & 255u);
-            const float dl = fmaf(hz[g2], P.inv_dr12, -__uint_as_float(pe.y));
-            const float c12 = (hx[g1] * hx[g2] + hy[g1] * hy[g2]) * P.inv_r1r2;
-            const bool pass = (e < WT) & (fabsf(dl) <= P.dl_max) & (c12 >= P.c12_min);
-            const unsigned m = __ballot_sync(0xffffffffu, pass);
-            if (pass) W.q[qn + __popc(m & lt)] = (pe.x & 0xFF00FFFFu) | ((uint32_t)g2 << 16);
-            qn += __popc(m);
-            if (qn >= 32) {
-                __syncwarp();
+        pn = 0;
+        // FIFO entry g0 | g1 << 8 | g2 << 16 | j << 24 (the pair's s2 field replaced by g2)
+        const uint32_t ebase = pe.x & 0xFF00FFFFu, t2 = (pe.x >> 16) & 255u;
+        for (;;) {
+            const uint32_t c = __popc(rem);
+            const uint32_t inc = warp_incl(c), exc = inc - c;
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            const uint32_t fr = 64u - (uint32_t)qn;
+            const uint32_t take = exc >= fr ? 0u : min(c, fr - exc);
+            uint32_t pos = (uint32_t)qn + exc;
+            for (uint32_t t = 0; t < take; ++t) {
+                const uint32_t k = __ffs(rem) - 1;
+                W.q[pos++] = ebase | ((t2 + k) << 16);
+                rem &= rem - 1u;
+            }
+            qn += (int)min(tot, fr);
+            __syncwarp();
+            while (qn >= 32) {
                 drain(32);
                 const uint32_t v = lane < qn - 32 ? W.q[32 + lane] : 0u;
                 __syncwarp();
                 if (lane < qn - 32) W.q[lane] = v;
                 qn -= 32;
+                __syncwarp();
             }
-            __syncwarp();
+            if (tot <= fr) break;
         }
-        // drop the K expanded pairs
-        const uint4 v = lane < pn - K ? S.pl[K + lane] : make_uint4(0u, 0u, 0u, 0u);
-        __syncwarp();
-        if (lane < pn - K) S.pl[lane] = v;
-        pn -= K;
-        __syncwarp();
+    };
+    // A. rows, 32 per step
+    for (uint32_t r0 = 0; r0 < NR; r0 += 32) {
+        const uint32_t bit = RAr - r0 < 32u ? 1u << (RAr - r0) : 0u;
+        const unsigned M = __reduce_or_sync(0xffffffffu, bit);
+        const uint4 rc = S.rec[cb + __popc(M & le) - 1];
+        cb += __popc(M);
+        const uint32_t r = r0 + lane;
+        const int i0 = (int)(r - rc.x);
+        const int g0 = (int)(rc.y & 255u) + i0, t1 = (int)((rc.y >> 8) & 255u), m1 = (int)(rc.z & 255u);
+        uint32_t rem = 0;
+        float z0 = 0.0f;
+        if (r < NR) {
+            const float x0 = hx[g0], y0 = hy[g0];
+            z0 = hz[g0];
+            for (int k = 0; k < m1; ++k)
+                rem |= (((x0 * hx[t1 + k] + y0 * hy[t1 + k]) * P.inv_r0r1 >= P.c01_min) ? 1u : 0u) << k;
+        }
+        // pair entry {g0 | g1 << 8 | s2 << 16 | j << 24, u, n2, 0}
+        const uint32_t ehi = rc.y & 0xFFFF0000u, m2 = rc.z >> 8;
+        for (;;) {
+            const uint32_t c = __popc(rem);
+            const uint32_t inc = warp_incl(c), exc = inc - c;
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            const uint32_t fr = 32u - (uint32_t)pn;
+            const uint32_t take = exc >= fr ? 0u : min(c, fr - exc);
+            uint32_t pos = (uint32_t)pn + exc;
+            for (uint32_t t = 0; t < take; ++t) {
+                const int k = __ffs(rem) - 1;
+                // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
+                const float z1 = hz[t1 + k];
+                const float u = z1 * P.inv_dr12 + (z1 - z0) * P.inv_dr01;
+                S.pl[pos++] = make_uint4((uint32_t)g0 | ((uint32_t)(t1 + k) << 8) | ehi, __float_as_uint(u), m2, 0u);
+                rem &= rem - 1u;
+            }
+            pn += (int)min(tot, fr);
+            __syncwarp();
+            if (pn == 32) expand();
+            if (tot <= fr) break;
+        }
     }
+    if (pn > 0) expand();
     if (qn > 0) drain(qn);
     __syncwarp();
 
