@@ -137,10 +137,11 @@ def dist_env():
     return rank, world, local
 
 
-def generate(preset: str, n_frames: int, frame0: int, seed: int):
+def generate(preset: str, n_frames: int, frame0: int, seed: int, world: int = 1):
     cfg = synth.preset(preset, seed=seed)
     t = time.time()
-    d = synth.generate(cfg, n_frames, frame0=frame0, threads=os.cpu_count())
+    # ranks of one node generate concurrently: share the host cores
+    d = synth.generate(cfg, n_frames, frame0=frame0, threads=max(1, (os.cpu_count() or 1) // max(world, 1)))
     return d, time.time() - t
 
 
@@ -212,7 +213,7 @@ def main():
 
     # ---- this rank's second of phase-I data (distinct frame ids per rank)
     F = a.frames
-    d, t_gen = generate(a.workload, F, rank * F, a.seed)
+    d, t_gen = generate(a.workload, F, rank * F, a.seed, world)
     H = len(d["x"])
     frames = m3e.DeviceFrames(d, device=dev)
     ctx = m3e.Context(local)
