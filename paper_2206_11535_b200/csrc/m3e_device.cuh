@@ -614,12 +614,11 @@ struct FitOut {
     float kappa1, kappa2, var1, var2, kappa, chi2, cth01, cx, cy;
 };
 
-M3E_HD FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, int i2,
-                                                float rtc) {
+// h0, h1, h2 given; F supplies the frame's layer-3 hits (F.s[3], F.n[3])
+M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, float3 h1, float3 h2, float rtc) {
     FitOut o;
     o.status = 0; o.hit3 = -1;
     o.kappa1 = o.kappa2 = o.var1 = o.var2 = o.kappa = o.chi2 = o.cth01 = o.cx = o.cy = 0.0f;
-    const float3 h0 = hit(F, 0, i0), h1 = hit(F, 1, i1), h2 = hit(F, 2, i2);
     Triplet T1, T2;
     if (!fit_triplet(P, h0, h1, h2, rtc, T1)) { o.status = 1; return o; }
     o.kappa1 = T1.q * T1.khat;
@@ -663,6 +662,10 @@ M3E_HD FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, 
     o.cx = 0.5f * (h0.x + h1.x) + q * off * uy;   // clockwise: centre right of the chord
     o.cy = 0.5f * (h0.y + h1.y) - q * off * ux;
     return o;
+}
+
+M3E_HD FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, int i2, float rtc) {
+    return fit_candidate_h(P, F, hit(F, 0, i0), hit(F, 1, i1), hit(F, 2, i2), rtc);
 }
 
 // ------------------------------------------------------------- Vertex Fit ----

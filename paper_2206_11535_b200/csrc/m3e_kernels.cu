@@ -487,16 +487,16 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             const uint32_t j = pk >> 24;
             const uint4 ft = S.pl[j];
             if (ft.w) {
-                const uint32_t i0 = (pk & 255u) - (ft.z & 255u), i1 = ((pk >> 8) & 255u) - ((ft.z >> 8) & 255u),
-                               i2 = ((pk >> 16) & 255u) - ((ft.z >> 16) & 255u);
-                A.cand_g[base + ft.y + ((uint32_t)e - ft.x)] =
-                    make_uint4(i0 | (i1 << 10) | (i2 << 20), 0u, f0 + j, j);
+                // hit offsets inside the frame (window index - the frame's window start)
+                const uint32_t s0w = ft.z & 255u;
+                const uint32_t o0 = (pk & 255u) - s0w, o1 = ((pk >> 8) & 255u) - s0w, o2 = ((pk >> 16) & 255u) - s0w;
+                A.cand_g[base + ft.y + ((uint32_t)e - ft.x)] = make_uint4(wlo + s0w, f0 + j, o1 | (o2 << 16), o0);
             }
         }
     } else {
         // a warp-batch that does not fit leaves its (partial) range marked unused
         const uint32_t nw = base < A.cand_cap ? (uint32_t)(A.cand_cap - base) : 0u;
-        for (uint32_t e = lane; e < nw; e += 32) A.cand_g[base + e] = make_uint4(0u, 0u, kSpilled, 0u);
+        for (uint32_t e = lane; e < nw; e += 32) A.cand_g[base + e] = make_uint4(0u, kSpilled, 0u, 0u);
     }
     if (lane == 0) {
         A.bsel[b] = fits ? (uint32_t)base : kSpilled;
@@ -799,18 +799,15 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
             // a warp-batch that does not fit leaves its (partial) range marked unused
             const uint32_t nw = fits ? tot : (base < A.cand_cap ? (uint32_t)(A.cand_cap - base) : 0u);
             for (uint32_t e = lane; e < nw; e += 32) {
-                uint4 c = make_uint4(0u, 0u, kSpilled, 0u);
+                uint4 c = make_uint4(0u, kSpilled, 0u, 0u);
                 if (fits) {
-                    if (e < (uint32_t)kCandSmem) {
-                        c.x = W.cidx[e];
-                        c.y = __float_as_uint(W.crt[e]);
-                    } else {
-                        c.x = cidx[e];
-                        c.y = __float_as_uint(crt[e]);
-                    }
+                    const uint32_t pk = e < (uint32_t)kCandSmem ? W.cidx[e] : cidx[e];
                     const int j = find_frame(W.pref, nf, e);
-                    c.z = f0 + (uint32_t)j;
-                    c.w = (uint32_t)j;   // frame within the warp-batch
+                    const uint32_t* of = W.offs[buf] + 4 * j;
+                    c.x = of[0];                                  // frame's first hit
+                    c.y = f0 + (uint32_t)j;                       // frame
+                    c.z = ((of[1] - of[0]) + ((pk >> 10) & 1023u)) | (((of[2] - of[0]) + ((pk >> 20) & 1023u)) << 16);
+                    c.w = pk & 1023u;                             // hit offsets inside the frame
                 }
                 A.cand_g[base + e] = c;
             }
@@ -1314,14 +1311,25 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
         // the next entry is loaded while this one is fitted (one dependent global
         // round trip less per candidate)
         const uint4 e = en;
-        en = c + stride < n ? A.cand_g[c + stride] : make_uint4(0u, 0u, kSpilled, 0u);
-        if (e.z == kSpilled) continue;
-        const uint4 o4 = *reinterpret_cast<const uint4*>(A.offsets + 4 * (size_t)e.z);
-        const uint32_t o5 = A.offsets[4 * (size_t)e.z + 4];
+        en = c + stride < n ? A.cand_g[c + stride] : make_uint4(0u, kSpilled, 0u, 0u);
+        if (e.y == kSpilled) continue;
+        // the entry locates the triplet's hits directly ({first hit of the frame,
+        // frame, offsets of h1 | h2 << 16, offset of h0}): their loads do not wait
+        // for the frame's layer offsets, which only the layer-3 search needs
+        const uint32_t f = e.y;
+        const float* fx = A.x + e.x;
+        const float* fy = A.y + e.x;
+        const float* fz = A.z + e.x;
+        const uint32_t o0 = e.w, o1 = e.z & 0xFFFFu, o2 = e.z >> 16;
+        const float3 h0 = make_float3(fx[o0], fy[o0], fz[o0]);
+        const float3 h1 = make_float3(fx[o1], fy[o1], fz[o1]);
+        const float3 h2 = make_float3(fx[o2], fy[o2], fz[o2]);
+        const uint4 o4 = *reinterpret_cast<const uint4*>(A.offsets + 4 * (size_t)f);
+        const uint32_t o5 = A.offsets[4 * (size_t)f + 4];
         Frame F;
-        F.x = A.x + o4.x;
-        F.y = A.y + o4.x;
-        F.z = A.z + o4.x;
+        F.x = fx;
+        F.y = fy;
+        F.z = fz;
         F.s[0] = 0;
         F.s[1] = (int)(o4.y - o4.x);
         F.s[2] = (int)(o4.z - o4.x);
@@ -1330,16 +1338,14 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
         F.n[1] = (int)(o4.z - o4.y);
         F.n[2] = (int)(o4.w - o4.z);
         F.n[3] = (int)(o5 - o4.w);
-        const uint32_t pk = e.x;
-        const int i0 = (int)(pk & 1023u), i1 = (int)((pk >> 10) & 1023u), i2 = (int)((pk >> 20) & 1023u);
         // r_tc of the selection (Eq. 5, same fp32 code as the selection's)
-        const float rtc = circle_radius(hit(F, 0, i0), hit(F, 1, i1), hit(F, 2, i2));
-        const FitOut o = fit_candidate(A.P, F, i0, i1, i2, rtc);
+        const float rtc = circle_radius(h0, h1, h2);
+        const FitOut o = fit_candidate_h(A.P, F, h0, h1, h2, rtc);
         m3e_track t;
-        t.frame = o.status == 0 ? e.z : kSpilled;
-        t.hit[0] = (uint16_t)(pk & 1023u);
-        t.hit[1] = (uint16_t)((pk >> 10) & 1023u);
-        t.hit[2] = (uint16_t)((pk >> 20) & 1023u);
+        t.frame = o.status == 0 ? f : kSpilled;
+        t.hit[0] = (uint16_t)o0;
+        t.hit[1] = (uint16_t)(o1 - (uint32_t)F.s[1]);
+        t.hit[2] = (uint16_t)(o2 - (uint32_t)F.s[2]);
         t.hit[3] = (uint16_t)o.hit3;
         t.kappa = o.kappa;
         t.chi2 = o.chi2;
@@ -1350,7 +1356,8 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
         // code byte for the finish kernel: frame within the warp-batch << 3 |
         // accepted | kappa < 0 | kappa > 0
         const bool acc = o.status == 0;
-        A.code_g[c] = (uint8_t)((e.w << 3) | (acc ? 1u : 0u) | (acc && o.kappa < 0.0f ? 2u : 0u) |
+        const uint32_t jb = f - (f / (uint32_t)A.fb) * (uint32_t)A.fb;   // frame within its warp-batch
+        A.code_g[c] = (uint8_t)((jb << 3) | (acc ? 1u : 0u) | (acc && o.kappa < 0.0f ? 2u : 0u) |
                                 (acc && o.kappa > 0.0f ? 4u : 0u));
     }
 }

@@ -70,8 +70,9 @@ struct KArgs {
     // candidate store of the split path (kModeSelectC writes, fit_kernel / finish_kernel read)
     uint32_t* spill_out;   // kModeSelectC: appends the warp-batches that did not fit (count in ticket[5])
     uint32_t* spill_list;  // kModeFull, non-NULL: process only these warp-batches
-    uint4* cand_g;         // {packed hit indices, r_tc bits, frame, 0}, warp-batch contiguous, frame
-                           // order; frame = kSpilled marks an unused entry
+    uint4* cand_g;         // {first hit of the frame, frame, offsets of h1 | h2 << 16 and of h0 inside the
+                           // frame}, warp-batch contiguous, frame order; frame = kSpilled marks an unused
+                           // entry
     m3e_track* fit_g;      // fit of store entry c (fit_kernel); frame = kSpilled: not accepted
     uint8_t* code_g;       // code of store entry c: frame within its warp-batch << 3 | accepted |
                            // kappa < 0 (2) | kappa > 0 (4)
