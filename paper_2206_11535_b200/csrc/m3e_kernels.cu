@@ -1383,23 +1383,47 @@ struct Group {
     bool inb, active;
 };
 
-__device__ __forceinline__ Group load_group(const KArgs& A, uint32_t g, int fb, int G, int bl, int fl) {
+// raw per-lane words of a group, fetched one iteration ahead (software pipelining
+// of the lane-per-frame loops: their loads are independent of the current group)
+struct GroupRaw {
+    uint32_t gb, w, fw;
+};
+
+template <bool kFw>
+__device__ __forceinline__ GroupRaw fetch_group(const KArgs& A, uint32_t g, int fb, int G, int bl, int fl) {
+    const int lane = threadIdx.x & 31;
+    GroupRaw r;
+    r.gb = kSpilled;
+    r.w = 0u;
+    r.fw = 0u;
+    const uint32_t b = g * (uint32_t)G + (uint32_t)bl;
+    const uint32_t f = b * (uint32_t)fb + (uint32_t)(lane - fl);
+    if (bl < G && b < A.nbatch) {
+        r.gb = A.bsel[b];
+        if (f < A.F) {
+            r.w = A.sel[f];
+            if (kFw) r.fw = A.fw[f];
+        }
+    }
+    return r;
+}
+
+__device__ __forceinline__ Group make_group(const KArgs& A, uint32_t g, const GroupRaw& r, int fb, int G, int bl,
+                                            int fl) {
     const int lane = threadIdx.x & 31;
     Group q;
     q.g = g;
     q.b = g * (uint32_t)G + (uint32_t)bl;
     q.f = q.b * (uint32_t)fb + (uint32_t)(lane - fl);
     q.inb = bl < G && q.b < A.nbatch;
-    q.gb = kSpilled;
-    if (q.inb) q.gb = A.bsel[q.b];
+    q.gb = r.gb;
     q.active = q.inb && q.gb != kSpilled && q.f < A.F;   // spilled warp-batches: fused kernel
     q.ncand = 0;
     q.reason = M3E_REASON_NONE;
     q.nst = 0;
     if (q.active) {
-        const uint32_t w = A.sel[q.f];
-        q.ncand = (int)(w & 0xFFFFu);
-        q.reason = (int)(w >> 16);
+        q.ncand = (int)(r.w & 0xFFFFu);
+        q.reason = (int)(r.w >> 16);
         q.nst = q.reason == M3E_REASON_NONE ? (uint32_t)q.ncand : 0u;
     }
     // store entries of the frame: warp-batch base + prefix within the warp-batch
@@ -1477,12 +1501,13 @@ __global__ void __launch_bounds__(kThreads, M3E_TRACKS_MIN_BLOCKS) tracks_kernel
     int* cnt = s_cnt[warp];
     int* neg = s_neg[warp];
     int* pos = s_pos[warp];
-    for (;;) {
-        uint32_t g = 0;
-        if (lane == 0) g = atomicAdd(A.ticket + 8, 1u);
-        g = __shfl_sync(0xffffffffu, g, 0);
-        if (g >= ngroups) break;
-        const Group q = load_group(A, g, fb, G, bl, fl);
+    // static round-robin over groups, the next group's words fetched ahead
+    const uint32_t nw = gridDim.x * kWarps;
+    uint32_t g = blockIdx.x * kWarps + warp;
+    GroupRaw rn = fetch_group<false>(A, g, fb, G, bl, fl);
+    for (; g < ngroups; g += nw) {
+        const Group q = make_group(A, g, rn, fb, G, bl, fl);
+        rn = fetch_group<false>(A, g + nw, fb, G, bl, fl);
         cnt[lane] = 0;
         neg[lane] = 0;
         pos[lane] = 0;
@@ -1740,7 +1765,7 @@ struct FinishSmem {
 };
 
 #ifndef M3E_FINISH_MIN_BLOCKS
-#define M3E_FINISH_MIN_BLOCKS 6
+#define M3E_FINISH_MIN_BLOCKS 4   // measured 6 / 5 / 4: 0.30 / 0.27 / 0.25 ms (40 registers spill)
 #endif
 __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel(const __grid_constant__ KArgs A) {
     __shared__ FinishSmem S;
@@ -1752,15 +1777,17 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
     const int fb = A.fb, G = 32 / fb, bl = lane / fb, fl = bl * fb;
     const uint32_t ngroups = (A.nbatch + G - 1) / G;
     bool overflow = false;
-    for (;;) {
-        uint32_t g = 0;
-        if (lane == 0) g = atomicAdd(A.ticket + 10, 1u);
-        g = __shfl_sync(0xffffffffu, g, 0);
-        if (g >= ngroups) break;
-        const Group q = load_group(A, g, fb, G, bl, fl);
+    // static round-robin over groups, the next group's words fetched ahead
+    const uint32_t nw = gridDim.x * kWarps;
+    uint32_t g = blockIdx.x * kWarps + warp;
+    GroupRaw rn = fetch_group<true>(A, g, fb, G, bl, fl);
+    for (; g < ngroups; g += nw) {
+        const uint32_t fwv = rn.fw;
+        const Group q = make_group(A, g, rn, fb, G, bl, fl);
+        rn = fetch_group<true>(A, g + nw, fb, G, bl, fl);
         int ntrk = 0, nneg = 0, ncomb = 0, reason = q.reason;
         if (q.active) {
-            const uint32_t w = A.fw[q.f];
+            const uint32_t w = fwv;
             ntrk = (int)(w & 0xFFu);
             nneg = (int)((w >> 8) & 0xFFu);
             ncomb = (int)((w >> 16) & 0xFFu);
