@@ -108,6 +108,24 @@ M3E_HD void sincos_half(float x, float& s, float& c) {
                                                                               x2 * (-2.7557319e-7f + x2 * 2.0876757e-9f)))));
 }
 
+// cos of the transverse angle between two hits, Eq. 4: (xa xb + ya yb) / (ra rb),
+// with a pinned operation order (one product, one fma, one product; no
+// contraction left to the compiler), so that every walk of the Selection Cuts,
+// scalar or packed fp32 (cos_sep2), takes identical decisions
+M3E_HD float cos_sep(float xa, float ya, float xb, float yb, float inv) {
+#ifdef __CUDA_ARCH__
+    return __fmul_rn(__fmaf_rn(xa, xb, __fmul_rn(ya, yb)), inv);
+#else
+    return fmaf(xa, xb, ya * yb) * inv;
+#endif
+}
+#if !defined(__CUDA_ARCH__) || __CUDA_ARCH__ >= 1000
+// two hits b against one hit a (sm_100 FMUL2 / FFMA2; per component = cos_sep)
+__device__ __forceinline__ float2 cos_sep2(float xa, float ya, float2 xb, float2 yb, float inv) {
+    return __fmul2_rn(__ffma2_rn(make_float2(xa, xa), xb, __fmul2_rn(make_float2(ya, ya), yb)), make_float2(inv, inv));
+}
+#endif
+
 // Kernel-side parameters, derived once on the host from m3e_params.
 struct DevParams {
     float R[4];                 // layer radii
@@ -162,9 +180,9 @@ __device__ __forceinline__ bool pass_dlambda(const DevParams& P, const Frame& F,
 __device__ __forceinline__ bool pass_rest(const DevParams& P, const Frame& F, int i0, int i1, int i2, float& rt) {
     const int g0 = F.s[0] + i0, g1 = F.s[1] + i1, g2 = F.s[2] + i2;
     const float x0 = F.x[g0], y0 = F.y[g0], x1 = F.x[g1], y1 = F.y[g1];
-    if (!((x0 * x1 + y0 * y1) * P.inv_r0r1 >= P.c01_min)) return false;
+    if (!(cos_sep(x0, y0, x1, y1, P.inv_r0r1) >= P.c01_min)) return false;
     const float x2 = F.x[g2], y2 = F.y[g2];
-    if (!((x1 * x2 + y1 * y2) * P.inv_r1r2 >= P.c12_min)) return false;
+    if (!(cos_sep(x1, y1, x2, y2, P.inv_r1r2) >= P.c12_min)) return false;
     rt = circle_radius(make_float3(x0, y0, 0.0f), make_float3(x1, y1, 0.0f), make_float3(x2, y2, 0.0f));
     const float ar = fabsf(rt);
     return ar >= P.rt_min && ar <= P.rt_max;
@@ -240,7 +258,7 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
         while (pn < 32 && pnext < np) {
             // branch-free: lanes past the last pair test a clamped (valid) one
             const int g0 = F.s[0] + min(j0, n0 - 1), g1 = F.s[1] + j1;
-            const bool pass = (j0 < n0) & ((F.x[g0] * F.x[g1] + F.y[g0] * F.y[g1]) * P.inv_r0r1 >= P.c01_min);
+            const bool pass = (j0 < n0) & (cos_sep(F.x[g0], F.y[g0], F.x[g1], F.y[g1], P.inv_r0r1) >= P.c01_min);
             const unsigned m = __ballot_sync(0xffffffffu, pass);
             // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
             const float z1 = F.z[g1];
@@ -264,7 +282,7 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
             const uint32_t pk = pe.x | ((uint32_t)i2 << 20);
             const int g1 = F.s[1] + (int)(pe.x >> 10), g2 = F.s[2] + i2;
             const float dl = fmaf(F.z[g2], P.inv_dr12, -__uint_as_float(pe.y));
-            const float c12 = (F.x[g1] * F.x[g2] + F.y[g1] * F.y[g2]) * P.inv_r1r2;
+            const float c12 = cos_sep(F.x[g1], F.y[g1], F.x[g2], F.y[g2], P.inv_r1r2);
             const bool pass = (cb + lane < nk) & (fabsf(dl) <= P.dl_max) & (c12 >= P.c12_min);
             const unsigned m = __ballot_sync(0xffffffffu, pass);
             if (pass) q[qn + __popc(m & lt_mask)] = pk;
@@ -332,7 +350,7 @@ __device__ __forceinline__ int pair_list(const Frame& F, int la, int lb, float i
         float t = 0.0f;
         if (ia < na) {
             const int ga = F.s[la] + ia, gb = F.s[lb] + ib;
-            pass = (F.x[ga] * F.x[gb] + F.y[ga] * F.y[gb]) * inv_rr >= cmin;
+            pass = cos_sep(F.x[ga], F.y[ga], F.x[gb], F.y[gb], inv_rr) >= cmin;
             t = (F.z[gb] - F.z[ga]) * inv_dr;
         }
         const unsigned m = __ballot_sync(0xffffffffu, pass);

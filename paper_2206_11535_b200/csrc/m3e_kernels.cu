@@ -380,12 +380,17 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
         if (lane < K) {
             pe = S.pl[lane];
             const int g1 = (int)((pe.x >> 8) & 255u), t2 = (int)((pe.x >> 16) & 255u), m2 = (int)pe.z;
-            const float x1 = hx[g1], y1 = hy[g1];   // same expressions as select_frame_warp
+            const float x1 = hx[g1], y1 = hy[g1];
             const float u = __uint_as_float(pe.y);
-            for (int k = 0; k < m2; ++k) {
-                const float dl = fmaf(hz[t2 + k], P.inv_dr12, -u);
-                const float c12 = (x1 * hx[t2 + k] + y1 * hy[t2 + k]) * P.inv_r1r2;
-                rem |= ((fabsf(dl) <= P.dl_max) & (c12 >= P.c12_min) ? 1u : 0u) << k;
+            // two layer-2 hits per iteration in packed fp32 (same per-hit arithmetic as
+            // select_frame_warp: fmaf for Delta-lambda, cos_sep for Phi_12); k + 1 < m2 masks
+            for (int k = 0; k < m2; k += 2) {
+                const float2 zz = make_float2(hz[t2 + k], hz[t2 + k + 1]);
+                const float2 dl = __ffma2_rn(zz, make_float2(P.inv_dr12, P.inv_dr12), make_float2(-u, -u));
+                const float2 c12 = cos_sep2(x1, y1, make_float2(hx[t2 + k], hx[t2 + k + 1]),
+                                            make_float2(hy[t2 + k], hy[t2 + k + 1]), P.inv_r1r2);
+                rem |= ((fabsf(dl.x) <= P.dl_max) & (c12.x >= P.c12_min) ? 1u : 0u) << k;
+                rem |= ((k + 1 < m2) & (fabsf(dl.y) <= P.dl_max) & (c12.y >= P.c12_min) ? 1u : 0u) << (k + 1);
             }
         }
         __syncwarp();
@@ -431,8 +436,13 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
         if (r < NR) {
             const float x0 = hx[g0], y0 = hy[g0];
             z0 = hz[g0];
-            for (int k = 0; k < m1; ++k)
-                rem |= (((x0 * hx[t1 + k] + y0 * hy[t1 + k]) * P.inv_r0r1 >= P.c01_min) ? 1u : 0u) << k;
+            // two layer-1 hits per iteration in packed fp32 (cos_sep per component)
+            for (int k = 0; k < m1; k += 2) {
+                const float2 c = cos_sep2(x0, y0, make_float2(hx[t1 + k], hx[t1 + k + 1]),
+                                          make_float2(hy[t1 + k], hy[t1 + k + 1]), P.inv_r0r1);
+                rem |= (c.x >= P.c01_min ? 1u : 0u) << k;
+                rem |= ((k + 1 < m1) & (c.y >= P.c01_min) ? 1u : 0u) << (k + 1);
+            }
         }
         // pair entry {g0 | g1 << 8 | s2 << 16 | j << 24, u, n2, 0}
         const uint32_t ehi = rc.y & 0xFFFF0000u, m2 = rc.z >> 8;
