@@ -384,13 +384,17 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             const float u = __uint_as_float(pe.y);
             // two layer-2 hits per iteration in packed fp32 (same per-hit arithmetic as
             // select_frame_warp: fmaf for Delta-lambda, cos_sep for Phi_12); k + 1 < m2 masks
-            for (int k = 0; k < m2; k += 2) {
-                const float2 zz = make_float2(hz[t2 + k], hz[t2 + k + 1]);
-                const float2 dl = __ffma2_rn(zz, make_float2(P.inv_dr12, P.inv_dr12), make_float2(-u, -u));
-                const float2 c12 = cos_sep2(x1, y1, make_float2(hx[t2 + k], hx[t2 + k + 1]),
-                                            make_float2(hy[t2 + k], hy[t2 + k + 1]), P.inv_r1r2);
-                rem |= ((fabsf(dl.x) <= P.dl_max) & (c12.x >= P.c12_min) ? 1u : 0u) << k;
-                rem |= ((k + 1 < m2) & (fabsf(dl.y) <= P.dl_max) & (c12.y >= P.c12_min) ? 1u : 0u) << (k + 1);
+            for (int k0 = 0; k0 < m2; k0 += 4) {
+#pragma unroll
+                for (int h = 0; h < 4; h += 2) {
+                    const int k = k0 + h;
+                    const float2 zz = make_float2(hz[t2 + k], hz[t2 + k + 1]);
+                    const float2 dl = __ffma2_rn(zz, make_float2(P.inv_dr12, P.inv_dr12), make_float2(-u, -u));
+                    const float2 c12 = cos_sep2(x1, y1, make_float2(hx[t2 + k], hx[t2 + k + 1]),
+                                                make_float2(hy[t2 + k], hy[t2 + k + 1]), P.inv_r1r2);
+                    rem |= ((k < m2) & (fabsf(dl.x) <= P.dl_max) & (c12.x >= P.c12_min) ? 1u : 0u) << k;
+                    rem |= ((k + 1 < m2) & (fabsf(dl.y) <= P.dl_max) & (c12.y >= P.c12_min) ? 1u : 0u) << (k + 1);
+                }
             }
         }
         __syncwarp();
@@ -437,11 +441,15 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             const float x0 = hx[g0], y0 = hy[g0];
             z0 = hz[g0];
             // two layer-1 hits per iteration in packed fp32 (cos_sep per component)
-            for (int k = 0; k < m1; k += 2) {
-                const float2 c = cos_sep2(x0, y0, make_float2(hx[t1 + k], hx[t1 + k + 1]),
-                                          make_float2(hy[t1 + k], hy[t1 + k + 1]), P.inv_r0r1);
-                rem |= (c.x >= P.c01_min ? 1u : 0u) << k;
-                rem |= ((k + 1 < m1) & (c.y >= P.c01_min) ? 1u : 0u) << (k + 1);
+            for (int k0 = 0; k0 < m1; k0 += 4) {
+#pragma unroll
+                for (int h = 0; h < 4; h += 2) {
+                    const int k = k0 + h;
+                    const float2 c = cos_sep2(x0, y0, make_float2(hx[t1 + k], hx[t1 + k + 1]),
+                                              make_float2(hy[t1 + k], hy[t1 + k + 1]), P.inv_r0r1);
+                    rem |= ((k < m1) & (c.x >= P.c01_min) ? 1u : 0u) << k;
+                    rem |= ((k + 1 < m1) & (c.y >= P.c01_min) ? 1u : 0u) << (k + 1);
+                }
             }
         }
         // pair entry {g0 | g1 << 8 | s2 << 16 | j << 24, u, n2, 0}
