@@ -382,8 +382,9 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             const int g1 = (int)((pe.x >> 8) & 255u), t2 = (int)((pe.x >> 16) & 255u), m2 = (int)pe.z;
             const float x1 = hx[g1], y1 = hy[g1];
             const float u = __uint_as_float(pe.y);
-            // two layer-2 hits per iteration in packed fp32 (same per-hit arithmetic as
-            // select_frame_warp: fmaf for Delta-lambda, cos_sep for Phi_12); k + 1 < m2 masks
+            // four layer-2 hits per iteration, two per packed fp32 operation (same
+            // per-hit arithmetic as select_frame_warp: fmaf for Delta-lambda, cos_sep for
+            // Phi_12)
             for (int k0 = 0; k0 < m2; k0 += 4) {
 #pragma unroll
                 for (int h = 0; h < 4; h += 2) {
@@ -392,10 +393,16 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
                     const float2 dl = __ffma2_rn(zz, make_float2(P.inv_dr12, P.inv_dr12), make_float2(-u, -u));
                     const float2 c12 = cos_sep2(x1, y1, make_float2(hx[t2 + k], hx[t2 + k + 1]),
                                                 make_float2(hy[t2 + k], hy[t2 + k + 1]), P.inv_r1r2);
-                    rem |= ((k < m2) & (fabsf(dl.x) <= P.dl_max) & (c12.x >= P.c12_min) ? 1u : 0u) << k;
-                    rem |= ((k + 1 < m2) & (fabsf(dl.y) <= P.dl_max) & (c12.y >= P.c12_min) ? 1u : 0u) << (k + 1);
+                    // |dl| <= dl_max and c12 >= c12_min as sign bits of exact differences
+                    // (a - b is 0 only for a == b and has the sign of a - b: same decisions)
+                    const float2 a = __fadd2_rn(c12, make_float2(-P.c12_min, -P.c12_min));
+                    const float2 b = __fadd2_rn(make_float2(P.dl_max, P.dl_max), make_float2(-fabsf(dl.x), -fabsf(dl.y)));
+                    const uint32_t fail = ((__float_as_uint(a.x) | __float_as_uint(b.x)) >> 31) |
+                                          (((__float_as_uint(a.y) | __float_as_uint(b.y)) >> 30) & 2u);
+                    rem |= (fail ^ 3u) << k;
                 }
             }
+            rem &= m2 >= 32 ? 0xFFFFFFFFu : (1u << m2) - 1u;   // hits past the frame's layer 2
         }
         __syncwarp();
         pn = 0;
@@ -440,17 +447,20 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
         if (r < NR) {
             const float x0 = hx[g0], y0 = hy[g0];
             z0 = hz[g0];
-            // two layer-1 hits per iteration in packed fp32 (cos_sep per component)
+            // four layer-1 hits per iteration, two per packed fp32 operation (cos_sep)
             for (int k0 = 0; k0 < m1; k0 += 4) {
 #pragma unroll
                 for (int h = 0; h < 4; h += 2) {
                     const int k = k0 + h;
                     const float2 c = cos_sep2(x0, y0, make_float2(hx[t1 + k], hx[t1 + k + 1]),
                                               make_float2(hy[t1 + k], hy[t1 + k + 1]), P.inv_r0r1);
-                    rem |= ((k < m1) & (c.x >= P.c01_min) ? 1u : 0u) << k;
-                    rem |= ((k + 1 < m1) & (c.y >= P.c01_min) ? 1u : 0u) << (k + 1);
+                    // c >= c01_min as the sign bit of the exact difference
+                    const float2 d = __fadd2_rn(c, make_float2(-P.c01_min, -P.c01_min));
+                    const uint32_t fail = (__float_as_uint(d.x) >> 31) | ((__float_as_uint(d.y) >> 30) & 2u);
+                    rem |= (fail ^ 3u) << k;
                 }
             }
+            rem &= m1 >= 32 ? 0xFFFFFFFFu : (1u << m1) - 1u;   // hits past the frame's layer 1
         }
         // pair entry {g0 | g1 << 8 | s2 << 16 | j << 24, u, n2, 0}
         const uint32_t ehi = rc.y & 0xFFFF0000u, m2 = rc.z >> 8;
