@@ -373,8 +373,8 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
     };
     // B + C for the K = pn <= 32 listed pairs: one lane per pair, its mask over
     // layer 2, ordered emission into the FIFO, full 32s drained
-    auto expand = [&]() {
-        const int K = pn;
+    auto expand = [&]() {   // the first K = min(pn, 32) listed pairs
+        const int K = min(pn, 32);
         uint4 pe = make_uint4(0u, 0u, 0u, 0u);
         uint32_t rem = 0;
         if (lane < K) {
@@ -405,7 +405,13 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             rem &= m2 >= 32 ? 0xFFFFFFFFu : (1u << m2) - 1u;   // hits past the frame's layer 2
         }
         __syncwarp();
-        pn = 0;
+        {   // drop the K expanded pairs
+            const uint4 v = lane < pn - K ? S.pl[K + lane] : make_uint4(0u, 0u, 0u, 0u);
+            __syncwarp();
+            if (lane < pn - K) S.pl[lane] = v;
+            pn -= K;
+            __syncwarp();
+        }
         // FIFO entry g0 | g1 << 8 | g2 << 16 | j << 24 (the pair's s2 field replaced by g2)
         const uint32_t ebase = pe.x & 0xFF00FFFFu, t2 = (pe.x >> 16) & 255u;
         for (;;) {
@@ -468,7 +474,7 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             const uint32_t c = __popc(rem);
             const uint32_t inc = warp_incl(c), exc = inc - c;
             const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-            const uint32_t fr = 32u - (uint32_t)pn;
+            const uint32_t fr = 64u - (uint32_t)pn;   // pair list capacity 64, expanded 32 at a time
             const uint32_t take = exc >= fr ? 0u : min(c, fr - exc);
             uint32_t pos = (uint32_t)pn + exc;
             for (uint32_t t = 0; t < take; ++t) {
@@ -481,11 +487,11 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             }
             pn += (int)min(tot, fr);
             __syncwarp();
-            if (pn == 32) expand();
+            while (pn >= 32) expand();
             if (tot <= fr) break;
         }
     }
-    if (pn > 0) expand();
+    while (pn > 0) expand();
     if (qn > 0) drain(qn);
     __syncwarp();
 
