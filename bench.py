@@ -192,6 +192,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=15000, help="oracle sample for cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-phys", action="store_true", help="skip the truth-based efficiency sample")
+    ap.add_argument("--phys-frames", type=int, default=200000)
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3) if a.impl == "b200" else a.warmup
     rank, world, local = dist_env()
@@ -300,6 +302,21 @@ def main():
                "frames_per_s": round(world * F / t_e2e, 1)}
         hctx.close()
 
+    # ---- physics figures on a sample with truth (rank 0; outside the timed region):
+    # signal-track / signal-event efficiency of the CUDA path (synth/truth.py)
+    phys = None
+    if rank == 0 and not a.no_phys:
+        from synth.truth import signal_efficiency
+        n_e = min(F, a.phys_frames)
+        de = synth.generate(synth.preset(a.workload, seed=a.seed), n_e, frame0=0, truth=True)
+        re_ = m3e.run_filter(ctx, params, m3e.DeviceFrames(de, device=dev))
+        torch.cuda.synchronize(dev)
+        sme = re_.summary_np()
+        phys = signal_efficiency(synth.preset(a.workload, seed=a.seed), de, re_.frames_np(n_e),
+                                 re_.tracks_np(int(sme["tracks"])), params.max_tracks)
+        phys["sample_frames"] = n_e
+        del re_, de
+
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -370,7 +387,8 @@ def main():
                        "realtime_factor": round(fps / (world * PHASE1_FRAMES_PER_S), 3),
                        "muon_rate": rate,
                        "l2": "inputs (%.2f GB) >> 126 MB L2, no flush needed" % (in_bytes / 1e9),
-                       "parallelism": f"frame-sharded dp{world}", "generation_s": round(t_gen, 1)},
+                       "parallelism": f"frame-sharded dp{world}", "generation_s": round(t_gen, 1),
+                       "physics": phys},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": traffic, "peak_kind": peak_kind, "issue": issue or None,
