@@ -1527,14 +1527,10 @@ __device__ __forceinline__ bool code_pass(const KArgs& A, const Group& q, int fb
 #define M3E_TRACKS_MIN_BLOCKS 6
 #endif
 __global__ void __launch_bounds__(kThreads, M3E_TRACKS_MIN_BLOCKS) tracks_kernel(const __grid_constant__ KArgs A) {
-    __shared__ int s_cnt[kWarps][33], s_neg[kWarps][33], s_pos[kWarps][33];   // per frame lane (+1: invalid lanes)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int fb = A.fb, G = 32 / fb, bl = lane / fb, fl = bl * fb;
     const uint32_t ngroups = (A.nbatch + G - 1) / G;
-    int* cnt = s_cnt[warp];
-    int* neg = s_neg[warp];
-    int* pos = s_pos[warp];
     // static round-robin over groups, the next group's words fetched ahead
     const uint32_t nw = gridDim.x * kWarps;
     uint32_t g = blockIdx.x * kWarps + warp;
@@ -1542,14 +1538,22 @@ __global__ void __launch_bounds__(kThreads, M3E_TRACKS_MIN_BLOCKS) tracks_kernel
     for (; g < ngroups; g += nw) {
         const Group q = make_group(A, g, rn, fb, G, bl, fl);
         rn = fetch_group<false>(A, g + nw, fb, G, bl, fl);
-        cnt[lane] = 0;
-        neg[lane] = 0;
-        pos[lane] = 0;
-        __syncwarp();
-        code_pass<false>(A, q, fb, G, cnt, neg, pos, 0u);
-        const int c = cnt[lane];
-        int nneg = neg[lane];
-        const int npos = pos[lane];
+        // accepted tracks and charges of the frame from its code bytes: one lane per
+        // frame walks its own store range (candidate order; charges of the first
+        // max_tracks accepted, the stored tracks)
+        const uint32_t cs = q.gb + q.cex - __shfl_sync(0xffffffffu, q.cex, fl);
+        int c = 0, nneg = 0, npos = 0;
+        if (q.active) {
+            const uint8_t* cb = A.code_g + cs;
+            for (uint32_t k = 0; k < q.nst; ++k) {
+                const int code = cb[k];
+                const int acc = code & 1;
+                const int st = acc & (c < A.P.max_tracks ? 1 : 0);
+                nneg += st & (code >> 1);
+                npos += st & (code >> 2);
+                c += acc;
+            }
+        }
         int reason = q.reason;
         if (q.active && reason == M3E_REASON_NONE && c > A.P.max_tracks) {
             reason = M3E_REASON_TRACK_OVERFLOW;
@@ -1564,7 +1568,6 @@ __global__ void __launch_bounds__(kThreads, M3E_TRACKS_MIN_BLOCKS) tracks_kernel
             uint32_t base = 0;
             if (lane == 0) base = atomicAdd(A.ticket + 9, (uint32_t)__popc(m));
             base = __shfl_sync(0xffffffffu, base, 0);
-            const uint32_t cs = q.gb + q.cex - __shfl_sync(0xffffffffu, q.cex, fl);
             if (need) A.vlist[base + __popc(m & lt_mask)] = make_uint2(q.f, cs);
         }
         __syncwarp();
