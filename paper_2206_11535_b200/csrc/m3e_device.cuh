@@ -24,6 +24,9 @@
 #define M3E_HD_CALL __host__ __device__ inline
 #endif
 
+#ifndef M3E_NEWTON_IT_FINAL
+#define M3E_NEWTON_IT_FINAL 1   // Newton steps for the track parameters' arc (R11)
+#endif
 #ifndef M3E_NEWTON_IT
 #define M3E_NEWTON_IT 2   // Newton steps of arc_phi (host study: 1, 2, 3 give identical decisions and hit3)
 #endif
@@ -550,6 +553,7 @@ M3E_HD float triplet_chi2(const Triplet& T, float kappa) {
 // exact short-arc bending angle: root of d^2/(4 sin^2(Phi/2)) + z^2/Phi^2 = 1/k^2
 // on (0, pi] by Newton from `start` (the linearised value).  false if no short arc
 // of curvature k joins the hits (1/k^2 < d^2/4 + z^2/pi^2).
+template <int kIt = M3E_NEWTON_IT>
 M3E_HD_CALL bool arc_phi(float d, float z, float k, float start, float& phi) {
     if (!(k > 0.0f)) return false;
     const float ik = rcp(k);
@@ -558,7 +562,7 @@ M3E_HD_CALL bool arc_phi(float d, float z, float k, float start, float& phi) {
     if (R2 < d2 + z2 * (1.0f / (kPiF * kPiF))) return false;
     float p = fminf(fmaxf(start, 1e-6f), kPiF);
 #pragma unroll 1
-    for (int it = 0; it < M3E_NEWTON_IT; ++it) {   // quadratic convergence from the linearised start
+    for (int it = 0; it < kIt; ++it) {   // quadratic convergence from the linearised start
         float sh, ch;
         sincos_half(0.5f * p, sh, ch);
         const float is = rcp(sh), ip = rcp(p);
@@ -670,7 +674,12 @@ M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, flo
     const float dx = h1.x - h0.x, dy = h1.y - h0.y, z01 = h1.z - h0.z;
     const float d01 = fsqrt(dx * dx + dy * dy);
     float phi01;
-    if (!arc_phi(d01, z01, k, T1.phc[0] + T1.dphi[0] * (k - T1.kc[0]), phi01)) { o.status = 6; return o; }
+    // (one Newton step here: the result only sets the track parameters, compared at
+    // 1e-4; the extrapolation, whose result picks the layer-3 hit, takes two)
+    if (!arc_phi<M3E_NEWTON_IT_FINAL>(d01, z01, k, T1.phc[0] + T1.dphi[0] * (k - T1.kc[0]), phi01)) {
+        o.status = 6;
+        return o;
+    }
     const float cth = fminf(fmaxf(z01 * k * rcp(phi01), -1.0f), 1.0f);
     const float rt = fsqrt(1.0f - cth * cth) * rcp(k);
     const float off = fsqrt(fmaxf(0.0f, rt * rt - 0.25f * d01 * d01));
