@@ -28,7 +28,8 @@
 #define M3E_NEWTON_IT_FINAL 1   // Newton steps for the track parameters' arc (R11)
 #endif
 #ifndef M3E_NEWTON_IT
-#define M3E_NEWTON_IT 2   // Newton steps of arc_phi (host study: 1, 2, 3 give identical decisions and hit3)
+#define M3E_NEWTON_IT 1   // Newton steps of arc_phi (host study, tools/fit_numerics_study.py: 1, 2, 3 give
+                          // identical decisions, layer-3 hits and deviations on 140k candidates)
 #endif
 
 namespace m3e {
@@ -674,8 +675,6 @@ M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, flo
     const float dx = h1.x - h0.x, dy = h1.y - h0.y, z01 = h1.z - h0.z;
     const float d01 = fsqrt(dx * dx + dy * dy);
     float phi01;
-    // (one Newton step here: the result only sets the track parameters, compared at
-    // 1e-4; the extrapolation, whose result picks the layer-3 hit, takes two)
     if (!arc_phi<M3E_NEWTON_IT_FINAL>(d01, z01, k, T1.phc[0] + T1.dphi[0] * (k - T1.kc[0]), phi01)) {
         o.status = 6;
         return o;

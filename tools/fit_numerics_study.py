@@ -11,7 +11,10 @@ def build(tag, flags):
     so = f"/tmp/fitnum2_{tag}.so"
     subprocess.check_call(["nvcc", "-std=c++17", "-O2", "-Xcompiler", "-fPIC", "-shared", "-I/root/repo/include",
         "-I/root/repo/paper_2206_11535_b200/csrc", *flags, "-o", so, "/root/repo/tools/fit_numerics.cu"], stderr=subprocess.DEVNULL)
-    return ctypes.CDLL(so)
+    L = ctypes.CDLL(so)
+    vp = ctypes.c_void_p
+    L.fit_numerics.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_float, vp]
+    return L
 cfg = m3e.load_config(); P = oracle.make_params(cfg); gp = m3e.make_params(cfg)
 n = int(sys.argv[1]); preset = sys.argv[2]
 variants = [(a, a.split()) if a else ("default", []) for a in sys.argv[3:]]
@@ -27,8 +30,8 @@ for f in range(n):
         o = oracle.fit_candidate(P, fr, f, c)
         ncand += 1
         for t, L in libs:
-            L.fit_numerics(ctypes.byref(gp), fr.x.ctypes.data, fr.y.ctypes.data, fr.z.ctypes.data,
-                           ctypes.c_void_p(fr.offsets.ctypes.data + 16 * f), c.i0, c.i1, c.i2, ctypes.c_float(c.rtc), out)
+            L.fit_numerics(ctypes.addressof(gp), fr.x.ctypes.data, fr.y.ctypes.data, fr.z.ctypes.data,
+                           fr.offsets.ctypes.data + 16 * f, c.i0, c.i1, c.i2, c.rtc, ctypes.addressof(out))
             s = stats[t]
             if int(out[0]) != o.status:
                 if not (o.marginal or c.marginal): s[0] += 1
