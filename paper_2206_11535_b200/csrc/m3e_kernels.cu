@@ -1339,13 +1339,10 @@ __global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const
     const unsigned long long filled = *reinterpret_cast<const volatile unsigned long long*>(A.ticket + 6);
     const uint64_t n = filled < A.cand_cap ? filled : A.cand_cap;
     const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-    uint64_t c = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    uint4 en = c < n ? A.cand_g[c] : make_uint4(0u, 0u, kSpilled, 0u);
-    for (; c < n; c += stride) {
-        // the next entry is loaded while this one is fitted (one dependent global
-        // round trip less per candidate)
-        const uint4 e = en;
-        en = c + stride < n ? A.cand_g[c + stride] : make_uint4(0u, kSpilled, 0u, 0u);
+    // (no prefetch of the next entry: since the entries locate the hits directly, the
+    // 4 registers it held cost more in spills than the load latency it hid)
+    for (uint64_t c = (uint64_t)blockIdx.x * kThreads + threadIdx.x; c < n; c += stride) {
+        const uint4 e = A.cand_g[c];
         if (e.y == kSpilled) continue;
         // the entry locates the triplet's hits directly ({first hit of the frame,
         // frame, offsets of h1 | h2 << 16, offset of h0}): their loads do not wait
