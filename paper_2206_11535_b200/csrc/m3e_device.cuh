@@ -66,6 +66,32 @@ M3E_HD float fsqrt(float x) {
     return sqrtf(x);
 #endif
 }
+// Packed fp32 pairs: sm_100 issues FFMA2 / FMUL2 / FADD2 (two fp32 lanes per
+// instruction); the fit evaluates its two arcs side by side with them.  Per
+// component the numerics are fmaf / fmul / fadd (round to nearest).  The host
+// build (numerics studies) uses the scalar forms.
+#ifndef M3E_PACKED
+#define M3E_PACKED 1
+#endif
+M3E_HD float2 f2(float a, float b) { return make_float2(a, b); }
+M3E_HD float2 f2s(float a) { return make_float2(a, a); }
+M3E_HD float2 mul2(float2 a, float2 b) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000 && M3E_PACKED
+    return __fmul2_rn(a, b);
+#else
+    return make_float2(a.x * b.x, a.y * b.y);
+#endif
+}
+M3E_HD float2 fma2(float2 a, float2 b, float2 c) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000 && M3E_PACKED
+    return __ffma2_rn(a, b, c);
+#else
+    return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+#endif
+}
+M3E_HD float2 sqrt2(float2 a) { return make_float2(fsqrt(a.x), fsqrt(a.y)); }
+M3E_HD float2 rcp2(float2 a) { return make_float2(rcp(a.x), rcp(a.y)); }
+
 #ifndef M3E_FAST_TRIG
 #define M3E_FAST_TRIG 1   // 0: CUDA asinf / atan2f in the fit
 #endif
@@ -81,6 +107,22 @@ M3E_HD float fasin(float x) {
     return big ? 1.57079632679f - 2.0f * p : p;
 #else
     return asinf(x);
+#endif
+}
+// fasin of a pair (0 <= x <= 1), the polynomial in FFMA2
+M3E_HD float2 fasin2(float2 x) {
+#if M3E_FAST_TRIG
+    const bool bx = x.x > 0.5f, by = x.y > 0.5f;
+    const float2 z = f2(bx ? 0.5f * (1.0f - x.x) : x.x * x.x, by ? 0.5f * (1.0f - x.y) : x.y * x.y);
+    const float2 t = f2(bx ? fsqrt(z.x) : x.x, by ? fsqrt(z.y) : x.y);
+    float2 p = fma2(f2s(4.2163199048e-2f), z, f2s(2.4181311049e-2f));
+    p = fma2(p, z, f2s(4.5470025998e-2f));
+    p = fma2(p, z, f2s(7.4953002686e-2f));
+    p = fma2(p, z, f2s(1.6666752422e-1f));
+    p = fma2(mul2(p, z), t, t);
+    return f2(bx ? 1.57079632679f - 2.0f * p.x : p.x, by ? 1.57079632679f - 2.0f * p.y : p.y);
+#else
+    return make_float2(asinf(x.x), asinf(x.y));
 #endif
 }
 // atan2: octant reduction to [0, 1], then tan(pi/8) reduction and the Cephes atanf
@@ -499,40 +541,40 @@ M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2
     T.q = rtc > 0.0f ? 1 : -1;
     const float r = fabsf(rtc);
     const float ir = rcp(r);
-    float sthv[2], cthv[2], sth0 = 0.0f, dth[2];
-    const float3 H[3] = {h0, h1, h2};
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-        const float dx = H[a + 1].x - H[a].x, dy = H[a + 1].y - H[a].y, z = H[a + 1].z - H[a].z;
-        const float d = fsqrt(dx * dx + dy * dy);
-        float s = d * (0.5f * ir);
-        s = fminf(s, 1.0f);
-        const float phc = 2.0f * fasin(s);
-        const float den = fsqrt(r * r * phc * phc + z * z);
-        const float iden = rcp(den);
-        const float kc = phc * iden;
-        const float cth = z * iden, sth = r * phc * iden;
-        const float ch = fsqrt(fmaxf(0.0f, 1.0f - s * s));     // cos(Phi_C / 2)
-        // dPhi/dk = (2/k^3) / (d^2 cos(Phi/2) / (4 sin^3(Phi/2)) + 2 z^2/Phi^3), sin(Phi_C/2) = d/(2r)
-        const float iphc = rcp(phc), ikc = rcp(kc);
-        const float dphi = 2.0f * ikc * ikc * ikc * rcp(r * r * ch * rcp(s) + 2.0f * z * z * iphc * iphc * iphc);
-        // dtheta/dk = -z (Phi - k Phi') / (Phi^2 sin theta)
-        dth[a] = -z * (phc - kc * dphi) * iphc * iphc * rcp(sth);
-        sthv[a] = sth;
-        cthv[a] = cth;
-        if (a == 0) sth0 = sth;
-        T.phc[a] = phc;
-        T.kc[a] = kc;
-        T.dphi[a] = dphi;
-    }
+    // the two arcs h0 -> h1 (.x) and h1 -> h2 (.y) side by side (packed fp32)
+    const float2 dx = f2(h1.x - h0.x, h2.x - h1.x), dy = f2(h1.y - h0.y, h2.y - h1.y);
+    const float2 z = f2(h1.z - h0.z, h2.z - h1.z);
+    const float2 d = sqrt2(fma2(dx, dx, mul2(dy, dy)));
+    float2 sv = mul2(d, f2s(0.5f * ir));
+    sv = f2(fminf(sv.x, 1.0f), fminf(sv.y, 1.0f));
+    const float2 phc = mul2(f2s(2.0f), fasin2(sv));
+    const float2 rphc = mul2(f2s(r), phc);
+    const float2 z2 = mul2(z, z);
+    const float2 iden = rcp2(sqrt2(fma2(rphc, rphc, z2)));
+    const float2 kc = mul2(phc, iden);
+    const float2 cthv = mul2(z, iden), sthv = mul2(rphc, iden);
+    const float2 cs2 = fma2(make_float2(-sv.x, -sv.y), sv, f2s(1.0f));
+    const float2 ch = sqrt2(f2(fmaxf(0.0f, cs2.x), fmaxf(0.0f, cs2.y)));   // cos(Phi_C / 2)
+    // dPhi/dk = (2/k^3) / (d^2 cos(Phi/2) / (4 sin^3(Phi/2)) + 2 z^2/Phi^3), sin(Phi_C/2) = d/(2r)
+    const float2 iphc = rcp2(phc), ikc = rcp2(kc);
+    const float2 iphc2 = mul2(iphc, iphc);
+    const float2 dd = fma2(mul2(f2s(2.0f), z2), mul2(iphc2, iphc), mul2(mul2(f2s(r * r), ch), rcp2(sv)));
+    const float2 dphi = mul2(mul2(mul2(f2s(2.0f), ikc), mul2(ikc, ikc)), rcp2(dd));
+    // dtheta/dk = -z (Phi - k Phi') / (Phi^2 sin theta)
+    const float2 dth = mul2(mul2(make_float2(-z.x, -z.y), fma2(make_float2(-kc.x, -kc.y), dphi, phc)),
+                            mul2(iphc2, rcp2(sthv)));
+    const float sth0 = sthv.x;
+    T.phc[0] = phc.x; T.phc[1] = phc.y;
+    T.kc[0] = kc.x; T.kc[1] = kc.y;
+    T.dphi[0] = dphi.x; T.dphi[1] = dphi.y;
     const float dk = T.kc[1] - T.kc[0];
     T.kref = 0.5f * (T.kc[0] + T.kc[1]);
     T.b_phi = 0.5f * T.q * (T.dphi[0] + T.dphi[1]);
     T.al_phi = 0.25f * T.q * dk * (T.dphi[0] - T.dphi[1]);
-    T.b_th = dth[1] - dth[0];
+    T.b_th = dth.y - dth.x;
     // theta_12 - theta_01 (both in (0, pi)) with one atan2
-    const float dtheta = fatan2(sthv[1] * cthv[0] - cthv[1] * sthv[0], cthv[1] * cthv[0] + sthv[1] * sthv[0]);
-    T.al_th = dtheta - 0.5f * dk * (dth[1] + dth[0]);
+    const float dtheta = fatan2(sthv.y * cthv.x - cthv.y * sthv.x, cthv.y * cthv.x + sthv.y * sthv.x);
+    T.al_th = dtheta - 0.5f * dk * (dth.y + dth.x);
     const float sig = P.chl * T.kref;
     T.w_th = rcp(sig * sig);
     T.w_phi = sth0 * sth0 * T.w_th;
