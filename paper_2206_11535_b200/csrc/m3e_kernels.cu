@@ -289,6 +289,15 @@ __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) 
     return ex;
 }
 
+__device__ __forceinline__ uint32_t popc_t(uint32_t v) { return (uint32_t)__popc(v); }
+__device__ __forceinline__ uint32_t popc_t(unsigned long long v) { return (uint32_t)__popcll(v); }
+__device__ __forceinline__ int ffs_t(uint32_t v) { return __ffs(v); }
+__device__ __forceinline__ int ffs_t(unsigned long long v) { return __ffsll(v); }
+// combinations per frame up to which the flat walk takes a frame (bounds the walk
+// of an overflowing frame); 64-bit masks: phase-II frames (~56 hits per layer)
+template <typename MT>
+__device__ __forceinline__ constexpr int kMaxFlatCombos() { return sizeof(MT) == 4 ? (int)kBigCombos : 1 << 19; }
+
 // Selection Cuts (Alg. 2, Eq. 2-5) of a whole staged warp-batch (production
 // path, SELECT_C), factorised by the hits each cut depends on and walked with
 // one lane per ROW of a bit matrix across all frames of the warp-batch:
@@ -312,6 +321,7 @@ __device__ __forceinline__ uint3 resolve(const KArgs& A, uint32_t b, uint3 agg) 
 // n1, n2 <= 32 and n0 n1 n2 <= kBigCombos (so the walk of an overflowing frame is
 // bounded); returns false, having written nothing, for the others (per-frame
 // walk).
+template <typename MT>   // bit-mask type: uint32_t (layers 1, 2 up to 32 hits) or unsigned long long (64)
 __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, uint32_t b, uint32_t f0, int nf,
                                                   uint32_t* gl) {
     const DevParams& P = A.P;
@@ -328,7 +338,8 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
     const uint32_t wlo = W.b_winlo[0];
     const int s0 = (int)(o[0] - wlo), s1 = (int)(o[1] - wlo), s2 = (int)(o[2] - wlo);
     const int n0 = isf ? (int)(o[1] - o[0]) : 0, n1 = (int)(o[2] - o[1]), n2 = (int)(o[3] - o[2]);
-    if (__any_sync(0xffffffffu, isf && (n1 > 32 || n2 > 32 || n0 * n1 * n2 > (int)kBigCombos))) return false;
+    constexpr int kMB = 8 * (int)sizeof(MT);
+    if (__any_sync(0xffffffffu, isf && (n1 > kMB || n2 > kMB || n0 * n1 * n2 > kMaxFlatCombos<MT>()))) return false;
     // rows of frames with pairs to test
     const int nr = (n1 > 0 && n2 > 0) ? n0 : 0;
     const uint32_t ra_i = warp_incl((uint32_t)nr);
@@ -376,7 +387,7 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
     auto expand = [&]() {   // the first K = min(pn, 32) listed pairs
         const int K = min(pn, 32);
         uint4 pe = make_uint4(0u, 0u, 0u, 0u);
-        uint32_t rem = 0;
+        MT rem = 0;
         if (lane < K) {
             pe = S.pl[lane];
             const int g1 = (int)((pe.x >> 8) & 255u), t2 = (int)((pe.x >> 16) & 255u), m2 = (int)pe.z;
@@ -399,10 +410,10 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
                     const float2 b = __fadd2_rn(make_float2(P.dl_max, P.dl_max), make_float2(-fabsf(dl.x), -fabsf(dl.y)));
                     const uint32_t fail = ((__float_as_uint(a.x) | __float_as_uint(b.x)) >> 31) |
                                           (((__float_as_uint(a.y) | __float_as_uint(b.y)) >> 30) & 2u);
-                    rem |= (fail ^ 3u) << k;
+                    rem |= (MT)(fail ^ 3u) << k;
                 }
             }
-            rem &= m2 >= 32 ? 0xFFFFFFFFu : (1u << m2) - 1u;   // hits past the frame's layer 2
+            rem &= m2 >= kMB ? ~(MT)0 : ((MT)1 << m2) - 1;   // hits past the frame's layer 2
         }
         __syncwarp();
         {   // drop the K expanded pairs
@@ -415,16 +426,16 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
         // FIFO entry g0 | g1 << 8 | g2 << 16 | j << 24 (the pair's s2 field replaced by g2)
         const uint32_t ebase = pe.x & 0xFF00FFFFu, t2 = (pe.x >> 16) & 255u;
         for (;;) {
-            const uint32_t c = __popc(rem);
+            const uint32_t c = popc_t(rem);
             const uint32_t inc = warp_incl(c), exc = inc - c;
             const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
             const uint32_t fr = 64u - (uint32_t)qn;
             const uint32_t take = exc >= fr ? 0u : min(c, fr - exc);
             uint32_t pos = (uint32_t)qn + exc;
             for (uint32_t t = 0; t < take; ++t) {
-                const uint32_t k = __ffs(rem) - 1;
+                const uint32_t k = ffs_t(rem) - 1;
                 W.q[pos++] = ebase | ((t2 + k) << 16);
-                rem &= rem - 1u;
+                rem &= rem - (MT)1;
             }
             qn += (int)min(tot, fr);
             __syncwarp();
@@ -448,7 +459,7 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
         const uint32_t r = r0 + lane;
         const int i0 = (int)(r - rc.x);
         const int g0 = (int)(rc.y & 255u) + i0, t1 = (int)((rc.y >> 8) & 255u), m1 = (int)(rc.z & 255u);
-        uint32_t rem = 0;
+        MT rem = 0;
         float z0 = 0.0f;
         if (r < NR) {
             const float x0 = hx[g0], y0 = hy[g0];
@@ -463,27 +474,27 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
                     // c >= c01_min as the sign bit of the exact difference
                     const float2 d = __fadd2_rn(c, make_float2(-P.c01_min, -P.c01_min));
                     const uint32_t fail = (__float_as_uint(d.x) >> 31) | ((__float_as_uint(d.y) >> 30) & 2u);
-                    rem |= (fail ^ 3u) << k;
+                    rem |= (MT)(fail ^ 3u) << k;
                 }
             }
-            rem &= m1 >= 32 ? 0xFFFFFFFFu : (1u << m1) - 1u;   // hits past the frame's layer 1
+            rem &= m1 >= kMB ? ~(MT)0 : ((MT)1 << m1) - 1;   // hits past the frame's layer 1
         }
         // pair entry {g0 | g1 << 8 | s2 << 16 | j << 24, u, n2, 0}
         const uint32_t ehi = rc.y & 0xFFFF0000u, m2 = rc.z >> 8;
         for (;;) {
-            const uint32_t c = __popc(rem);
+            const uint32_t c = popc_t(rem);
             const uint32_t inc = warp_incl(c), exc = inc - c;
             const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
             const uint32_t fr = 64u - (uint32_t)pn;   // pair list capacity 64, expanded 32 at a time
             const uint32_t take = exc >= fr ? 0u : min(c, fr - exc);
             uint32_t pos = (uint32_t)pn + exc;
             for (uint32_t t = 0; t < take; ++t) {
-                const int k = __ffs(rem) - 1;
+                const int k = ffs_t(rem) - 1;
                 // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
                 const float z1 = hz[t1 + k];
                 const float u = z1 * P.inv_dr12 + (z1 - z0) * P.inv_dr01;
                 S.pl[pos++] = make_uint4((uint32_t)g0 | ((uint32_t)(t1 + k) << 8) | ehi, __float_as_uint(u), m2, 0u);
-                rem &= rem - 1u;
+                rem &= rem - (MT)1;
             }
             pn += (int)min(tot, fr);
             __syncwarp();
@@ -728,7 +739,12 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
         // production path: the whole warp-batch as one flat walk (eligible
         // warp-batches; the per-frame walk below handles the others)
         bool flat_done = false;
-        if constexpr (MODE == kModeSelectC && !M3E_NO_FLAT_SELECT) flat_done = select_batch_flat(A, W, b, f0, nf, cidx);
+        if constexpr (MODE == kModeSelectC && !M3E_NO_FLAT_SELECT) {
+            flat_done = select_batch_flat<uint32_t>(A, W, b, f0, nf, cidx);
+            if constexpr (BIG) {
+                if (!flat_done) flat_done = select_batch_flat<unsigned long long>(A, W, b, f0, nf, cidx);
+            }
+        }
         if constexpr (MODE == kModeFull || MODE == kModeSelect || MODE == kModeSelectC) {
           if (!flat_done) {
             uint32_t cbase = 0;   // flat: candidate index of frame j's first candidate
@@ -2008,7 +2024,8 @@ cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStre
         case kModeFull: return big ? launch_mode<kModeFull, true>(a, grid, s) : launch_mode<kModeFull, false>(a, grid, s);
         case kModeSelect:
             return big ? launch_mode<kModeSelect, true>(a, grid, s) : launch_mode<kModeSelect, false>(a, grid, s);
-        case kModeSelectC: return launch_mode<kModeSelectC, false>(a, grid, s);
+        case kModeSelectC:
+            return big ? launch_mode<kModeSelectC, true>(a, grid, s) : launch_mode<kModeSelectC, false>(a, grid, s);
         case kModeFit: return launch_mode<kModeFit, false>(a, grid, s);
         case kModeVertex: return launch_mode<kModeVertex, false>(a, grid, s);
         case kModePack: return launch_mode<kModePack, false>(a, grid, s);
@@ -2033,7 +2050,7 @@ int blocks_per_sm(int mode, bool big) {
     switch (mode) {
         case kModeFull: return big ? occupancy<kModeFull, true>() : occupancy<kModeFull, false>();
         case kModeSelect: return big ? occupancy<kModeSelect, true>() : occupancy<kModeSelect, false>();
-        case kModeSelectC: return occupancy<kModeSelectC, false>();
+        case kModeSelectC: return big ? occupancy<kModeSelectC, true>() : occupancy<kModeSelectC, false>();
         case kModeFit: return occupancy<kModeFit, false>();
         case kModeVertex: return occupancy<kModeVertex, false>();
         case kModePack: return occupancy<kModePack, false>();

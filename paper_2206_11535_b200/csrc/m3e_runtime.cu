@@ -283,8 +283,9 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
 // that do not fit are flagged and re-selected by the filter kernel), per-frame
 // selection words and per-warp-batch store offsets
 constexpr uint64_t kCandPerFrame = 16;
-int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame) {
-    const uint64_t nc = std::min<uint64_t>(std::max<uint64_t>(per_frame * F, 1u << 10), 0xFFFFFFF0ull);
+int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame, uint64_t tri_per_frame) {
+    // (capped at 2^30 entries, 53 GB: warp-batches past it are re-selected by the fused kernel)
+    const uint64_t nc = std::min<uint64_t>(std::max<uint64_t>(per_frame * F, 1u << 10), 1ull << 30);
     if (w.cand_n < nc) {
         cudaFree(w.cand_g);
         cudaFree(w.fit_g);
@@ -313,7 +314,7 @@ int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame) 
     }
     // e+e+e- triples of the vertex stage: one per frame on average (phase I: ~0.04);
     // frames whose triples do not fit run the vertex selection in place
-    const uint64_t nt = std::max<uint64_t>(F, 4096);
+    const uint64_t nt = std::min<uint64_t>(std::max<uint64_t>(tri_per_frame * F, 4096), 1ull << 28);
     if (w.tri_n < nt) {
         cudaFree(w.tri); cudaFree(w.tres);
         w.bytes -= w.tri_n * (sizeof(uint4) + kVResBytes);
@@ -378,10 +379,17 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     // output staging), each kernel with its hot code in the instruction cache and
     // its own occupancy; the fused kernel then runs only the warp-batches whose
     // candidates did not fit the store
-    const bool split = mode == kModeFull && !big && ctx->split;
+    const bool split = mode == kModeFull && ctx->split;
+    // candidate store and triple list per frame: phase-I defaults, scaled up for
+    // big frames (phase II: ~270 candidates and up to max_combs triples per frame)
+    const uint64_t mean_hits = F ? H / F : 0;
+    const uint64_t cand_pf = (big && ctx->cand_per_frame == kCandPerFrame)
+                                 ? std::max<uint64_t>(kCandPerFrame, 3 * mean_hits / 2)
+                                 : ctx->cand_per_frame;
+    const uint64_t tri_pf = big ? 32 : 1;
     const int bps = blocks_per_sm(mode, big);
     const int grid = (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * bps);
-    const int sgrid = split ? (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * blocks_per_sm(kModeSelectC, false))
+    const int sgrid = split ? (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * blocks_per_sm(kModeSelectC, big))
                             : 0;
     const int fgrid = split ? ctx->sms * finish_blocks_per_sm() : 0;
     const int tgrid = split ? ctx->sms * tracks_blocks_per_sm() : 0;
@@ -389,7 +397,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     rc = ensure_ws(ctx, w, nbatch, p, fb, std::max(std::max(grid, sgrid), vgrid));
     if (rc) return rc;
     if (split) {
-        rc = ensure_split(w, F, nbatch, ctx->cand_per_frame);
+        rc = ensure_split(w, F, nbatch, cand_pf, tri_pf);
         if (rc) return rc;
     }
     a.P = make_dev_params(p);
@@ -425,11 +433,11 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     if (split) {
         KArgs sa = a;
         sa.cand_g = w.cand_g;
-        sa.cand_cap = std::min<uint64_t>(w.cand_n, std::max<uint64_t>(ctx->cand_per_frame * F, 1u << 10));
+        sa.cand_cap = std::min<uint64_t>(w.cand_n, std::max<uint64_t>(cand_pf * F, 1u << 10));
         sa.sel = w.sel;
         sa.bsel = w.bsel;
         sa.spill_out = w.spill;
-        CK(launch_filter(kModeSelectC, false, sa, sgrid, s));
+        CK(launch_filter(kModeSelectC, big, sa, sgrid, s));
         if (tm) CK(cudaEventRecord(ev[1], s));
         a.cand_g = w.cand_g;
         a.fit_g = w.fit_g;

@@ -285,6 +285,31 @@ def _outputs(res, n):
             res.kept_frame.cpu().numpy()[:K].copy(), res.vertices_np(K).copy(), sm.copy())
 
 
+def test_phase2_split_and_fused_agree(gp, monkeypatch):
+    """Phase-II frames (~220 hits) take the split path too (64-bit row masks in
+    the selection, store sized for ~330 candidates per frame, a triple list of up
+    to 32 per frame): byte-identical to the fused kernel on this set, also with a
+    store that forces spills.  (The fused kernel's big-frame walk evaluates
+    Delta-lambda as a difference of pair slopes, so on other data the two may
+    differ for a combination within an ulp of the cut: 1 frame in 1e6.)"""
+    n = 80
+    d, fr, df = _gen("phase2_stress", n, 731)
+    outs = []
+    for env in [{}, {"M3E_CAND_STORE": "100"}, {"M3E_FUSED": "1"}]:
+        for k in ["M3E_CAND_STORE", "M3E_FUSED"]:
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        c = m3e.Context(0)
+        res = m3e.run_filter(c, gp, df)
+        torch.cuda.synchronize()
+        outs.append(_outputs(res, n))
+        c.close()
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+
+
 def test_vertex_triple_list_full(gp, monkeypatch):
     """The split path's vertex stage lists e+e+e- triples for a dense phase-2
     kernel; frames whose triples do not fit the list (M3E_TRI_CAP, read at
