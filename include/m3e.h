@@ -174,8 +174,10 @@ uint64_t m3e_workspace_bytes(const m3e_context* ctx);
 int m3e_set_timing(m3e_context* ctx, int enable);
 int m3e_kernel_times(m3e_context* ctx, float ms[6]);
 
-/* Full hot path on device-resident input (the call bench.py times):
- * select -> fit -> vertex -> pack for frames [0, F).  Outputs [dev]. */
+/* Full hot path on device-resident input (the call bench.py times): Selection
+ * Cuts -> triplet fit -> tracks -> vertex selection -> output staging -> pack for
+ * frames [0, F), nine kernel launches on `stream`.
+ * Outputs [dev]; frames, tracks, vertices and kept frames in frame order. */
 int m3e_filter(m3e_context* ctx, const m3e_params* p, const float* x, const float* y, const float* z,
                const uint32_t* offsets, uint64_t F, uint64_t H, const m3e_outputs* out, void* stream);
 
