@@ -483,16 +483,14 @@ static __device__ __noinline__ int select_frame_big(const DevParams* __restrict_
         count += __popc(m);
         return count > P.cuts_max;
     };
+    int lo = 0;   // this lane's list-1 entry, advanced monotonically (e grows by 32 per step)
     for (long long base = 0; base < Wk; base += 32) {
         const long long e = base + lane;
         bool pass = false;
         uint32_t pk = 0;
         if (e < Wk) {
-            int lo = 0, hi = c01 - 1;               // list-1 entry: largest p with wpre[p] <= e
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if ((long long)wpre[mid] <= e) lo = mid; else hi = mid - 1;
-            }
+            // list-1 entry: largest p with wpre[p] <= e (wpre non-decreasing)
+            while (lo + 1 < c01 && (long long)wpre[lo + 1] <= e) ++lo;
             const uint32_t a = l01[lo];
             const int i1 = (a >> 10) & 1023u;
             const int k = (int)off12[i1] + (int)(e - (long long)wpre[lo]);
