@@ -106,19 +106,34 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def kernel_source_hash() -> str:
+    """sha256 (16 hex) of the CUDA sources: a committed ncu capture is used only if
+    it was taken of these sources"""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2206_11535_b200", "csrc")
+    for fn in sorted(os.listdir(csrc)):
+        with open(os.path.join(csrc, fn), "rb") as fh:
+            h.update(fn.encode() + fh.read())
+    return h.hexdigest()[:16]
+
+
 def load_profile(workload: str, frames: int, seed: int):
-    """Per-kernel ncu counters (DRAM bytes, executed warp instructions per launch)
-    of the committed capture of this exact configuration
-    (profiles/*_bench_traffic.json), else {}."""
+    """Per-kernel ncu counters (DRAM bytes, executed warp instructions, pipe
+    utilisation per launch) of the committed capture of this exact configuration
+    AND these kernel sources (profiles/*_bench_traffic.json): (kernels, file name),
+    else ({}, None)."""
     import glob
+    src = kernel_source_hash()
     for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_bench_traffic.json")), reverse=True):
         try:
             t = json.load(open(fn))
         except Exception:
             continue
-        if t.get("workload") == workload and t.get("frames") == frames and t.get("seed") == seed:
-            return t.get("kernels", {})
-    return {}
+        if (t.get("workload") == workload and t.get("frames") == frames and t.get("seed") == seed
+                and t.get("source_hash") == src):
+            return t.get("kernels", {}), os.path.relpath(fn, ROOT)
+    return {}, None
 
 
 def load_peaks():
@@ -145,6 +160,27 @@ def generate(preset: str, n_frames: int, frame0: int, seed: int, world: int = 1)
     return d, time.time() - t
 
 
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def time_oracle(P, fr, first: int, count: int, threads: int) -> float:
+    """Wall time of the CPU oracle (unchanged, fp64 C) over frames [first,
+    first + count), split into `threads` contiguous slices run concurrently (frames
+    are independent, Sec. V; ctypes releases the GIL during each call)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    cuts = [first + count * i // threads for i in range(threads + 1)]
+    t = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda i: oracle.process_frames(P, fr, first=cuts[i], count=cuts[i + 1] - cuts[i]),
+                    range(threads)))
+    return time.perf_counter() - t
+
+
 def run_reference(a, rank, world):
     """Tier reference arm: the CPU oracle as it stands, on the host cores."""
     if rank != 0:
@@ -153,14 +189,13 @@ def run_reference(a, rank, world):
     from paper_2206_11535_b200.m3e import load_config
     cfg = load_config()
     P = oracle.make_params(cfg)
-    sample = a.ref_frames
+    cores = host_cores()
+    sample = a.ref_frames * cores
     d, _ = generate(a.workload, sample * (a.steps + a.warmup), 0, a.seed)
     fr = oracle.Frames(d)
     times = []
     for s in range(a.warmup + a.steps):
-        t = time.perf_counter()
-        oracle.process_frames(P, fr, first=s * sample, count=sample)
-        dt = time.perf_counter() - t
+        dt = time_oracle(P, fr, s * sample, sample, cores)
         if s >= a.warmup:
             times.append(dt)
     fps = sample / statistics.mean(times)
@@ -170,9 +205,10 @@ def run_reference(a, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT.get(a.workload, a.workload).format(F=a.frames),
-                       "sample_frames_per_step": sample, "parallelism": "single core"},
-            "cpu_baseline": {"value": round(v, 6), "unit": "Gbps", "cores": 1, "kind": "oracle",
-                             "sample": f"{sample} frames per step, single-threaded fp64 C oracle",
+                       "sample_frames_per_step": sample, "parallelism": f"{cores} host threads"},
+            "cpu_baseline": {"value": round(v, 6), "unit": "Gbps", "cores": cores, "kind": "oracle",
+                             "sample": f"{sample} frames per step (consecutive frames of the workload), fp64 C "
+                                       f"oracle, {cores} threads on contiguous frame slices",
                              "frames_per_s": round(fps, 1)},
             "e2e": {"value": round(v, 6), "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -188,15 +224,27 @@ def main():
     ap.add_argument("--workload", default="phase1_sig", help="synth preset (phase1_sig, phase1_bg, phase2_stress)")
     ap.add_argument("--seed", type=int, default=20220623)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--ref-frames", type=int, default=4000, help="oracle sample per step")
-    ap.add_argument("--cpu-sample", type=int, default=15000, help="oracle sample for cpu_baseline")
+    ap.add_argument("--ref-frames", type=int, default=4000, help="oracle sample per step and host core")
+    ap.add_argument("--cpu-sample", type=int, default=15000, help="oracle sample for cpu_baseline, per host core")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-phys", action="store_true", help="skip the truth-based efficiency sample")
     ap.add_argument("--phys-frames", type=int, default=200000)
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3) if a.impl == "b200" else a.warmup
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (rendezvous on
+        # 127.0.0.1), which sets RANK / LOCAL_RANK / WORLD_SIZE for every rank
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank, world, local = dist_env()
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
 
     if a.impl == "reference":
         run_reference(a, rank, world)
@@ -205,6 +253,8 @@ def main():
     import torch
     from paper_2206_11535_b200 import m3e
 
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local}, {torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -323,81 +373,103 @@ def main():
         import oracle
         P = oracle.make_params(m3e.load_config())
         fr = oracle.Frames(d)
-        n = min(a.cpu_sample, F)
-        t = time.perf_counter()
-        oracle.process_frames(P, fr, first=0, count=n)
-        dt = time.perf_counter() - t
-        cpu = {"value": round(gbps_equiv(n / dt, rate), 6), "unit": "Gbps", "cores": 1, "kind": "oracle",
-               "sample": f"first {n} frames of the workload, single-threaded fp64 C oracle",
+        cores = host_cores()
+        n = min(a.cpu_sample * cores, F)
+        dt = time_oracle(P, fr, 0, n, cores)
+        cpu = {"value": round(gbps_equiv(n / dt, rate), 6), "unit": "Gbps", "cores": cores, "kind": "oracle",
+               "sample": f"first {n} frames of the workload, fp64 C oracle, {cores} threads on contiguous "
+                         f"frame slices",
                "frames_per_s": round(n / dt, 1)}
 
     if rank == 0:
         peak, peak_kind = load_peaks()
-        # algorithmic bytes per launch:
-        #   selection kernel: hit stream in, selection words (4 B/frame) + store entries (16 B) out
-        #   fit kernel: store entries + the candidates' frames (hit stream) in, fit records (32 B) out
-        #   tracks kernel: selection words + code bytes (1 B per entry) in, track words out
-        #   vertex kernel: the listed frames' fit records + hits in (~1% of frames), small
-        #   finish kernel (+ the fused kernel over spilled warp-batches, ~0): selection
-        #   and track words in, per-frame outputs, kept records out
-        #   (fused path: one kernel, hit stream in + outputs)
-        split = ms_select > 0
-        cand = int(sm["candidates"])
-        big = H > 60 * F
-        if split:
-            kernels = [("m3e::filter_kernel<SELECT_C, BIG=false>", ms_select, in_bytes + 4 * F + 16 * cand),
-                       ("m3e::fit_kernel", ms_fit, in_bytes + 16 * cand + 32 * cand),
-                       ("m3e::tracks_kernel", ms_tracks, 4 * F + cand + 4 * F),
-                       ("m3e::finish_kernel", ms_filter, 8 * F + F * (1 + 16) + kept * 64)]
-        else:
-            kernels = [("m3e::filter_kernel<FULL, BIG=%s>" % ("true" if big else "false"), ms_filter,
-                        in_bytes + out_bytes)]
-        kname, kms, alg_bytes = max(kernels, key=lambda k: k[1])
-        achieved = alg_bytes / (kms / 1e3) / 1e9
         clocks = clk.summary()
-        prof = load_profile(a.workload, F, a.seed)
-        kp = prof.get(kname, {})
-        traffic = (kp["dram_read_bytes"] + kp["dram_write_bytes"]) if "dram_read_bytes" in kp else None
-        # instruction-issue roofline of the two issue-bound kernels:
-        # warp instructions per launch (ncu, committed capture of this configuration) over
-        # the live kernel time, against 148 SMs x 4 schedulers x 1 warp-instruction/cycle
-        # at the sampled SM clock
+        prof, prof_file = load_profile(a.workload, F, a.seed)
+        # instruction-issue peak: 148 SMs x 4 schedulers x 1 warp instruction per cycle at
+        # the SM clock sampled during the timed region
         sm_mhz = clocks.get("sm_mhz") or 1965.0
         issue_peak = 148 * 4 * sm_mhz * 1e6 / 1e9   # G warp-instructions/s
-        issue = {}
-        for key, kn, kt in (("select", "m3e::filter_kernel<SELECT_C, BIG=false>", ms_select),
-                            ("fit", "m3e::fit_kernel", ms_fit)):
-            ie = prof.get(kn, {}).get("inst_executed")
-            if ie and kt > 0:
-                ach = ie / (kt / 1e3) / 1e9
-                issue[key] = {"warp_inst_per_launch": int(ie), "achieved": round(ach, 1), "peak": round(issue_peak, 1),
-                              "unit": "G warp-inst/s", "frac": round(ach / issue_peak, 4)}
+        # the method's own bytes: hit stream in, final outputs out
+        tracks = int(sm["tracks"])
+        split = ms_select > 0
+        big = H > 60 * F
+        if split:
+            names = [("select", "m3e::filter_kernel<SELECT_C, BIG=false>", ms_select, in_bytes),
+                     ("fit", "m3e::fit_kernel", ms_fit, in_bytes + 32 * tracks),
+                     ("tracks", "m3e::tracks_kernel", ms_tracks, 0),
+                     ("vertex", "m3e::vertex_kernel+triple_kernel+vpost_kernel", ms_vertex, 0),
+                     ("finish", "m3e::finish_kernel", ms_filter, 17 * F),
+                     ("pack", "m3e::pack_kernel", ms_pack, out_bytes - 17 * F)]
+        else:
+            names = [("filter", "m3e::filter_kernel<FULL, BIG=%s>" % ("true" if big else "false"), ms_filter,
+                      in_bytes + out_bytes), ("pack", "m3e::pack_kernel", ms_pack, out_bytes)]
+        per = {}
+        for key, kn, kt, alg in names:
+            e = {"ms": round(kt, 4), "share": round(kt / ms_step, 4), "method_bytes": int(alg)}
+            kp = {}
+            parts = kn.split("+")
+            for part in parts:
+                part = part if part.startswith("m3e::") else "m3e::" + part
+                for k2, v2 in prof.get(part, {}).items():
+                    if len(parts) == 1 or k2 in ("dram_read_bytes", "dram_write_bytes", "inst_executed"):
+                        kp[k2] = kp.get(k2, 0) + v2
+            if kp and kt > 0:
+                e["dram_bytes"] = int(kp["dram_read_bytes"] + kp["dram_write_bytes"])
+                e["dram_frac"] = round(e["dram_bytes"] / (kt / 1e3) / 1e9 / peak, 4)
+                e["issue_frac"] = round(kp["inst_executed"] / (kt / 1e3) / 1e9 / issue_peak, 4)
+                for pipe in ("alu", "fma", "xu", "lsu"):
+                    if f"pipe_{pipe}_pct" in kp:
+                        e[f"pipe_{pipe}_pct"] = round(kp[f"pipe_{pipe}_pct"], 1)
+            if alg and kt > 0:
+                e["method_frac"] = round(alg / (kt / 1e3) / 1e9 / peak, 4)
+            per[key] = e
+        # dominant kernel: the one taking the largest share of the step
+        dom = max(names, key=lambda k: k[2])
+        kname, kms, alg_bytes = dom[1], dom[2], dom[3]
+        kp = prof.get(kname, {})
+        traffic = (kp["dram_read_bytes"] + kp["dram_write_bytes"]) if "dram_read_bytes" in kp else None
+        ie = kp.get("inst_executed")
+        if ie:
+            # bound by instruction issue (DRAM well below peak: see roofline.kernels)
+            roof = {"bound": "issue", "achieved": round(ie / (kms / 1e3) / 1e9, 2), "peak": round(issue_peak, 2),
+                    "unit": "G warp-inst/s", "frac": round(ie / (kms / 1e3) / 1e9 / issue_peak, 4),
+                    "warp_inst_per_launch": int(ie)}
+        else:
+            roof = {"bound": "hbm", "achieved": round(alg_bytes / (kms / 1e3) / 1e9, 2), "peak": peak,
+                    "unit": "GB/s", "frac": round(alg_bytes / (kms / 1e3) / 1e9 / peak, 4)}
+        step_bytes = in_bytes + out_bytes
+        roof.update({
+            "traffic": traffic, "kernel": kname, "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms_step, 4),
+            "algorithmic_bytes_per_launch": int(alg_bytes),
+            "hbm_frac_of_kernel": round(alg_bytes / (kms / 1e3) / 1e9 / peak, 4),
+            "hbm_peak": peak, "peak_kind": peak_kind, "profile": prof_file,
+            "step_hbm": {"method_bytes": int(step_bytes), "achieved": round(step_bytes / (ms_step / 1e3) / 1e9, 1),
+                         "peak": peak, "unit": "GB/s", "frac": round(step_bytes / (ms_step / 1e3) / 1e9 / peak, 4),
+                         "dram_bytes_ncu": int(sum(v.get("dram_bytes", 0) for v in per.values())) if prof else None},
+            "kernels": per, "candidates_per_frame": round(int(sm["candidates"]) / F, 3)})
         line = {
             "metric": METRIC, "value": round(gbps_equiv(fps, rate), 3), "unit": "Gbps", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT.get(a.workload, a.workload).format(F=F),
-                       "frames": int(tot_frames), "hits": int(tot_hits),
+                       # headline: frames/s and the real-time factor (64 ns frames arrive at
+                       # 15.625e6 frames/s); value = the same rate as Phase-I-equivalent Gbps
+                       "realtime_factor": round(fps / PHASE1_FRAMES_PER_S, 3),
+                       "realtime_factor_per_gpu": round(fps / (world * PHASE1_FRAMES_PER_S), 3),
                        "frames_per_s": round(fps, 1), "hits_per_s": round(tot_hits / ms_max * 1e3, 1),
+                       "value_definition": "frames/s x 80 Gbps / 15.625e6 frames/s x (muon rate / 1e8): the "
+                                           "paper's 80 Gbps Phase-I stream scaled by the real-time factor",
                        "hit_stream_gbps": round(8 * in_bytes * world / ms_max / 1e9 * 1e3, 3),
+                       "frames": int(tot_frames), "hits": int(tot_hits),
                        "kept_frames": int(tot_kept),
                        "reduction_factor": round(tot_frames / tot_kept, 2) if tot_kept else None,
                        "kept_by_reason": {m3e.REASON_NAMES[i]: int(counters[6 + i]) for i in range(1, 6)},
-                       "realtime_factor": round(fps / (world * PHASE1_FRAMES_PER_S), 3),
                        "muon_rate": rate,
                        "l2": "inputs (%.2f GB) >> 126 MB L2, no flush needed" % (in_bytes / 1e9),
                        "parallelism": f"frame-sharded dp{world}", "generation_s": round(t_gen, 1),
                        "physics": phys},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "peak_kind": peak_kind, "issue": issue or None,
-                         "kernel": kname, "kernel_ms": round(kms, 4), "share_of_step": round(kms / ms_step, 4),
-                         "algorithmic_bytes_per_launch": int(alg_bytes),
-                         "kernels_ms": {"select": round(ms_select, 4), "fit": round(ms_fit, 4),
-                                        "tracks": round(ms_tracks, 4), "vertex": round(ms_vertex, 4),
-                                        "finish": round(ms_filter, 4), "pack": round(ms_pack, 4)},
-                         "candidates_per_frame": round(cand / F, 3)},
+            "roofline": roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (9 if split else 2) * a.steps, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -103,6 +103,7 @@ def lib():
         L.or_select.argtypes = [_P(Params), _vp, _vp, _vp, _vp, _P(Candidate), ctypes.c_int,
                                 _P(FrameResult)]
         L.or_fit_candidate.argtypes = [_P(Params), _vp, _vp, _vp, _vp, _P(Candidate), _P(Track)]
+        L.or_track_params.argtypes = [_P(Params), d3, d3, c_double, _P(Track)]
         L.or_vertex_frame.argtypes = [_P(Params), _P(VTrack), ctypes.c_int, _P(FrameResult),
                                       _P(Vertex), ctypes.c_int]
         L.or_process_frame.argtypes = [_P(Params), _vp, _vp, _vp, _vp, _P(FrameResult),
@@ -222,6 +223,16 @@ def fit_candidate(P: Params, fr: Frames, f: int, cand: Candidate) -> Track:
     o = Track()
     lib().or_fit_candidate(ctypes.byref(P), fr.x.ctypes.data, fr.y.ctypes.data, fr.z.ctypes.data,
                            fr.start_ptr(f), ctypes.byref(cand), ctypes.byref(o))
+    return o
+
+
+def track_params(P: Params, h0, h1, kappa: float):
+    """Reading R11 at signed curvature kappa: a Track with q, cos_theta01, cx, cy,
+    rt, p, energy set (None if no short arc of that curvature joins h0, h1)."""
+    o = Track()
+    o.kappa = kappa
+    if lib().or_track_params(ctypes.byref(P), _d3(h0), _d3(h1), kappa, ctypes.byref(o)) != 0:
+        return None
     return o
 
 

@@ -308,12 +308,25 @@ int or_fit_candidate(const or_params* P, const float* x, const float* y, const f
     o->chi2 = triplet_chi2_at(&o->t1, o->kappa) + triplet_chi2_at(&o->t2, o->kappa);
     if (near(o->chi2, P->chi2_max, band)) o->marginal = 1;
     if (!(o->chi2 < P->chi2_max)) { o->status = OR_FIT_CHI2; return 0; }
-    /* track parameters (Sec. IV-B last paragraph, Sec. IV-C circles), reading R11 */
-    double k = fabs(o->kappa);
-    o->q = o->kappa > 0 ? +1 : -1;
+    if (or_track_params(P, h0, h1, o->kappa, o) != 0) { o->status = OR_FIT_DOMAIN; return 0; }
+    o->status = OR_FIT_OK;
+    o->accepted = 1;
+    return 0;
+}
+
+/* Track parameters of an accepted track (Sec. IV-B last paragraph "the track
+ * parameters are calculated", Sec. IV-C circles), reading R11, at signed global
+ * curvature kappa: charge q = sign(kappa), polar angle of arc h0 -> h1 from the
+ * exact arc relation at |kappa|, transverse circle of radius sin(theta01)/|kappa|
+ * through h0 and h1, p = PT_CONV B / |kappa|, E = sqrt(p^2 + m_e^2).
+ * Sets o->q, cos_theta01, cx, cy, rt, p, energy; -1 if no short arc of that
+ * curvature joins h0 and h1. */
+int or_track_params(const or_params* P, const double h0[3], const double h1[3], double kappa, or_track* o) {
+    double k = fabs(kappa);
+    o->q = kappa > 0 ? +1 : -1;
     double d01 = hypot(h1[0] - h0[0], h1[1] - h0[1]), z01 = h1[2] - h0[2];
     double phi01 = or_arc_phi(d01, z01, k);
-    if (isnan(phi01)) { o->status = OR_FIT_DOMAIN; return 0; }
+    if (isnan(phi01)) return -1;
     double cth = z01 * k / phi01;
     if (cth > 1) cth = 1;
     if (cth < -1) cth = -1;
@@ -327,8 +340,6 @@ int or_fit_candidate(const or_params* P, const float* x, const float* y, const f
     o->rt = rt;
     o->p = PT_CONV * P->b_field / k;
     o->energy = sqrt(o->p * o->p + M_E * M_E);
-    o->status = OR_FIT_OK;
-    o->accepted = 1;
     return 0;
 }
 

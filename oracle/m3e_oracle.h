@@ -157,6 +157,9 @@ int or_select(const or_params* P, const float* x, const float* y, const float* z
               or_candidate* cand, int cap, or_frame_result* res);
 int or_fit_candidate(const or_params* P, const float* x, const float* y, const float* z,
                      const uint32_t start[5], const or_candidate* c, or_track* out);
+/* reading R11 at a given signed kappa (used by or_fit_candidate; exported so the
+ * tests can propagate the kappa tolerance through the vertex stage) */
+int or_track_params(const or_params* P, const double h0[3], const double h1[3], double kappa, or_track* o);
 int or_vertex_frame(const or_params* P, const or_vtrack* tracks, int n, or_frame_result* res,
                     or_vertex* all_out, int all_cap);
 int or_process_frame(const or_params* P, const float* x, const float* y, const float* z,

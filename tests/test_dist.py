@@ -51,3 +51,21 @@ def test_gloo_world2():
         assert tmax == 1.5
         assert ids == [0, 3, 1000, 1003, 1006]
     assert [r[4] for r in res] == [(0, 500), (500, 501)]
+
+
+def test_bench_spawns_ranks_for_gpus_n():
+    """bench.py --gpus 2 without an outer torchrun re-launches itself under
+    torch.distributed.run (2 ranks, 127.0.0.1); on the reference arm rank 0 alone
+    prints the JSON line and rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "0", "--ref-frames", "20"], capture_output=True, text=True,
+                         timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
+    assert lines[0]["cpu_baseline"]["cores"] >= 1

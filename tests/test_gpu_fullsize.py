@@ -7,7 +7,7 @@ import pytest
 
 import oracle
 import synth
-from parity import KAPPA_FLOOR, REL_KAPPA
+from parity import compare_outputs
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -21,24 +21,12 @@ BENCH_SEED = 20220623   # bench.py --seed default
 FRAMES_1S = 15_625_000  # one second of 64 ns frames
 
 
-def _check_frames(P, fr, d, frames_np, tracks_np, sample):
-    explained = []
-    for f in sample:
-        f = int(f)
-        o, otr = oracle.process_frame(P, fr, f)
-        g = frames_np[f]
-        gt = tracks_np[int(g["track_first"]):int(g["track_first"]) + min(int(g["n_tracks"]), P.max_tracks)]
-        same = (int(g["reason"]) == o.reason and int(g["n_cand"]) == o.n_cand and
-                int(g["n_tracks"]) == o.n_tracks and int(g["n_combs"]) == o.n_combs)
-        if same and o.reason != oracle.REASON_TRIPLET_OVERFLOW:
-            same = [tuple(int(h) for h in t["hit"]) for t in gt] == [tuple(t.hit) for t in otr]
-        if not same:
-            assert o.n_cand_marginal or o.n_fit_marginal or o.n_vertex_marginal, f"frame {f}: {g} vs {o.reason}"
-            explained.append(f)
-            continue
-        for t, u in zip(gt, otr):
-            assert abs(float(t["kappa"]) - u.kappa) <= REL_KAPPA * max(abs(u.kappa), KAPPA_FLOOR)
-    return explained
+def _check_frames(P, fr, res, frames_np, tracks_np, sample, name):
+    """sampled frames against the oracle, item by item (tests/parity.py)"""
+    K = int(np.count_nonzero(frames_np["reason"]))
+    tally = compare_outputs(P, fr, frames_np, tracks_np, res.vertices_np(K), sample)
+    print(tally.report(f"{name}: {len(sample)} sampled frames"))
+    return tally
 
 
 def _run(ctx, gp, d, track_cap, kept_cap):
@@ -81,9 +69,9 @@ def test_fullsize_phase1_second(cfg):
     rng = np.random.default_rng(1)
     sample = np.unique(np.concatenate([rng.integers(0, F, 2500), rng.choice(kept, min(K, 1500), replace=False)]))
     fr = oracle.Frames(d)
-    explained = _check_frames(P, fr, d, frames_np, tracks_np, sample)
-    print(f"full size: {len(sample)} sampled frames, {len(explained)} near-threshold: {explained[:10]}")
-    assert len(explained) <= max(2, 2e-3 * len(sample))
+    tally = _check_frames(P, fr, res, frames_np, tracks_np, sample, "configs[3] full size")
+    assert len(tally.frames) <= max(2, 2e-3 * len(sample))
+    assert tally.counts().get("_vertex_compared", 0) > 100
     # packed kept frames: verbatim hits of sampled kept frames
     koff = res.kept_offsets[:4 * K + 1].cpu().numpy().view(np.uint32).astype(np.int64)
     kz = res.kept_z.cpu().numpy()
@@ -108,6 +96,6 @@ def test_phase2_sampled(cfg):
     frames_np = res.frames_np(n)
     tracks_np = res.tracks_np(int(sm["tracks"]))
     sample = np.random.default_rng(2).choice(n, 400, replace=False)
-    explained = _check_frames(P, oracle.Frames(d), d, frames_np, tracks_np, sample)
-    assert len(explained) <= max(2, 5e-3 * len(sample))
+    tally = _check_frames(P, oracle.Frames(d), res, frames_np, tracks_np, sample, "configs[4]")
+    assert len(tally.frames) <= max(2, 5e-3 * len(sample))
     ctx.close()

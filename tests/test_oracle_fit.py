@@ -126,6 +126,29 @@ def test_full_track_noiseless(P):
         assert t.cos_theta01 == pytest.approx(mom[2] / np.linalg.norm(mom), abs=1e-5)
 
 
+@pytest.mark.parametrize("q", [+1, -1])
+@pytest.mark.parametrize("mom", [(-12.0, 21.0, 9.0), (30.0, 4.0, -20.0), (3.0, -18.0, 1.0)])
+def test_track_params_recover_helix_circle(P, q, mom):
+    """Reading R11 at the TRUE curvature of a helix (test-side model, not the
+    oracle): the circle through h0, h1 of radius sin(theta)/|kappa| is the helix's
+    transverse circle, cos(theta01) its p_z / p, p and E the true ones; a curvature
+    too small to join h0 and h1 by a short arc has no parameters."""
+    mom = np.array(mom)
+    v = (2.0, -3.0, 7.0)
+    hits = track_hits(v, mom, q, LAYERS)
+    h = Helix(v, mom, q)
+    kap = q * 0.299792458 / np.linalg.norm(mom)
+    t = oracle.track_params(P, hits[0], hits[1], kap)
+    assert t is not None and t.q == q
+    assert t.rt == pytest.approx(h.Rt, rel=1e-9)
+    assert (t.cx, t.cy) == pytest.approx(tuple(h.c), abs=1e-7)
+    assert t.cos_theta01 == pytest.approx(mom[2] / np.linalg.norm(mom), abs=1e-9)
+    assert t.p == pytest.approx(np.linalg.norm(mom), rel=1e-12)
+    assert t.energy == pytest.approx(math.hypot(np.linalg.norm(mom), 0.51099895), rel=1e-12)
+    d01 = math.hypot(hits[1][0] - hits[0][0], hits[1][1] - hits[0][1])
+    assert oracle.track_params(P, hits[0], hits[1], q * 2.5 / d01) is None   # 1/k^2 < d^2/4
+
+
 def test_closest_layer3_hit_chosen(P):
     """Alg. 3 find_closest_layer3_hit: the true hit is picked among decoys."""
     mom = np.array([15.0, 20.0, -6.0])
