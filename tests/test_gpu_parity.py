@@ -240,6 +240,7 @@ def test_full_parity(ctx, gp, P, name, n, seed):
     sm = res.summary_np()
     assert int(sm["overflow"]) == 0
     frames_np = res.frames_np(n)
+    tracks_np = res.tracks_np(int(sm["tracks"]))
     tally = _compare_full(P, fr, res, n, name)
     assert len(tally.frames) <= max(1, 2e-3 * n)
     if name in ("phase1_sig", "signal_only"):

@@ -62,6 +62,25 @@ def cut_variables(cfg, d, f, P):
     return rows
 
 
+def _signal_tracks(sig, sig_cfg, f, tracks):
+    """({signal particle: index of the track with exactly its four hits}, signal
+    particle ids, particle table), or (None, ...) unless all three are found"""
+    parts = synth.particles(sig_cfg, f)
+    th = true_hits(sig, f)
+    sigp = [i for i, p in enumerate(parts) if p["kind"] in (1, 2)]
+    idx = {}
+    for s in sigp:
+        lay = th.get(s, {})
+        if len(lay) != 4:
+            continue
+        want = tuple(lay[l] - int(sig["offsets"][4 * f + l]) for l in range(4))
+        for ti, t in enumerate(tracks):
+            if tuple(t.hit) == want:
+                idx[s] = ti
+                break
+    return (idx if len(idx) == 3 and len(sigp) == 3 else None), sigp, parts
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=4000)
@@ -110,9 +129,38 @@ def main():
           f"({kept_true}/{n_true}); funnel kept fractions {np.round(funnel[1:] / funnel[0], 4)}")
 
     # ---------------- vertex tests: tune on reconstructed true signal triples
+    qv = a.qv
+    frs = oracle.Frames(sig)
+    # "All intersections too far away from the target, represented by a disk with a
+    # radius of 19mm, are dismissed" (Sec. IV-C): the disk is given, "too far" is not
+    # (reading R18): xy_margin = the qv quantile, over reconstructed true signal
+    # triples, of the largest distance beyond the disk among the triple's three pair
+    # intersections nearest the true decay vertex
+    Pv = oracle.make_params(dict(cfg, xy_margin=1e9))
+    excess = []
+    for f in range(sig["n_frames"]):
+        res, tracks = oracle.process_frame(Pv, frs, f)
+        idx, sigp, parts = _signal_tracks(sig, sig_cfg, f, tracks)
+        if idx is None:
+            continue
+        v = parts[sigp[0]]["v"]
+        ks = [idx[s] for s in sigp]
+        worst = -1e9
+        for u, w in ((ks[0], ks[1]), (ks[0], ks[2]), (ks[1], ks[2])):
+            pts, _ = oracle.circle_intersections((tracks[u].cx, tracks[u].cy), tracks[u].rt,
+                                                 (tracks[w].cx, tracks[w].cy), tracks[w].rt)
+            if not pts:
+                worst = None
+                break
+            p = min(pts, key=lambda p: np.hypot(p[0] - v[0], p[1] - v[1]))
+            worst = max(worst, float(np.hypot(*p)) - cfg["target_r"])
+        if worst is not None:
+            excess.append(worst)
+    cfg["xy_margin"] = float(max(0.0, np.quantile(excess, qv)))
+    print(f"xy_margin: {len(excess)} true triples with three intersecting pairs; "
+          f"{qv} quantile of the distance beyond the {cfg['target_r']} mm disk: {cfg['xy_margin']:.3f} mm")
     vac = dict(cfg, e_window=1e9, chi2_vertex_max=1e30, target_dist_max=1e9, p_total_max=1e9)
     Pv = oracle.make_params(vac)
-    frs = oracle.Frames(sig)
     dE, chi, tdist, ptot = [], [], [], []
     for f in range(sig["n_frames"]):
         res, tracks = oracle.process_frame(Pv, frs, f)
@@ -150,7 +198,6 @@ def main():
         tdist.append(verts[0].target_dist)
         ptot.append(verts[0].p_total)
     dE, chi, tdist, ptot = map(np.array, (dE, chi, tdist, ptot))
-    qv = a.qv
     cfg["e_window"] = float(np.quantile(dE, qv))
     cfg["chi2_vertex_max"] = float(np.quantile(chi, qv))
     cfg["target_dist_max"] = float(np.quantile(tdist, qv))
@@ -162,7 +209,7 @@ def main():
         print(f"  {k} = {cfg[k]:.6g}")
     cfg["_provenance"] = ("written by tools/tune_thresholds.py (oracle/ + synth/ only), seeds 7001/7002, "
                           f"{a.frames} phase1_bg + {a.signal_frames} signal_only frames, per-cut quantile {q}, "
-                          f"vertex quantile {qv}")
+                          f"vertex quantile {qv} (xy_margin included, R18)")
     if a.write:
         with open(CFG_PATH, "w") as fh:
             json.dump(cfg, fh, indent=2)
