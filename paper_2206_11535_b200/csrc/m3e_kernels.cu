@@ -545,6 +545,7 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
     }
     if (lane == 0) {
         A.bsel[b] = fits ? (uint32_t)base : kSpilled;
+        A.bcnt[b] = fits ? tot : 0u;
         if (!fits) A.spill_out[atomicAdd(A.ticket + 5, 1u)] = b;   // for the fused kernel
     }
     return true;
@@ -863,6 +864,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
             }
             if (lane == 0) {
                 A.bsel[b] = fits ? (uint32_t)base : kSpilled;
+                A.bcnt[b] = fits ? tot : 0u;
                 if (!fits) A.spill_out[atomicAdd(A.ticket + 5, 1u)] = b;   // for the fused kernel
             }
         }
@@ -1216,8 +1218,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const KArgs A) {
                     if (ps_trk == kSpilled && pc_n) {
                         const char* fr = reinterpret_cast<const char*>(A.fit_g + pc_base);
                         const uint32_t nl = (pc_n * 32u + 127u) / 128u + 1u;
-                        if ((uint32_t)lane < nl) prefetch_l2(fr + 128 * lane);
-                        if (lane == 31) prefetch_l2(A.code_g + pc_base);
+                        if ((uint32_t)lane < nl && lane < 30) prefetch_l2(fr + 128 * lane);
                     }
                     if (lane == 30 && O.frames) prefetch_l2(O.frames + (size_t)(bb + 2) * A.fb);
                 }
@@ -1235,24 +1236,16 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const KArgs A) {
             const uint32_t c_base = __shfl_sync(0xffffffffu, bs.c_base, src);
             const uint32_t c_n = __shfl_sync(0xffffffffu, bs.c_n, src);
             if (O.tracks && A.stage_trk && s_trk == kSpilled) {
-                // straight from the fit records: the warp-batch's accepted store entries, in order
-                uint32_t n = 0;
-                for (uint32_t e0 = 0; e0 < c_n; e0 += 32) {
-                    const uint32_t e = e0 + lane;
-                    const bool acc = e < c_n && (A.code_g[c_base + e] & 1u);
-                    const unsigned m = __ballot_sync(0xffffffffu, acc);
-                    if (acc) {
-                        const uint32_t dst = g_trk + n + __popc(m & ((1u << lane) - 1u));
-                        if (dst < O.track_capacity) {
-                            const uint4* s4 = reinterpret_cast<const uint4*>(A.fit_g + c_base + e);
-                            uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst);
-                            d4[0] = s4[0];
-                            d4[1] = s4[1];
-                        } else {
-                            overflow = true;
-                        }
+                // straight from the front of the warp-batch's store segment (fit kernel:
+                // each frame's output tracks, frame order), one 16 B half per lane
+                for (uint32_t e = lane; e < 2 * c_n; e += 32) {
+                    const uint32_t dst = g_trk + (e >> 1);
+                    if (dst < O.track_capacity) {
+                        reinterpret_cast<uint4*>(O.tracks + dst)[e & 1u] =
+                            reinterpret_cast<const uint4*>(A.fit_g + c_base + (e >> 1))[e & 1u];
+                    } else {
+                        overflow = true;
                     }
-                    n += __popc(m);
                 }
             } else if (O.tracks && A.stage_trk) {
                 for (uint32_t e = lane; e < n_trk; e += 32) {
@@ -1344,83 +1337,301 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const KArgs A) {
 }
 
 // ------------------------------------------------------------ fit kernel ----
-// Split path, F: the triplet fit of every candidate in the store, one thread per
-// candidate (dense lanes; the frame's hits are read through L1/L2, consecutive
-// candidates share frames).  Record c = the accepted track, frame = kSpilled
-// when the fit rejects it (status != 0).  PAPER.md Sec. III-C, Eqs. 5-8.
-#ifndef M3E_FIT_MIN_BLOCKS
-#define M3E_FIT_MIN_BLOCKS 4
+// Split path, F + T: the triplet fit (Sec. IV-B, Alg. 3, Eqs. 5-8) of
+// every stored candidate and the per-frame track stage.  Each warp keeps a ring
+// of two warp-batch slots in shared memory: a slot holds the warp-batch's hits
+// and layer offsets, staged by TMA bulk copies (double-buffered: the next
+// warp-batch loads while the current one is fitted), and its store segment (the
+// candidates in frame order, L2-prefetched by a bulk prefetch).  Candidates are
+// fitted one lane per candidate, 32 at a time; a chunk runs on from the end of
+// the current warp-batch into the next one, so lanes stay dense although a
+// warp-batch holds ~50 candidates.  Accepted tracks are ranked per frame
+// (match_any on slot | frame; candidate order = Alg. 3's order); the first
+// max_tracks of each frame (the tracks a frame outputs, R3) are written
+// compacted to the front of their warp-batch's segment of fit_g, so each frame's
+// output tracks are contiguous there and the pack kernel copies them in one run.
+// Rejected candidates write nothing.  Once a warp-batch is consumed, one lane per
+// frame: track-overflow decision, the frame's track word, and frames with e+ e+
+// e- appended to the vertex list; its slot then takes the next warp-batch.
+constexpr int kFitHCap = 240;   // hits of a warp-batch staged (larger ones are read from HBM)
+
+struct __align__(16) FitSlot {
+    float hx[kFitHCap], hy[kFitHCap], hz[kFitHCap];
+    uint32_t offs[4 * kFB + 4];   // layer offsets of the warp-batch's frames (+ end)
+    uint32_t selw[kFB];           // its frames' selection words (cp.async)
+    uint64_t bar;
+    uint32_t b, f0, nf, winlo;    // warp-batch, its frames, first staged hit (0xFFFFFFFF: from HBM)
+    uint32_t sbase, n, t, nacc;   // store segment, its entries, entries consumed, output tracks written
+    int cnt[kFB], neg[kFB], pos[kFB];   // per frame: accepted, stored e-, stored e+
+};
+
+// descriptor words of the warp's next warp-batch, fetched ahead by cp.async:
+// {first hit, end hit, store segment, its entries}
+struct FitPre {
+    uint32_t w[4];
+};
+
+__device__ __forceinline__ void prefetch_bulk_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// lanes 0-3: start fetching the descriptor words of warp-batch b (none if b >= nbatch)
+__device__ __forceinline__ void fit_prefetch(const KArgs& A, FitPre& D, uint32_t b) {
+    const int lane = threadIdx.x & 31;
+    if (b < A.nbatch && lane < 4) {
+        const uint32_t f0 = b * (uint32_t)A.fb;
+        const uint32_t nf = min(A.F - f0, (uint32_t)A.fb);
+        const uint32_t* src = lane == 0 ? A.offsets + 4 * (size_t)f0
+                            : lane == 1 ? A.offsets + 4 * (size_t)(f0 + nf)
+                            : lane == 2 ? A.bsel + b : A.bcnt + b;
+        cp_async4(&D.w[lane], src);
+    }
+    cp_async_commit();
+}
+
+// whole warp: warp-batch b into slot S (every read of the slot's previous
+// warp-batch done); its descriptor is in D; then D starts fetching b_next
+__device__ __forceinline__ void fit_assign(const KArgs& A, FitSlot& S, FitPre& D, uint32_t b, uint32_t b_next) {
+    const int lane = threadIdx.x & 31;
+    cp_async_wait_all();
+    __syncwarp();
+    if (lane < kFB) {
+        S.cnt[lane] = 0;
+        S.neg[lane] = 0;
+        S.pos[lane] = 0;
+    }
+    const bool live = b < A.nbatch;
+    const uint32_t f0 = b * (uint32_t)A.fb;
+    const uint32_t nf = live ? min(A.F - f0, (uint32_t)A.fb) : 0u;
+    if ((uint32_t)lane < nf) cp_async4(&S.selw[lane], A.sel + f0 + lane);   // waited for by fit_frames
+    if (lane == 0) {
+        S.b = b;
+        S.t = 0;
+        S.nacc = 0;
+        S.f0 = f0;
+        S.nf = nf;
+        S.n = 0;
+        if (live) {
+            const uint32_t lo = D.w[0], hi = D.w[1], sb = D.w[2];
+            const uint32_t n = sb == kSpilled ? 0u : D.w[3];
+            const uint32_t wlo = lo & ~3u, whi = (hi + 3u) & ~3u;
+            const bool inw = whi - wlo <= (uint32_t)kFitHCap;
+            S.winlo = inw ? wlo : 0xFFFFFFFFu;
+            S.sbase = sb;
+            S.n = n;
+            S.offs[4 * nf] = hi;
+            if (n) prefetch_bulk_l2(A.cand_g + sb, n * (uint32_t)sizeof(uint4));
+            const uint32_t hb = inw ? (whi - wlo) * 4u : 0u, ob = nf * 16u;
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&S.bar, 3u * hb + ob);
+            bulk_g2s(S.offs, A.offsets + 4 * (size_t)f0, ob, &S.bar);
+            if (hb) {
+                bulk_g2s(S.hx, A.x + wlo, hb, &S.bar);
+                bulk_g2s(S.hy, A.y + wlo, hb, &S.bar);
+                bulk_g2s(S.hz, A.z + wlo, hb, &S.bar);
+            }
+        }
+    }
+    __syncwarp();   // D read, slot published
+    fit_prefetch(A, D, b_next);
+}
+
+// T: one lane per frame of the consumed warp-batch in slot S
+__device__ __forceinline__ void fit_frames(const KArgs& A, FitSlot& S) {
+    const int lane = threadIdx.x & 31;
+    const DevParams& P = A.P;
+    cp_async_wait_all();   // S.selw
+    __syncwarp();
+    const bool active = (uint32_t)lane < S.nf && S.sbase != kSpilled;
+    int c = 0, nneg = 0, npos = 0, reason = M3E_REASON_NONE;
+    if (active) {
+        c = S.cnt[lane];
+        nneg = S.neg[lane];
+        npos = S.pos[lane];
+        reason = (int)(S.selw[lane] >> 16);
+        if (reason == M3E_REASON_NONE && c > P.max_tracks) {
+            reason = M3E_REASON_TRACK_OVERFLOW;
+            nneg = 0;
+        }
+        A.fw[S.f0 + lane] = (uint32_t)min(c, P.max_tracks + 1) | ((uint32_t)min(nneg, 255) << 8) |
+                            ((uint32_t)reason << 24);
+    }
+    // the frame's first output track: segment base + prefix of the stored counts
+    const uint32_t stored = active ? (uint32_t)min(c, P.max_tracks) : 0u;
+    const uint32_t cs = S.sbase + warp_incl(stored) - stored;
+    // frames for the vertex stage (Alg. 4 needs two e+ and one e-)
+    const bool need = active && reason == M3E_REASON_NONE && npos >= 2 && nneg >= 1;
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (m) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(A.ticket + 9, (uint32_t)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (need) A.vlist[base + __popc(m & ((1u << lane) - 1u))] = make_uint2(S.f0 + (uint32_t)lane, cs);
+    }
+}
+
+#ifndef M3E_FIT_WARPS
+#define M3E_FIT_WARPS 8        // warps per CTA of the fit kernel
 #endif
-__global__ void __launch_bounds__(kThreads, M3E_FIT_MIN_BLOCKS) fit_kernel(const __grid_constant__ KArgs A) {
-    const unsigned long long filled = *reinterpret_cast<const volatile unsigned long long*>(A.ticket + 6);
-    const uint64_t n = filled < A.cand_cap ? filled : A.cand_cap;
-    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-    // (no prefetch of the next entry: since the entries locate the hits directly, the
-    // 4 registers it held cost more in spills than the load latency it hid)
-    for (uint64_t c = (uint64_t)blockIdx.x * kThreads + threadIdx.x; c < n; c += stride) {
-        const uint4 e = A.cand_g[c];
-        if (e.y == kSpilled) continue;
-        // the entry locates the triplet's hits directly ({first hit of the frame,
-        // frame, offsets of h1 | h2 << 16, offset of h0}): their loads do not wait
-        // for the frame's layer offsets, which only the layer-3 search needs
-        const uint32_t f = e.y;
-        const float* fx = A.x + e.x;
-        const float* fy = A.y + e.x;
-        const float* fz = A.z + e.x;
-        const uint32_t o0 = e.w, o1 = e.z & 0xFFFFu, o2 = e.z >> 16;
-        const float3 h0 = make_float3(fx[o0], fy[o0], fz[o0]);
-        const float3 h1 = make_float3(fx[o1], fy[o1], fz[o1]);
-        const float3 h2 = make_float3(fx[o2], fy[o2], fz[o2]);
-        const uint4 o4 = *reinterpret_cast<const uint4*>(A.offsets + 4 * (size_t)f);
-        const uint32_t o5 = A.offsets[4 * (size_t)f + 4];
-        Frame F;
-        F.x = fx;
-        F.y = fy;
-        F.z = fz;
-        F.s[0] = 0;
-        F.s[1] = (int)(o4.y - o4.x);
-        F.s[2] = (int)(o4.z - o4.x);
-        F.s[3] = (int)(o4.w - o4.x);
-        F.n[0] = F.s[1];
-        F.n[1] = (int)(o4.z - o4.y);
-        F.n[2] = (int)(o4.w - o4.z);
-        F.n[3] = (int)(o5 - o4.w);
-        // r_tc of the selection (Eq. 5, same fp32 code as the selection's)
-        const float rtc = circle_radius(h0, h1, h2);
-        const FitOut o = fit_candidate_h(A.P, F, h0, h1, h2, rtc);
-        m3e_track t;
-        t.frame = o.status == 0 ? f : kSpilled;
-        t.hit[0] = (uint16_t)o0;
-        t.hit[1] = (uint16_t)(o1 - (uint32_t)F.s[1]);
-        t.hit[2] = (uint16_t)(o2 - (uint32_t)F.s[2]);
-        t.hit[3] = (uint16_t)o.hit3;
-        t.kappa = o.kappa;
-        t.chi2 = o.chi2;
-        t.cos_theta01 = o.cth01;
-        t.cx = o.cx;
-        t.cy = o.cy;
-        A.fit_g[c] = t;
-        // code byte for the finish kernel: frame within the warp-batch << 3 |
-        // accepted | kappa < 0 | kappa > 0
+#ifndef M3E_FIT_MIN_BLOCKS
+#define M3E_FIT_MIN_BLOCKS 3   // 80 registers (no spills), 24 warps per SM
+#endif
+constexpr int kFitWarps = M3E_FIT_WARPS;
+__global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel(const __grid_constant__ KArgs A) {
+    extern __shared__ __align__(16) uint8_t fit_smem_raw[];
+    FitSlot* R = reinterpret_cast<FitSlot*>(fit_smem_raw) + 2 * (threadIdx.x >> 5);   // the warp's two slots
+    FitPre& D = reinterpret_cast<FitPre*>(fit_smem_raw + 2 * kFitWarps * sizeof(FitSlot))[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const DevParams& P = A.P;
+    // warp-batches claimed with an atomic ticket, pipelined so that no claim or
+    // descriptor load is waited for: `claim` (lane 0) is the warp-batch after next,
+    // bq the next one, whose descriptor D is being fetched
+    if (lane == 0) {
+        mbar_init(&R[0].bar, 1);
+        mbar_init(&R[1].bar, 1);
+        fence_mbar_init();
+    }
+    uint32_t claim = 0;
+    if (lane == 0) claim = atomicAdd(A.ticket + 8, 1u);
+    uint32_t bq = __shfl_sync(0xffffffffu, claim, 0);
+    fit_prefetch(A, D, bq);
+    if (lane == 0) claim = atomicAdd(A.ticket + 8, 1u);
+    auto refill = [&](FitSlot& S) {
+        const uint32_t bn = __shfl_sync(0xffffffffu, claim, 0);
+        fit_assign(A, S, D, bq, bn);
+        bq = bn;
+        if (lane == 0) claim = atomicAdd(A.ticket + 8, 1u);
+    };
+    refill(R[0]);
+    refill(R[1]);
+    uint32_t ph = 0u;      // mbarrier parity of slot s: bit s
+    uint32_t ready = 0u;   // slot s loaded (waited): bit s
+    int cur = 0;
+    for (;;) {
+        FitSlot& C = R[cur];
+        FitSlot& X = R[cur ^ 1];
+        if (C.b >= A.nbatch) break;   // claims are in order: X is past the end too
+        if (!((ready >> cur) & 1u)) {
+            mbar_wait(&C.bar, (ph >> cur) & 1u);
+            ph ^= 1u << cur;
+            ready |= 1u << cur;
+        }
+        const uint32_t left = C.n - C.t;
+        const uint32_t xleft = X.n - X.t;
+        // the chunk runs on into the next warp-batch when this one has < 32 left
+        const bool useX = left < 32u && xleft > 0u;
+        if (useX && !((ready >> (cur ^ 1)) & 1u)) {
+            mbar_wait(&X.bar, (ph >> (cur ^ 1)) & 1u);
+            ph ^= 1u << (cur ^ 1);
+            ready |= 1u << (cur ^ 1);
+        }
+        __syncwarp();
+        const bool inX = (uint32_t)lane >= left;
+        const uint32_t idx = inX ? X.t + ((uint32_t)lane - left) : C.t + (uint32_t)lane;
+        const bool valid = inX ? (useX && (uint32_t)lane - left < xleft) : true;
+        FitSlot& L = inX ? X : C;
+        int key = 64 + lane;   // slot | frame (invalid lanes: a key of their own)
+        int j = 0;
+        FitOut o;
+        o.status = 7;
+        o.hit3 = 0;
+        uint4 e = make_uint4(0u, 0u, 0u, 0u);
+        if (valid) {
+            e = A.cand_g[L.sbase + idx];
+            j = (int)(e.y - L.f0);
+            key = (inX ? 16 : 0) + j;
+            // the entry locates the triplet's hits: {first hit of the frame, frame,
+            // offsets of h1 | h2 << 16, offset of h0} (inside the frame)
+            Frame F;
+            const uint32_t wlo = L.winlo;
+            if (wlo != 0xFFFFFFFFu) {
+                const uint32_t d = e.x - wlo;
+                F.x = L.hx + d;
+                F.y = L.hy + d;
+                F.z = L.hz + d;
+            } else {
+                F.x = A.x + e.x;
+                F.y = A.y + e.x;
+                F.z = A.z + e.x;
+            }
+            const uint32_t* of = L.offs + 4 * j;
+            F.s[0] = 0;
+            F.s[1] = (int)(of[1] - of[0]);
+            F.s[2] = (int)(of[2] - of[0]);
+            F.s[3] = (int)(of[3] - of[0]);
+            F.n[0] = F.s[1];
+            F.n[1] = F.s[2] - F.s[1];
+            F.n[2] = F.s[3] - F.s[2];
+            F.n[3] = (int)(of[4] - of[3]);
+            const uint32_t o0 = e.w, o1 = e.z & 0xFFFFu, o2 = e.z >> 16;
+            const float3 h0 = make_float3(F.x[o0], F.y[o0], F.z[o0]);
+            const float3 h1 = make_float3(F.x[o1], F.y[o1], F.z[o1]);
+            const float3 h2 = make_float3(F.x[o2], F.y[o2], F.z[o2]);
+            // r_tc of the selection (Eq. 5, same fp32 code as the selection's)
+            o = fit_candidate_h(P, F, h0, h1, h2, circle_radius(h0, h1, h2));
+            e.z = (o1 - (uint32_t)F.s[1]) | ((o2 - (uint32_t)F.s[2]) << 16);   // layer-local h1 | h2
+        }
         const bool acc = o.status == 0;
-        const uint32_t jb = f - (f / (uint32_t)A.fb) * (uint32_t)A.fb;   // frame within its warp-batch
-        A.code_g[c] = (uint8_t)((jb << 3) | (acc ? 1u : 0u) | (acc && o.kappa < 0.0f ? 2u : 0u) |
-                                (acc && o.kappa > 0.0f ? 4u : 0u));
+        // per-frame rank among accepted candidates (candidate order); the first
+        // max_tracks are the frame's output tracks (R3)
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const unsigned ma = __ballot_sync(0xffffffffu, acc);
+        const int before = valid ? L.cnt[j] : 0;
+        const int rank = before + __popc(ma & grp & lt);
+        const bool st = acc && rank < P.max_tracks;
+        const unsigned ms = __ballot_sync(0xffffffffu, st);
+        const unsigned mx = __ballot_sync(0xffffffffu, valid && inX);
+        const unsigned mn = __ballot_sync(0xffffffffu, st && o.kappa < 0.0f);
+        const unsigned mp = __ballot_sync(0xffffffffu, st && o.kappa > 0.0f);
+        if (st) {
+            m3e_track tr;
+            tr.frame = e.y;
+            tr.hit[0] = (uint16_t)e.w;
+            tr.hit[1] = (uint16_t)(e.z & 0xFFFFu);
+            tr.hit[2] = (uint16_t)(e.z >> 16);
+            tr.hit[3] = (uint16_t)o.hit3;
+            tr.kappa = o.kappa;
+            tr.chi2 = o.chi2;
+            tr.cos_theta01 = o.cth01;
+            tr.cx = o.cx;
+            tr.cy = o.cy;
+            A.fit_g[L.sbase + L.nacc + __popc(ms & (inX ? mx : ~mx) & lt)] = tr;
+        }
+        __syncwarp();
+        if (valid && lane == __ffs(grp) - 1) {
+            L.cnt[j] = before + __popc(ma & grp);
+            L.neg[j] += __popc(mn & grp);
+            L.pos[j] += __popc(mp & grp);
+        }
+        if (lane == 0) {
+            C.nacc += __popc(ms & ~mx);
+            C.t += min(left, 32u);
+            X.nacc += __popc(ms & mx);
+            X.t += __popc(mx);
+        }
+        __syncwarp();
+        if (C.t == C.n) {   // warp-batch consumed: its frames, then the slot takes the next one
+            fit_frames(A, C);
+            refill(C);
+            ready &= ~(1u << cur);
+            cur ^= 1;
+        }
     }
 }
 
 // ------------------------------------------- tracks / vertex / finish kernels ----
-// Split path, T + V + O for the warp-batches fitted by fit_kernel, as three
-// kernels so that each has no out-of-line call (no ABI register saves in its
-// loop) and its hot code in the instruction cache:
-//   tracks_kernel  T: one warp takes G = 32 / fb consecutive warp-batches at a
-//                  time, one lane per frame: accepted tracks and charges from the
-//                  code bytes, track-overflow decision; frames with e+ e+ e-
-//                  candidates are listed for the vertex stage;
+// Split path, V + O for the warp-batches fitted by fit_kernel (which also ran
+// the track stage T), as kernels without out-of-line calls in their loops and
+// with their hot code in the instruction cache:
 //   vertex_kernel  V: one warp per listed frame, fp64 (Alg. 4);
 //   finish_kernel  O: frame records in place (warp-batch relative offsets),
-//                  kept-frame records and the tracks of warp-batches with a
-//                  track-overflow frame staged, BatchStat per warp-batch.
+//                  kept-frame records, BatchStat per warp-batch.
 // Results are identical to the fused kernel's stages T, V and O.
 
 // group of G warp-batches of one warp, lane = frame (shared by T and O)
@@ -1479,114 +1690,6 @@ __device__ __forceinline__ Group make_group(const KArgs& A, uint32_t g, const Gr
     return q;
 }
 
-// One pass over the code bytes of the group's warp-batches (coalesced, one lane
-// per candidate, candidate order): per frame lane, cnt = accepted tracks so far.
-// STAGE = false: also counts the stored tracks' charges into neg / pos.
-// STAGE = true: copies the first lim[j] accepted fit records of frame lane j to
-// stage_trk[dst[j] + rank] (warp-batches flagged in `which` only).
-template <bool STAGE>
-__device__ __forceinline__ bool code_pass(const KArgs& A, const Group& q, int fb, int G, int* cnt, int* neg, int* pos,
-                                          unsigned which) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    bool overflow = false;
-    for (int qq = 0; qq < G; ++qq) {
-        const int ql = qq * fb;
-        if (STAGE && !((which >> ql) & 1u)) continue;
-        const uint32_t qb = __shfl_sync(0xffffffffu, q.gb, ql);
-        const uint32_t qn = __shfl_sync(0xffffffffu, q.cin, min(ql + fb, 32) - 1) - __shfl_sync(0xffffffffu, q.cex, ql);
-        if (qb == kSpilled || q.g * (uint32_t)G + (uint32_t)qq >= A.nbatch) continue;
-        for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
-            const uint32_t e = e0 + lane;
-            const bool valid = e < qn;
-            const uint32_t code = valid ? A.code_g[qb + e] : 0u;
-            const int j = valid ? ql + (int)(code >> 3) : 32;
-            const unsigned grp = __match_any_sync(0xffffffffu, j);
-            const unsigned ma = __ballot_sync(0xffffffffu, code & 1u);
-            const int before = valid ? cnt[j] : 0;
-            const int rank = before + __popc(ma & grp & lt_mask);
-            if constexpr (STAGE) {
-                if ((code & 1u) && rank < neg[j]) {
-                    const uint32_t dst = (uint32_t)pos[j] + (uint32_t)rank;
-                    if (dst < A.stage_trk_cap) {
-                        const uint4* s4 = reinterpret_cast<const uint4*>(A.fit_g + qb + e);
-                        uint4* d4 = reinterpret_cast<uint4*>(A.stage_trk + dst);
-                        d4[0] = s4[0];
-                        d4[1] = s4[1];
-                    } else {
-                        overflow = true;
-                    }
-                }
-                __syncwarp();
-                if (valid && lane == __ffs(grp) - 1) cnt[j] = before + __popc(ma & grp);
-            } else {
-                const bool st = (code & 1u) && rank < A.P.max_tracks;   // stored track
-                const unsigned mn = __ballot_sync(0xffffffffu, st && (code & 2u));
-                const unsigned mp = __ballot_sync(0xffffffffu, st && (code & 4u));
-                __syncwarp();
-                if (valid && lane == __ffs(grp) - 1) {
-                    cnt[j] = before + __popc(ma & grp);
-                    neg[j] += __popc(mn & grp);
-                    pos[j] += __popc(mp & grp);
-                }
-            }
-            __syncwarp();
-        }
-    }
-    return overflow;
-}
-
-#ifndef M3E_TRACKS_MIN_BLOCKS
-#define M3E_TRACKS_MIN_BLOCKS 6
-#endif
-__global__ void __launch_bounds__(kThreads, M3E_TRACKS_MIN_BLOCKS) tracks_kernel(const __grid_constant__ KArgs A) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const int fb = A.fb, G = 32 / fb, bl = lane / fb, fl = bl * fb;
-    const uint32_t ngroups = (A.nbatch + G - 1) / G;
-    // static round-robin over groups, the next group's words fetched ahead
-    const uint32_t nw = gridDim.x * kWarps;
-    uint32_t g = blockIdx.x * kWarps + warp;
-    GroupRaw rn = fetch_group<false>(A, g, fb, G, bl, fl);
-    for (; g < ngroups; g += nw) {
-        const Group q = make_group(A, g, rn, fb, G, bl, fl);
-        rn = fetch_group<false>(A, g + nw, fb, G, bl, fl);
-        // accepted tracks and charges of the frame from its code bytes: one lane per
-        // frame walks its own store range (candidate order; charges of the first
-        // max_tracks accepted, the stored tracks)
-        const uint32_t cs = q.gb + q.cex - __shfl_sync(0xffffffffu, q.cex, fl);
-        int c = 0, nneg = 0, npos = 0;
-        if (q.active) {
-            const uint8_t* cb = A.code_g + cs;
-            for (uint32_t k = 0; k < q.nst; ++k) {
-                const int code = cb[k];
-                const int acc = code & 1;
-                const int st = acc & (c < A.P.max_tracks ? 1 : 0);
-                nneg += st & (code >> 1);
-                npos += st & (code >> 2);
-                c += acc;
-            }
-        }
-        int reason = q.reason;
-        if (q.active && reason == M3E_REASON_NONE && c > A.P.max_tracks) {
-            reason = M3E_REASON_TRACK_OVERFLOW;
-            nneg = 0;
-        }
-        const int ntrk = min(c, A.P.max_tracks + 1);
-        if (q.active) A.fw[q.f] = (uint32_t)ntrk | ((uint32_t)min(nneg, 255) << 8) | ((uint32_t)reason << 24);
-        // frames for the vertex stage (Alg. 4 needs two e+ and one e-)
-        const bool need = q.active && reason == M3E_REASON_NONE && npos >= 2 && nneg >= 1;
-        const unsigned m = __ballot_sync(0xffffffffu, need);
-        if (m) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(A.ticket + 9, (uint32_t)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (need) A.vlist[base + __popc(m & lt_mask)] = make_uint2(q.f, cs);
-        }
-        __syncwarp();
-    }
-}
-
 // V, three kernels over the frames the track stage listed (Alg. 4,
 // Sec. IV-C; same arithmetic and order as vertex_frame):
 //   vertex_kernel  one warp per listed frame: its first max_tracks accepted tracks
@@ -1630,7 +1733,8 @@ __global__ void __launch_bounds__(kThreads, 4) vertex_kernel(const __grid_consta
     for (uint32_t k = (uint32_t)gwarp; k < n; k += gridDim.x * kWarps) {
         const uint2 e = A.vlist[k];
         const uint32_t f = e.x, cs = e.y;
-        const uint32_t nj = A.sel[f] & 0xFFFFu;
+        // the frame's output tracks, contiguous from cs (fit kernel)
+        const uint32_t nj = min(A.fw[f] & 0xFFu, (uint32_t)P.max_tracks);
         // accepted tracks (track index = rank among the frame's accepted entries,
         // the first max_tracks only) split by charge, in track order
         int nt = 0, npos = 0, nneg = 0;
@@ -1811,7 +1915,6 @@ __global__ void __launch_bounds__(kThreads) vpost_kernel(const __grid_constant__
 
 struct FinishSmem {
     uint32_t acc[kWarps][12];
-    int cnt[kWarps][33], lim[kWarps][33], dst[kWarps][33];   // per frame lane (+1 for invalid lanes)
 };
 
 #ifndef M3E_FINISH_MIN_BLOCKS
@@ -1853,20 +1956,10 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
         const uint32_t e_trk = i_trk - o_trk, e_kept = i_kept - o_kept, e_hits = i_hits - o_hits;
         const uint32_t t_trk = __shfl_sync(0xffffffffu, i_trk, 31), t_kept = __shfl_sync(0xffffffffu, i_kept, 31);
         const uint32_t t_hits = __shfl_sync(0xffffffffu, i_hits, 31);
-        // a warp-batch without track-overflow frame outputs exactly its accepted
-        // store entries: the pack kernel copies them from the fit records; only
-        // the others stage their (capped) tracks here
-        const unsigned m_tov = __ballot_sync(0xffffffffu, q.active && reason == M3E_REASON_TRACK_OVERFLOW);
-        const bool staged = ((m_tov >> fl) & ((1u << fb) - 1u)) != 0u;
-        const uint32_t so_trk = staged ? o_trk : 0u;
-        const uint32_t si_trk = warp_incl(so_trk), se_trk = si_trk - so_trk;
-        const uint32_t st_trk = __shfl_sync(0xffffffffu, si_trk, 31);
-        uint32_t s_trk = 0, s_kept = 0;
-        if (lane == 0) {
-            if (st_trk && A.stage_trk) s_trk = atomicAdd(A.ticket + 1, st_trk);
-            if (t_kept) s_kept = atomicAdd(A.ticket + 2, t_kept);
-        }
-        s_trk = __shfl_sync(0xffffffffu, s_trk, 0);
+        // a warp-batch's output tracks (each frame's first max_tracks accepted) are
+        // the front of its store segment (fit kernel): the pack kernel copies them
+        uint32_t s_kept = 0;
+        if (lane == 0 && t_kept) s_kept = atomicAdd(A.ticket + 2, t_kept);
         s_kept = __shfl_sync(0xffffffffu, s_kept, 0);
         const uint32_t b_trk = __shfl_sync(0xffffffffu, e_trk, fl), b_kept = __shfl_sync(0xffffffffu, e_kept, fl);
         const uint32_t b_hits = __shfl_sync(0xffffffffu, e_hits, fl);
@@ -1901,34 +1994,21 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
                 }
             }
         }
-        // staged warp-batches: the first o_trk accepted tracks of each frame, in
-        // candidate order (a pass over their code bytes)
-        if (A.stage_trk && st_trk) {
-            S.cnt[warp][lane] = 0;
-            S.dst[warp][lane] = (int)(s_trk + se_trk);   // staging slot of the frame's first track
-            S.lim[warp][lane] = (int)so_trk;
-            __syncwarp();
-            const unsigned which = __ballot_sync(0xffffffffu, staged);
-            overflow |= code_pass<true>(A, q, fb, G, S.cnt[warp], S.lim[warp], S.dst[warp], which);
-        }
         // BatchStat of each fitted warp-batch (written by its first lane)
         const int ll = fl + fb - 1;   // last lane of the warp-batch (frames past F are inactive: 0)
         const uint32_t l_trk = __shfl_sync(0xffffffffu, i_trk, ll & 31);
         const uint32_t l_kept = __shfl_sync(0xffffffffu, i_kept, ll & 31);
         const uint32_t l_hits = __shfl_sync(0xffffffffu, i_hits, ll & 31);
-        const uint32_t l_cand = __shfl_sync(0xffffffffu, q.cin, ll & 31);
-        const uint32_t b_cand = __shfl_sync(0xffffffffu, q.cex, fl);
-        const uint32_t b_strk = __shfl_sync(0xffffffffu, se_trk, fl);
         if (q.inb && q.gb != kSpilled && lane == fl) {
             BatchStat bs;
             bs.n_trk = l_trk - b_trk;
             bs.n_kept = l_kept - b_kept;
             bs.n_hits = l_hits - b_hits;
-            bs.s_trk = staged ? s_trk + b_strk : kSpilled;   // kSpilled: tracks = accepted store entries
+            bs.s_trk = kSpilled;   // kSpilled: its tracks are the front of its store segment
             bs.s_kept = s_kept + b_kept;
             bs.nf = min(A.F - q.b * (uint32_t)fb, (uint32_t)fb);
             bs.c_base = q.gb;
-            bs.c_n = l_cand - b_cand;
+            bs.c_n = bs.n_trk;
             A.bstat[q.b] = bs;
         }
         // run summary (per-warp counters in shared memory)
@@ -1953,17 +2033,6 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
 cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s) {
     finish_kernel<<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();
-}
-
-cudaError_t launch_tracks(const KArgs& a, int grid, cudaStream_t s) {
-    tracks_kernel<<<grid, kThreads, 0, s>>>(a);
-    return cudaGetLastError();
-}
-
-int tracks_blocks_per_sm() {
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tracks_kernel, kThreads, 0) != cudaSuccess) return 1;
-    return n > 0 ? n : 1;
 }
 
 cudaError_t launch_vertex(const KArgs& a, int grid, int sms, cudaStream_t s) {
@@ -1994,13 +2063,19 @@ int finish_blocks_per_sm() {
 }
 
 cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s) {
-    fit_kernel<<<grid, kThreads, 0, s>>>(a);
+    const size_t smem = 2 * kFitWarps * sizeof(FitSlot) + kFitWarps * sizeof(FitPre);
+    cudaError_t e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fit_kernel<<<grid, 32 * kFitWarps, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 int fit_blocks_per_sm() {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fit_kernel, kThreads, 0) != cudaSuccess) return 1;
+    const size_t smem = 2 * kFitWarps * sizeof(FitSlot) + kFitWarps * sizeof(FitPre);
+    if (cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fit_kernel, 32 * kFitWarps, smem) != cudaSuccess) return 1;
     return n > 0 ? n : 1;
 }
 

@@ -39,9 +39,9 @@ constexpr int kPackTile = 256;       // warp-batches per CTA of the pack kernel 
 struct BatchStat {
     uint32_t n_trk, n_kept, n_hits;  // tracks, kept frames, hits of kept frames
     uint32_t s_trk, s_kept;          // staging offsets of its tracks / kept-frame records; s_trk =
-                                     // kSpilled: its tracks are its accepted store entries
+                                     // kSpilled: its tracks are the front of its store segment
     uint32_t nf;                     // frames in the warp-batch
-    uint32_t c_base, c_n;            // its store entries (split path)
+    uint32_t c_base, c_n;            // its store segment and output tracks there (split path)
 };
 
 // kept-frame record staged by the filter kernel (64 B)
@@ -64,7 +64,7 @@ struct KArgs {
     uint32_t* ticket;      // counters (zeroed before the launch): [0] select warp-batch ticket, [1] staged
                            // tracks, [2] staged kept frames, [3] pack-kernel tile ticket, [4] filter
                            // warp-batch ticket, [5] spilled warp-batches, [6..7] candidate-store fill (u64),
-                           // [8] tracks-kernel group ticket, [9] vertex-list fill, [10] finish-kernel
+                           // [8] fit-kernel unit ticket, [9] vertex-list fill, [10] finish-kernel
                            // group ticket, [11] triple-list fill
     uint32_t* bticket;     // this launch's warp-batch ticket (ticket + 0 or ticket + 4)
     // candidate store of the split path (kModeSelectC writes, fit_kernel / finish_kernel read)
@@ -73,13 +73,12 @@ struct KArgs {
     uint4* cand_g;         // {first hit of the frame, frame, offsets of h1 | h2 << 16 and of h0 inside the
                            // frame}, warp-batch contiguous, frame order; frame = kSpilled marks an unused
                            // entry
-    m3e_track* fit_g;      // fit of store entry c (fit_kernel); frame = kSpilled: not accepted
-    uint8_t* code_g;       // code of store entry c: frame within its warp-batch << 3 | accepted |
-                           // kappa < 0 (2) | kappa > 0 (4)
+    m3e_track* fit_g;      // fit_kernel: each warp-batch's output tracks (every frame's first
+                           // max_tracks accepted, frame order) compacted to the front of its segment
     uint64_t cand_cap;     // entries of cand_g (< 2^32)
     uint32_t* sel;         // [F] per frame: n_cand | reason << 16
     uint32_t* fw;          // [F] per frame after the track stage: n_tracks | n_neg << 8 | n_combs << 16 |
-                           // reason << 24 (tracks_kernel writes, vertex_kernel updates, finish_kernel reads)
+                           // reason << 24 (fit_kernel writes, vertex_kernel updates, finish_kernel reads)
     uint32_t* vk;          // [F] vertex_kernel: list position of a frame's vertex (reason VERTEX only)
     uint2* vlist;          // frames for the vertex stage {frame, first store entry}, count in ticket[9]
     m3e_vertex* vrec;      // vertex of vlist entry k
@@ -89,6 +88,7 @@ struct KArgs {
     struct VRes* tres;     // phase-2 result of each listed triple
     uint64_t tri_cap;      // entries of tri / tres
     uint32_t* bsel;        // [nbatch] first store entry of the warp-batch, or kSpilled
+    uint32_t* bcnt;        // [nbatch] its store entries
     uint4* status;         // pack-kernel decoupled look-back, one 16 B word per tile
     uint32_t epoch;        // launch epoch tag of the status words (never 0)
     BatchStat* bstat;      // [nbatch]
@@ -125,8 +125,6 @@ cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s);
 int fit_blocks_per_sm();
 cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s);
 int finish_blocks_per_sm();
-cudaError_t launch_tracks(const KArgs& a, int grid, cudaStream_t s);
-int tracks_blocks_per_sm();
 cudaError_t launch_vertex(const KArgs& a, int grid, int sms, cudaStream_t s);
 int vertex_blocks_per_sm();
 int blocks_per_sm(int mode, bool big);

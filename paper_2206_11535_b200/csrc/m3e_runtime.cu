@@ -60,8 +60,7 @@ struct Workspace {
     int pair_warps = 0;
     void* vscratch = nullptr;           // vertex-stage scratch, kVScratchBytes per warp
     uint4* cand_g = nullptr;            // candidate store of the split path
-    m3e_track* fit_g = nullptr;         // fit records of the store entries
-    uint8_t* code_g = nullptr;          // their code bytes
+    m3e_track* fit_g = nullptr;         // output tracks, compacted per store segment (fit kernel)
     size_t cand_n = 0;
     uint32_t* sel = nullptr;            // per-frame selection words of the split path
     uint32_t* fw = nullptr;             // per-frame track/vertex words of the split path
@@ -74,8 +73,10 @@ struct Workspace {
     size_t tri_n = 0;
     size_t sel_n = 0;
     uint32_t* bsel = nullptr;           // per-warp-batch store offsets of the split path
+    uint32_t* bcnt = nullptr;           // per-warp-batch store entries
     uint32_t* spill = nullptr;          // warp-batches the store could not take
     size_t bsel_n = 0;
+    bool status_fresh = false;          // status words allocated, not yet zeroed
     size_t bytes = 0;
 };
 
@@ -123,7 +124,6 @@ namespace {
 void free_ws(Workspace& w) {
     cudaFree(w.cand_g);
     cudaFree(w.fit_g);
-    cudaFree(w.code_g);
     cudaFree(w.sel);
     cudaFree(w.fw);
     cudaFree(w.vk);
@@ -133,6 +133,7 @@ void free_ws(Workspace& w) {
     cudaFree(w.tri);
     cudaFree(w.tres);
     cudaFree(w.bsel);
+    cudaFree(w.bcnt);
     cudaFree(w.spill);
     cudaFree(w.pair_scratch);
     cudaFree(w.vscratch);
@@ -243,8 +244,8 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
         w.bytes -= w.status_n * sizeof(uint4);
         const size_t n = std::max<size_t>(ntiles, 1024);
         CK(cudaMalloc(&w.status, n * sizeof(uint4)));
-        CK(cudaMemset(w.status, 0, n * sizeof(uint4)));
         w.status_n = n;
+        w.status_fresh = true;   // zeroed on the launch stream before its first use (run_mode)
         w.bytes += n * sizeof(uint4);
         w.epoch = 0;
     }
@@ -289,14 +290,12 @@ int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame, 
     if (w.cand_n < nc) {
         cudaFree(w.cand_g);
         cudaFree(w.fit_g);
-        cudaFree(w.code_g);
-        w.bytes -= w.cand_n * (sizeof(uint4) + sizeof(m3e_track) + 1);
+        w.bytes -= w.cand_n * (sizeof(uint4) + sizeof(m3e_track));
         w.cand_n = 0;
         CK(cudaMalloc(&w.cand_g, nc * sizeof(uint4)));
         CK(cudaMalloc(&w.fit_g, nc * sizeof(m3e_track)));
-        CK(cudaMalloc(&w.code_g, nc));
         w.cand_n = nc;
-        w.bytes += nc * (sizeof(uint4) + sizeof(m3e_track) + 1);
+        w.bytes += nc * (sizeof(uint4) + sizeof(m3e_track));
     }
     if (w.sel_n < F) {
         constexpr size_t per = 3 * sizeof(uint32_t) + 2 * sizeof(uint2) + sizeof(m3e_vertex);
@@ -326,13 +325,15 @@ int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame, 
     }
     if (w.bsel_n < nbatch) {
         cudaFree(w.bsel);
+        cudaFree(w.bcnt);
         cudaFree(w.spill);
-        w.bytes -= 2 * w.bsel_n * sizeof(uint32_t);
+        w.bytes -= 3 * w.bsel_n * sizeof(uint32_t);
         w.bsel_n = 0;
         CK(cudaMalloc(&w.bsel, nbatch * sizeof(uint32_t)));
+        CK(cudaMalloc(&w.bcnt, nbatch * sizeof(uint32_t)));
         CK(cudaMalloc(&w.spill, nbatch * sizeof(uint32_t)));
         w.bsel_n = nbatch;
-        w.bytes += 2 * nbatch * sizeof(uint32_t);
+        w.bytes += 3 * nbatch * sizeof(uint32_t);
     }
     return M3E_OK;
 }
@@ -392,7 +393,6 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     const int sgrid = split ? (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * blocks_per_sm(kModeSelectC, big))
                             : 0;
     const int fgrid = split ? ctx->sms * finish_blocks_per_sm() : 0;
-    const int tgrid = split ? ctx->sms * tracks_blocks_per_sm() : 0;
     const int vgrid = split ? ctx->sms * vertex_blocks_per_sm() : 0;   // its warps own vscratch / pool slots
     rc = ensure_ws(ctx, w, nbatch, p, fb, std::max(std::max(grid, sgrid), vgrid));
     if (rc) return rc;
@@ -426,6 +426,10 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         a.stage_kept_cap = a.out.kept_capacity;
     }
     CK(cudaMemsetAsync(w.ticket, 0, 16 * sizeof(uint32_t), s));
+    if (w.status_fresh) {   // look-back words: no stale epoch tag may survive from recycled memory
+        CK(cudaMemsetAsync(w.status, 0, w.status_n * sizeof(uint4), s));
+        w.status_fresh = false;
+    }
     if (a.out.summary) CK(cudaMemsetAsync(a.out.summary, 0, sizeof(m3e_summary), s));
     const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + kNEv <= ctx->tev.size();
     cudaEvent_t* ev = tm ? &ctx->tev[ctx->tev_used] : nullptr;
@@ -436,15 +440,16 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         sa.cand_cap = std::min<uint64_t>(w.cand_n, std::max<uint64_t>(cand_pf * F, 1u << 10));
         sa.sel = w.sel;
         sa.bsel = w.bsel;
+        sa.bcnt = w.bcnt;
         sa.spill_out = w.spill;
         CK(launch_filter(kModeSelectC, big, sa, sgrid, s));
         if (tm) CK(cudaEventRecord(ev[1], s));
         a.cand_g = w.cand_g;
         a.fit_g = w.fit_g;
-        a.code_g = w.code_g;
         a.cand_cap = sa.cand_cap;
         a.sel = w.sel;
         a.bsel = w.bsel;
+        a.bcnt = w.bcnt;
         a.fw = w.fw;
         a.vk = w.vk;
         a.vlist = w.vlist;
@@ -453,9 +458,8 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         a.tri = w.tri;
         a.tres = reinterpret_cast<VRes*>(w.tres);
         a.tri_cap = ctx->tri_cap ? std::min<uint64_t>(ctx->tri_cap, w.tri_n) : w.tri_n;
-        CK(launch_fit(a, ctx->sms * fit_blocks_per_sm(), s));
+        CK(launch_fit(a, ctx->sms * fit_blocks_per_sm(), s));   // F + T (track stage)
         if (tm) CK(cudaEventRecord(ev[2], s));
-        CK(launch_tracks(a, tgrid, s));
         if (tm) CK(cudaEventRecord(ev[3], s));
         CK(launch_vertex(a, vgrid, ctx->sms, s));
         if (tm) CK(cudaEventRecord(ev[4], s));
