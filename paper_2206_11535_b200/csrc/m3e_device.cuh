@@ -423,9 +423,13 @@ __device__ __forceinline__ int pair_list(const Frame& F, int la, int lb, float i
 // on full warps (same survivor set and order as select_frame_warp, R3 overflow).
 // Returns -1 if a list exceeds kPairCapG (caller falls back to select_frame_warp).
 // Out of line: phase-I frames never take it, so its code stays out of the I-cache.
-static __device__ __noinline__ int select_frame_big(const DevParams* __restrict__ Pp, const Frame& F, uint32_t* q,
+static __device__ __noinline__ int select_frame_big(const DevParams* __restrict__ Pp, const Frame& Fin, uint32_t* q,
                                                     uint32_t* X, CandSink sink, int cap) {
     const DevParams& P = *Pp;
+    // the frame view in registers: the caller's copy is in local memory (its address
+    // is passed), and the list stores below could alias it, forcing a reload of
+    // every field on every access
+    const Frame F = Fin;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int n1 = F.n[1];
@@ -761,13 +765,8 @@ __device__ __forceinline__ VTrk make_vtrk(const DevParams& P, const m3e_track& t
 }
 
 // signed turning angle from point (px,py) on the track circle to the layer-0 hit,
-// in the direction of motion, wrapped to (-pi, pi] (R12)
-// (one atan2 of the cross and dot products of the two radii; out of line to keep
-// the code small)
-static __device__ __noinline__ double turn_to_h0(const VTrk& t, double px, double py) {
-    const double ax = t.h0x - t.cx, ay = t.h0y - t.cy, bx = px - t.cx, by = py - t.cy;
-    return t.q * atan2(ax * by - ay * bx, ax * bx + ay * by);
-}
+// in the direction of motion, wrapped to (-pi, pi] (R12): one atan2 of the cross
+// and dot products of the two radii (turn_to_h0_inl below)
 
 // circle-circle intersections; 0 or 2 points {x0,y0,x1,y1}
 __device__ __forceinline__ int intersect(const VTrk& A, const VTrk& B, double o[4]) {
@@ -801,89 +800,114 @@ struct VResult {
     double x, y, z, chi2, tdist, ptot;
 };
 
-static __device__ __noinline__ VResult vertex_triple(const DevParams* __restrict__ Pp, const VTrk T[3]) {
-    const DevParams& P = *Pp;
+// intersections of one track pair within target_r + xy_margin (Sec. IV-C), slot 0
+// first; n = 0: the pair does not intersect or no intersection is near the target
+struct PairPts {
+    double x0, y0, x1, y1, w0, w1;   // points, Eq. 10 variances (R13)
+    int n;
+};
+
+__device__ __forceinline__ double turn_to_h0_inl(const VTrk& t, double px, double py) {
+    const double ax = t.h0x - t.cx, ay = t.h0y - t.cy, bx = px - t.cx, by = py - t.cy;
+    return t.q * atan2(ax * by - ay * bx, ax * bx + ay * by);
+}
+
+__device__ __forceinline__ void pair_points(const DevParams& P, const VTrk& A, const VTrk& B, PairPts& o) {
+    o.n = 0;
+    const double dx = B.cx - A.cx, dy = B.cy - A.cy, D = sqrt(dx * dx + dy * dy);
+    if (D == 0.0 || D > A.rt + B.rt || D < fabs(A.rt - B.rt)) return;   // "the track triplet is skipped"
+    const double a = (A.rt * A.rt - B.rt * B.rt + D * D) / (2.0 * D);
+    const double h = sqrt(fmax(0.0, A.rt * A.rt - a * a));
+    const double ux = dx / D, uy = dy / D;
+    const double ax0 = A.cx + a * ux - h * uy, ay0 = A.cy + a * uy + h * ux;
+    const double ax1 = A.cx + a * ux + h * uy, ay1 = A.cy + a * uy - h * ux;
+    const bool k0 = sqrt(ax0 * ax0 + ay0 * ay0) <= P.rlim, k1 = sqrt(ax1 * ax1 + ay1 * ay1) <= P.rlim;
+    o.x0 = k0 ? ax0 : ax1;
+    o.y0 = k0 ? ay0 : ay1;
+    o.x1 = ax1;
+    o.y1 = ay1;
+    o.n = (int)k0 + (int)k1;
+    // Eq. 10 (R13) for each kept point, once (the choice loop combines them 2^3 ways)
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const double px = s ? o.x1 : o.x0, py = s ? o.y1 : o.y0;
+        const double sa = A.rt * fabs(turn_to_h0_inl(A, px, py));
+        const double sb = B.rt * fabs(turn_to_h0_inl(B, px, py));
+        const double w = 0.5 * (A.sms * A.sms * sa * sa + B.sms * B.sms * sb * sb) + P.sig_pix2;
+        if (s) o.w1 = w; else o.w0 = w;
+    }
+}
+
+// Alg. 4 phase 2 for one (e+, e+, e-) triple, inline: every array a named
+// register (choices selected by value), so that a kernel running one triple per
+// thread keeps it out of local memory
+__device__ __forceinline__ VResult vertex_triple_inl(const DevParams& P, const VTrk& T0, const VTrk& T1,
+                                                     const VTrk& T2) {
     VResult best;
     best.found = 0; best.pass = 0;
     best.x = best.y = best.z = best.tdist = best.ptot = 0.0;
     best.chi2 = 1e300;
-    const int pr[3][2] = {{0, 1}, {0, 2}, {1, 2}};
-    double pts[3][2][2];
-    int npt[3];
-    for (int pi = 0; pi < 3; ++pi) {
-        double o[4];
-        if (intersect(T[pr[pi][0]], T[pr[pi][1]], o) == 0) return best;   // "the track triplet is skipped"
-        npt[pi] = 0;
-        for (int s = 0; s < 2; ++s) {
-            if (sqrt(o[2 * s] * o[2 * s] + o[2 * s + 1] * o[2 * s + 1]) <= P.rlim) {
-                pts[pi][npt[pi]][0] = o[2 * s];
-                pts[pi][npt[pi]][1] = o[2 * s + 1];
-                ++npt[pi];
-            }
+    PairPts Q0, Q1, Q2;   // pairs (0,1), (0,2), (1,2)
+    pair_points(P, T0, T1, Q0);
+    if (Q0.n == 0) return best;
+    pair_points(P, T0, T2, Q1);
+    if (Q1.n == 0) return best;
+    pair_points(P, T1, T2, Q2);
+    if (Q2.n == 0) return best;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {   // (s0, s1, s2) in the oracle's nested order, s2 fastest
+        const int s0 = c >> 2, s1 = (c >> 1) & 1, s2 = c & 1;
+        if (s0 >= Q0.n || s1 >= Q1.n || s2 >= Q2.n) continue;
+        const double p0x = s0 ? Q0.x1 : Q0.x0, p0y = s0 ? Q0.y1 : Q0.y0, w0 = s0 ? Q0.w1 : Q0.w0;
+        const double p1x = s1 ? Q1.x1 : Q1.x0, p1y = s1 ? Q1.y1 : Q1.y0, w1 = s1 ? Q1.w1 : Q1.w0;
+        const double p2x = s2 ? Q2.x1 : Q2.x0, p2y = s2 ? Q2.y1 : Q2.y0, w2 = s2 ? Q2.w1 : Q2.w0;
+        // Eq. 9
+        double mx = p0x / w0, my = p0y / w0, ws = 1.0 / w0;
+        mx += p1x / w1; my += p1y / w1; ws += 1.0 / w1;
+        mx += p2x / w2; my += p2y / w2; ws += 1.0 / w2;
+        mx /= ws;
+        my /= ws;
+        double pcx[3], pcy[3], pcz[3], sg[3], mz = 0.0, wz = 0.0;
+        bool bad = false;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {   // Fig. 6, Eq. 11
+            const VTrk& A = t == 0 ? T0 : (t == 1 ? T1 : T2);
+            const double dx = mx - A.cx, dy = my - A.cy, dn = sqrt(dx * dx + dy * dy);
+            bad |= dn == 0.0;
+            pcx[t] = A.cx + A.rt * dx / dn;
+            pcy[t] = A.cy + A.rt * dy / dn;
+            const double dphi = turn_to_h0_inl(A, pcx[t], pcy[t]);
+            pcz[t] = A.h0z - dphi * A.cth / A.k;
+            const double sv = A.rt * fabs(dphi);
+            sg[t] = A.sms * A.sms * sv * sv + P.sig_pix2;
+            mz += pcz[t] / sg[t];
+            wz += 1.0 / sg[t];
         }
-        if (npt[pi] == 0) return best;
-    }
-    // Eq. 10 (R13) weight of every intersection point, once per point (the
-    // choice loop below combines them 2^3 ways)
-    double s2p[3][2];
-    for (int pi = 0; pi < 3; ++pi) {
-        const VTrk& A = T[pr[pi][0]];
-        const VTrk& B = T[pr[pi][1]];
-        for (int s = 0; s < npt[pi]; ++s) {
-            const double px = pts[pi][s][0], py = pts[pi][s][1];
-            const double sa = A.rt * fabs(turn_to_h0(A, px, py));
-            const double sb = B.rt * fabs(turn_to_h0(B, px, py));
-            s2p[pi][s] = 0.5 * (A.sms * A.sms * sa * sa + B.sms * B.sms * sb * sb) + P.sig_pix2;
+        if (bad) continue;
+        mz /= wz;
+        double chi = 0.0;   // Eq. 12 (R15)
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const double ex = pcx[t] - mx, ey = pcy[t] - my, ez = pcz[t] - mz;
+            chi += (ex * ex + ey * ey + ez * ez) / sg[t];
+        }
+        if (chi < best.chi2) {
+            best.found = 1;
+            best.chi2 = chi;
+            best.x = mx; best.y = my; best.z = mz;
+            double px = 0.0, py = 0.0, pz = 0.0;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const VTrk& A = t == 0 ? T0 : (t == 1 ? T1 : T2);
+                // direction of motion at the pca: q (sin ph, -cos ph), ph = angle of pca - c
+                const double irt = 1.0 / A.rt;
+                px += A.p * A.sth * A.q * (pcy[t] - A.cy) * irt;
+                py += A.p * A.sth * (-A.q) * (pcx[t] - A.cx) * irt;
+                pz += A.p * A.cth;
+            }
+            best.ptot = sqrt(px * px + py * py + pz * pz);
         }
     }
-    for (int s0 = 0; s0 < npt[0]; ++s0)
-        for (int s1 = 0; s1 < npt[1]; ++s1)
-            for (int s2 = 0; s2 < npt[2]; ++s2) {
-                const int sel[3] = {s0, s1, s2};
-                double mx = 0.0, my = 0.0, ws = 0.0;
-                for (int pi = 0; pi < 3; ++pi) {                           // Eq. 9
-                    const double px = pts[pi][sel[pi]][0], py = pts[pi][sel[pi]][1];
-                    const double s2v = s2p[pi][sel[pi]];
-                    mx += px / s2v; my += py / s2v; ws += 1.0 / s2v;
-                }
-                mx /= ws; my /= ws;
-                double pcx[3], pcy[3], pcz[3], sg[3], mz = 0.0, wz = 0.0;
-                bool bad = false;
-                for (int t = 0; t < 3; ++t) {                              // Fig. 6, Eq. 11
-                    const VTrk& A = T[t];
-                    const double dx = mx - A.cx, dy = my - A.cy, dn = sqrt(dx * dx + dy * dy);
-                    if (dn == 0.0) { bad = true; break; }
-                    pcx[t] = A.cx + A.rt * dx / dn;
-                    pcy[t] = A.cy + A.rt * dy / dn;
-                    const double dphi = turn_to_h0(A, pcx[t], pcy[t]);
-                    pcz[t] = A.h0z - dphi * A.cth / A.k;
-                    const double s = A.rt * fabs(dphi);
-                    sg[t] = A.sms * A.sms * s * s + P.sig_pix2;
-                    mz += pcz[t] / sg[t]; wz += 1.0 / sg[t];
-                }
-                if (bad) continue;
-                mz /= wz;
-                double chi = 0.0;                                          // Eq. 12 (R15)
-                for (int t = 0; t < 3; ++t) {
-                    const double ex = pcx[t] - mx, ey = pcy[t] - my, ez = pcz[t] - mz;
-                    chi += (ex * ex + ey * ey + ez * ez) / sg[t];
-                }
-                if (chi < best.chi2) {
-                    best.found = 1;
-                    best.chi2 = chi;
-                    best.x = mx; best.y = my; best.z = mz;
-                    double px = 0.0, py = 0.0, pz = 0.0;
-                    for (int t = 0; t < 3; ++t) {
-                        const VTrk& A = T[t];
-                        // direction of motion at the pca: q (sin ph, -cos ph), ph = angle of pca - c
-                        const double irt = 1.0 / A.rt;
-                        px += A.p * A.sth * A.q * (pcy[t] - A.cy) * irt;
-                        py += A.p * A.sth * (-A.q) * (pcx[t] - A.cx) * irt;
-                        pz += A.p * A.cth;
-                    }
-                    best.ptot = sqrt(px * px + py * py + pz * pz);
-                }
-            }
     if (best.found) {
         best.tdist = target_distance(P, best.x, best.y, best.z);
         best.pass = best.chi2 <= P.chi2v_max && best.tdist <= P.tdist_max && best.ptot <= P.ptot_max;

@@ -36,6 +36,9 @@
 #ifndef M3E_MIN_BLOCKS_SEL
 #define M3E_MIN_BLOCKS_SEL 4   // same for the selection kernel of the split path
 #endif
+#ifndef M3E_MIN_BLOCKS_SEL_BIG
+#define M3E_MIN_BLOCKS_SEL_BIG 3   // its big-frame variant (80 registers: the pair-list walk does not spill)
+#endif
 
 namespace m3e {
 
@@ -619,11 +622,11 @@ static __device__ __noinline__ VOut vertex_frame(const DevParams* __restrict__ P
                 bres.pass = 0;
                 for (int c = lane; c < ncomb; c += 32) {
                     const uint32_t code = V.vcomb[c];
-                    VTrk T[3];
-                    T[0] = make_vtrk(P, tj[code & 255u], Fv);
-                    T[1] = make_vtrk(P, tj[(code >> 8) & 255u], Fv);
-                    T[2] = make_vtrk(P, tj[(code >> 16) & 255u], Fv);
-                    const VResult r = vertex_triple(Pp, T);
+                    // the same inline routine as triple_kernel's (identical rounding)
+                    const VTrk T0 = make_vtrk(P, tj[code & 255u], Fv);
+                    const VTrk T1 = make_vtrk(P, tj[(code >> 8) & 255u], Fv);
+                    const VTrk T2 = make_vtrk(P, tj[(code >> 16) & 255u], Fv);
+                    const VResult r = vertex_triple_inl(P, T0, T1, T2);
                     if (r.pass && r.chi2 < bchi) { bchi = r.chi2; bidx = c; bres = r; }
                 }
                 // lowest chi2 among passing triples, earliest on ties
@@ -678,7 +681,8 @@ __device__ __forceinline__ void flush_summary(m3e_summary* sm, const uint32_t* a
 
 // ------------------------------------------------------------------ kernel ----
 template <int MODE, bool BIG>
-__global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCKS_SEL : M3E_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MIN_BLOCKS_SEL_BIG : M3E_MIN_BLOCKS_SEL)
+                                                                  : M3E_MIN_BLOCKS)
     filter_kernel(const KArgs A) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -1156,30 +1160,43 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? M3E_MIN_BLOCK
 
 // ------------------------------------------------------------- pack kernel ----
 // Output packer (north-star row (f)): tile t = warp-batches [256 t, 256 t + 256),
-// one warp per 32 warp-batches.  The tile's counts are summed at once, a decoupled
-// look-back over tiles gives its global bases, and every warp-batch's tracks,
-// kept-frame records, packed hits (SoA) and per-frame indices are written in frame
-// order.  Memory bound: reads the staged records once, writes the outputs once.
+// one thread per warp-batch for the counts.  The tile's counts are scanned at
+// once, a decoupled look-back over tiles gives its global bases (all counts are
+// final, so it never waits on compute), and then every copy is a flat,
+// thread-strided stream over the tile's output:
+//   tracks  output index d -> its warp-batch by binary search over the tile's
+//           track prefix -> source (the front of the warp-batch's store segment,
+//           or the fused kernel's staging), 32 B each, four in flight per thread;
+//   frames  each frame record's track_first / kept_index made call-global;
+//   kept    the (rare) kept frames: vertex record, packed offsets and hits.
+// Memory bound: reads the staged tracks once, writes the outputs once.
+#ifndef M3E_PACK_MIN_BLOCKS
+#define M3E_PACK_MIN_BLOCKS 3   // 80 registers, no spills (4 CTAs: 64 registers and spills, 1.23 ms against 1.10)
+#endif
 struct PackSmem {
     uint32_t wagg[kWarps][3];
     uint32_t base[3];
     uint32_t tile;
+    uint32_t ptrk[kPackTile + 1];   // exclusive prefix of the tile's tracks per warp-batch (+ total)
+    uint32_t pkept[kPackTile];      // ... of its kept frames
+    uint32_t src[kPackTile];        // first track's source: store index, or staging index | 1 << 31
 };
 
-__global__ void __launch_bounds__(kThreads) pack_kernel(const KArgs A) {
+__global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(const KArgs A) {
     __shared__ PackSmem S;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const m3e_outputs& O = A.out;
     const uint32_t ntiles = (A.nbatch + kPackTile - 1) / kPackTile;
+    const uint32_t fb = (uint32_t)A.fb;
     for (;;) {
         if (tid == 0) S.tile = atomicAdd(A.ticket + 3, 1u);
         __syncthreads();
         const uint32_t t = S.tile;
         if (t >= ntiles) break;
-        const uint32_t b = t * kPackTile + warp * 32 + lane;
+        const uint32_t b = t * kPackTile + tid;
         BatchStat bs = {};
         if (b < A.nbatch) bs = A.bstat[b];
-        // warp-inclusive scans of the three counts
+        // block-wide scan of the three counts: warp-inclusive scans + warp totals
         uint32_t it = bs.n_trk, ik = bs.n_kept, ih = bs.n_hits;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1198,136 +1215,145 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const KArgs A) {
             const uint3 ex = resolve(A, t, agg);
             if (lane == 0) { S.base[0] = ex.x; S.base[1] = ex.y; S.base[2] = ex.z; }
         }
+        uint32_t w0 = 0, w1 = 0, w2 = 0;   // this warp's offset inside the tile
+        for (int w = 0; w < warp; ++w) { w0 += S.wagg[w][0]; w1 += S.wagg[w][1]; w2 += S.wagg[w][2]; }
+        S.ptrk[tid] = w0 + it - bs.n_trk;
+        S.pkept[tid] = w1 + ik - bs.n_kept;
+        S.src[tid] = bs.s_trk == kSpilled ? bs.c_base : (bs.s_trk | 0x80000000u);
+        if (tid == kThreads - 1) S.ptrk[kPackTile] = w0 + it;
         __syncthreads();
-        uint32_t wb0 = S.base[0], wb1 = S.base[1], wb2 = S.base[2];
-        for (int w = 0; w < warp; ++w) { wb0 += S.wagg[w][0]; wb1 += S.wagg[w][1]; wb2 += S.wagg[w][2]; }
-        // exclusive bases of this lane's warp-batch
-        const uint32_t eb_trk = wb0 + it - bs.n_trk, eb_kept = wb1 + ik - bs.n_kept, eb_hits = wb2 + ih - bs.n_hits;
+        const uint32_t base_trk = S.base[0], base_kept = S.base[1];
         bool overflow = false;
-        // each warp walks its 32 warp-batches; all lanes cooperate on one at a time
-        for (int src = 0; src < 32; ++src) {
-            const uint32_t bb = t * kPackTile + warp * 32 + src;
-            if (bb >= A.nbatch) break;
-            {   // L2 prefetch of the warp-batch two ahead: its fit records, code bytes and
-                // frame records (the walk is a chain of dependent loads per warp-batch)
-                const int pf = src + 2;
-                const uint32_t pc_base = __shfl_sync(0xffffffffu, bs.c_base, pf & 31);
-                const uint32_t pc_n = __shfl_sync(0xffffffffu, bs.c_n, pf & 31);
-                const uint32_t ps_trk = __shfl_sync(0xffffffffu, bs.s_trk, pf & 31);
-                if (pf < 32 && bb + 2 < A.nbatch) {
-                    if (ps_trk == kSpilled && pc_n) {
-                        const char* fr = reinterpret_cast<const char*>(A.fit_g + pc_base);
-                        const uint32_t nl = (pc_n * 32u + 127u) / 128u + 1u;
-                        if ((uint32_t)lane < nl && lane < 30) prefetch_l2(fr + 128 * lane);
-                    }
-                    if (lane == 30 && O.frames) prefetch_l2(O.frames + (size_t)(bb + 2) * A.fb);
-                }
-            }
-            const uint32_t n_trk = __shfl_sync(0xffffffffu, bs.n_trk, src);
-            const uint32_t n_kept = __shfl_sync(0xffffffffu, bs.n_kept, src);
-            const uint32_t s_trk = __shfl_sync(0xffffffffu, bs.s_trk, src);
-            const uint32_t s_kept = __shfl_sync(0xffffffffu, bs.s_kept, src);
-            const uint32_t nf = __shfl_sync(0xffffffffu, bs.nf, src);
-            const uint32_t g_trk = __shfl_sync(0xffffffffu, eb_trk, src);
-            const uint32_t g_kept = __shfl_sync(0xffffffffu, eb_kept, src);
-            uint32_t g_hits = __shfl_sync(0xffffffffu, eb_hits, src);
-            const uint32_t f0 = bb * (uint32_t)A.fb;
-            // tracks
-            const uint32_t c_base = __shfl_sync(0xffffffffu, bs.c_base, src);
-            const uint32_t c_n = __shfl_sync(0xffffffffu, bs.c_n, src);
-            if (O.tracks && A.stage_trk && s_trk == kSpilled) {
-                // straight from the front of the warp-batch's store segment (fit kernel:
-                // each frame's output tracks, frame order), one 16 B half per lane
-                for (uint32_t e = lane; e < 2 * c_n; e += 32) {
-                    const uint32_t dst = g_trk + (e >> 1);
-                    if (dst < O.track_capacity) {
-                        reinterpret_cast<uint4*>(O.tracks + dst)[e & 1u] =
-                            reinterpret_cast<const uint4*>(A.fit_g + c_base + (e >> 1))[e & 1u];
-                    } else {
-                        overflow = true;
-                    }
-                }
-            } else if (O.tracks && A.stage_trk) {
-                for (uint32_t e = lane; e < n_trk; e += 32) {
-                    const uint32_t dst = g_trk + e;
-                    if (dst < O.track_capacity && s_trk + e < A.stage_trk_cap) {
-                        const uint4* s4 = reinterpret_cast<const uint4*>(A.stage_trk + s_trk + e);
-                        uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst);
-                        d4[0] = s4[0];
-                        d4[1] = s4[1];
-                    } else {
-                        overflow = true;
-                    }
-                }
-            }
-            // per-frame indices: warp-batch relative -> call global
-            if (O.frames) {
-                for (uint32_t j = lane; j < nf; j += 32) {
-                    m3e_frame_out& fo = O.frames[f0 + j];
-                    fo.track_first += g_trk;
-                    if (fo.kept_index != 0xFFFFFFFFu) fo.kept_index += g_kept;
-                }
-            }
-            // kept frames: records, offsets and hits, in frame order
-            for (uint32_t k0 = 0; k0 < n_kept; k0 += 32) {
-                const uint32_t k = k0 + lane;
-                uint32_t f = 0, nh = 0, lo = 0;
-                const bool valid = k < n_kept && s_kept + k < A.stage_kept_cap;
-                KeptRec kr;
-                if (valid) {
-                    kr = A.stage_kept[s_kept + k];
-                    f = kr.frame;
-                    lo = A.offsets[4 * (size_t)f];
-                    nh = A.offsets[4 * (size_t)f + 4] - lo;
-                }
-                if (k < n_kept && !valid) overflow = true;
-                // exclusive prefix of the kept frames' hit counts inside this warp-batch
-                uint32_t inc = nh;
+        // ---- tracks: flat over the tile's output, 4 tracks in flight per thread
+        if (O.tracks && A.stage_trk) {
+            const uint32_t T = S.ptrk[kPackTile];
+            for (uint32_t d0 = tid; d0 < T; d0 += 4 * kThreads) {
+                uint4 v[4][2];
+                uint32_t dst[4];
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += a;
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t d = d0 + u * kThreads;
+                    dst[u] = 0xFFFFFFFFu;
+                    if (d < T) {
+                        int lo = 0, hi = kPackTile - 1;   // last warp-batch with ptrk <= d
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (S.ptrk[mid] <= d) lo = mid; else hi = mid - 1;
+                        }
+                        const uint32_t sr = S.src[lo], k = d - S.ptrk[lo];
+                        const uint4* s4 = (sr & 0x80000000u)
+                                              ? reinterpret_cast<const uint4*>(A.stage_trk + (sr & 0x7FFFFFFFu) + k)
+                                              : reinterpret_cast<const uint4*>(A.fit_g + sr + k);
+                        v[u][0] = s4[0];
+                        v[u][1] = s4[1];
+                        dst[u] = base_trk + d;
+                    }
                 }
-                const uint32_t hb = g_hits + inc - nh;
-                const uint32_t kidx = g_kept + k;
-                if (valid) {
-                    if (kidx < O.kept_capacity) {
-                        if (O.kept_frame) O.kept_frame[kidx] = f;
-                        if (O.vertices) O.vertices[kidx] = kr.v;
-                        if (O.kept_offsets)
-                            for (int l = 0; l < 4; ++l)
-                                O.kept_offsets[4 * (size_t)kidx + l] = hb + (A.offsets[4 * (size_t)f + l] - lo);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (dst[u] == 0xFFFFFFFFu) continue;
+                    if (dst[u] < O.track_capacity) {
+                        uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst[u]);
+                        d4[0] = v[u][0];
+                        d4[1] = v[u][1];
                     } else {
                         overflow = true;
                     }
                 }
-                const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-                __syncwarp();
-                if (O.kept_x) {
-                    // simple per-frame loop: kept frames are rare (<< 1 % of frames)
-                    for (int src2 = 0; src2 < 32; ++src2) {
-                        const uint32_t kk = k0 + src2;
-                        if (kk >= n_kept) break;
-                        const uint32_t fl = __shfl_sync(0xffffffffu, lo, src2);
-                        const uint32_t fn = __shfl_sync(0xffffffffu, nh, src2);
-                        const uint32_t fh = __shfl_sync(0xffffffffu, hb, src2);
-                        for (uint32_t e = lane; e < fn; e += 32) {
-                            const uint32_t dst = fh + e;
-                            if (dst < O.kept_hit_capacity) {
-                                O.kept_x[dst] = A.x[fl + e];
-                                O.kept_y[dst] = A.y[fl + e];
-                                O.kept_z[dst] = A.z[fl + e];
-                            } else {
-                                overflow = true;
+            }
+        }
+        // ---- frame records: warp-batch relative indices -> call global
+        if (O.frames) {
+            const uint32_t f0 = t * kPackTile * fb;
+            const uint32_t f1 = min(A.F, (t + 1) * kPackTile * fb);
+            for (uint32_t fa = f0 + tid; fa < f1; fa += 4 * kThreads) {   // 4 records in flight
+                uint2 w[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t f = fa + u * kThreads;
+                    if (f < f1) w[u] = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(O.frames + f) + 8);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t f = fa + u * kThreads;
+                    if (f >= f1) continue;
+                    const uint32_t bl = (f - f0) / fb;   // {track_first, kept_index} of the record
+                    w[u].x += base_trk + S.ptrk[bl];
+                    if (w[u].y != 0xFFFFFFFFu) w[u].y += base_kept + S.pkept[bl];
+                    *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(O.frames + f) + 8) = w[u];
+                }
+            }
+        }
+        // ---- kept frames (rare): each warp takes its 32 warp-batches that keep any
+        {
+            uint32_t g_hits = S.base[2];
+            for (int w = 0; w < warp; ++w) g_hits += S.wagg[w][2];
+            const uint32_t eb_hits = g_hits + ih - bs.n_hits;   // this lane's warp-batch
+            unsigned todo = __ballot_sync(0xffffffffu, bs.n_kept > 0);
+            while (todo) {
+                const int srcl = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const uint32_t n_kept = __shfl_sync(0xffffffffu, bs.n_kept, srcl);
+                const uint32_t s_kept = __shfl_sync(0xffffffffu, bs.s_kept, srcl);
+                const uint32_t g_kept = base_kept + S.pkept[warp * 32 + srcl];
+                uint32_t gh = __shfl_sync(0xffffffffu, eb_hits, srcl);
+                for (uint32_t k0 = 0; k0 < n_kept; k0 += 32) {
+                    const uint32_t k = k0 + lane;
+                    uint32_t f = 0, nh = 0, lo = 0;
+                    const bool valid = k < n_kept && s_kept + k < A.stage_kept_cap;
+                    KeptRec kr;
+                    if (valid) {
+                        kr = A.stage_kept[s_kept + k];
+                        f = kr.frame;
+                        lo = A.offsets[4 * (size_t)f];
+                        nh = A.offsets[4 * (size_t)f + 4] - lo;
+                    }
+                    if (k < n_kept && !valid) overflow = true;
+                    uint32_t inc = nh;   // prefix of the kept frames' hit counts
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+                        if (lane >= o) inc += a;
+                    }
+                    const uint32_t hb = gh + inc - nh;
+                    const uint32_t kidx = g_kept + k;
+                    if (valid) {
+                        if (kidx < O.kept_capacity) {
+                            if (O.kept_frame) O.kept_frame[kidx] = f;
+                            if (O.vertices) O.vertices[kidx] = kr.v;
+                            if (O.kept_offsets)
+                                for (int l = 0; l < 4; ++l)
+                                    O.kept_offsets[4 * (size_t)kidx + l] = hb + (A.offsets[4 * (size_t)f + l] - lo);
+                        } else {
+                            overflow = true;
+                        }
+                    }
+                    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+                    if (O.kept_x) {
+                        for (int s2 = 0; s2 < 32; ++s2) {
+                            if (k0 + s2 >= n_kept) break;
+                            const uint32_t fl = __shfl_sync(0xffffffffu, lo, s2);
+                            const uint32_t fn = __shfl_sync(0xffffffffu, nh, s2);
+                            const uint32_t fh = __shfl_sync(0xffffffffu, hb, s2);
+                            for (uint32_t e = lane; e < fn; e += 32) {
+                                const uint32_t dst = fh + e;
+                                if (dst < O.kept_hit_capacity) {
+                                    O.kept_x[dst] = A.x[fl + e];
+                                    O.kept_y[dst] = A.y[fl + e];
+                                    O.kept_z[dst] = A.z[fl + e];
+                                } else {
+                                    overflow = true;
+                                }
                             }
                         }
                     }
+                    gh += tot;
                 }
-                g_hits += tot;
             }
-            if (bb == A.nbatch - 1 && lane == 0 && O.kept_offsets) {   // close the packed offsets
-                const uint32_t K = g_kept + n_kept;
-                if (K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = g_hits;
+            // the call's last warp-batch closes the packed offsets
+            if (b == A.nbatch - 1 && O.kept_offsets) {
+                const uint32_t K = base_kept + S.pkept[tid] + bs.n_kept;
+                if (K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = eb_hits + bs.n_hits;
             }
         }
         if (__any_sync(0xffffffffu, overflow) && lane == 0 && O.summary)
@@ -1848,7 +1874,10 @@ __global__ void __launch_bounds__(kThreads, 4) vertex_kernel(const __grid_consta
 }
 
 // phase 2: one thread per listed triple
-__global__ void __launch_bounds__(kThreads, 2) triple_kernel(const __grid_constant__ KArgs A) {
+#ifndef M3E_TRIPLE_MIN_BLOCKS
+#define M3E_TRIPLE_MIN_BLOCKS 3   // 80 registers: occupancy beats the spills (measured 1 / 2 / 3: 0.74 / 0.58 / 0.52 ms vertex stage)
+#endif
+__global__ void __launch_bounds__(kThreads, M3E_TRIPLE_MIN_BLOCKS) triple_kernel(const __grid_constant__ KArgs A) {
     __shared__ DevParams SP;
     if (threadIdx.x == 0) SP = A.P;
     __syncthreads();
@@ -1864,11 +1893,10 @@ __global__ void __launch_bounds__(kThreads, 2) triple_kernel(const __grid_consta
         Fv.y = A.y + g0;
         Fv.z = A.z + g0;
         Fv.s[0] = 0;
-        VTrk T[3];
-        T[0] = make_vtrk(SP, A.fit_g[v.y + (e.y & 1023u)], Fv);
-        T[1] = make_vtrk(SP, A.fit_g[v.y + ((e.y >> 10) & 1023u)], Fv);
-        T[2] = make_vtrk(SP, A.fit_g[v.y + ((e.y >> 20) & 1023u)], Fv);
-        const VResult r = vertex_triple(&SP, T);
+        const VTrk T0 = make_vtrk(SP, A.fit_g[v.y + (e.y & 1023u)], Fv);
+        const VTrk T1 = make_vtrk(SP, A.fit_g[v.y + ((e.y >> 10) & 1023u)], Fv);
+        const VTrk T2 = make_vtrk(SP, A.fit_g[v.y + ((e.y >> 20) & 1023u)], Fv);
+        const VResult r = vertex_triple_inl(SP, T0, T1, T2);
         VRes o;
         o.x = r.x; o.y = r.y; o.z = r.z;
         o.chi2 = r.chi2;
@@ -2041,10 +2069,16 @@ cudaError_t launch_vertex(const KArgs& a, int grid, int sms, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     vertex_kernel<<<grid, kThreads, smem, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    triple_kernel<<<sms * 4, kThreads, 0, s>>>(a);
+    triple_kernel<<<sms * triple_blocks_per_sm(), kThreads, 0, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     vpost_kernel<<<sms * 2, kThreads, 0, s>>>(a);
     return cudaGetLastError();
+}
+
+int triple_blocks_per_sm() {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, triple_kernel, kThreads, 0) != cudaSuccess) return 1;
+    return n > 0 ? n : 1;
 }
 
 int vertex_blocks_per_sm() {

@@ -127,6 +127,7 @@ cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s);
 int finish_blocks_per_sm();
 cudaError_t launch_vertex(const KArgs& a, int grid, int sms, cudaStream_t s);
 int vertex_blocks_per_sm();
+int triple_blocks_per_sm();
 int blocks_per_sm(int mode, bool big);
 
 }  // namespace m3e
