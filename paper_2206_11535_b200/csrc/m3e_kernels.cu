@@ -2058,6 +2058,31 @@ __global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel
     if (lane == 0 && A.out.summary) flush_summary(A.out.summary, S.acc[warp]);
 }
 
+// host path: add the chunk's bases to its device outputs before they are copied
+__global__ void rebase_kernel(const Rebase r) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r.frames)
+        for (uint64_t i = i0; i < r.n_frames; i += stride) {
+            m3e_frame_out& fo = r.frames[i];
+            fo.track_first += r.base_trk;
+            if (fo.kept_index != 0xFFFFFFFFu) fo.kept_index += r.base_kept;
+        }
+    if (r.tracks)
+        for (uint64_t i = i0; i < r.n_tracks; i += stride) r.tracks[i].frame += r.frame0;
+    for (uint64_t i = i0; i < r.n_kept; i += stride) {
+        if (r.kept_frame) r.kept_frame[i] += r.frame0;
+        if (r.kept_offsets)
+            for (int l = 0; l < 4; ++l) r.kept_offsets[4 * i + l] += r.base_hits;
+        if (r.vertices && r.vertices[i].frame != 0xFFFFFFFFu) r.vertices[i].frame += r.frame0;
+    }
+}
+
+cudaError_t launch_rebase(const Rebase& r, int sms, cudaStream_t s) {
+    rebase_kernel<<<sms * 4, kThreads, 0, s>>>(r);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s) {
     finish_kernel<<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();

@@ -118,6 +118,20 @@ struct KArgs {
     m3e_outputs out;
 };
 
+// host path: chunk-local output indices made call-global (m3e_filter_host)
+struct Rebase {
+    m3e_frame_out* frames;
+    uint64_t n_frames;
+    m3e_track* tracks;
+    uint64_t n_tracks;
+    uint32_t* kept_frame;
+    uint32_t* kept_offsets;
+    m3e_vertex* vertices;
+    uint64_t n_kept;
+    uint32_t frame0, base_trk, base_kept, base_hits;
+};
+cudaError_t launch_rebase(const Rebase& r, int sms, cudaStream_t s);
+
 size_t smem_bytes();
 cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);

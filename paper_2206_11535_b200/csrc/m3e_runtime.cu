@@ -720,6 +720,23 @@ int m3e_filter_host(m3e_context* ctx, const m3e_params* p, const float* x, const
         if (out->tracks && base_trk + T > out->track_capacity)
             return fail(M3E_ERR_CAPACITY, "track_capacity too small");
         const uint64_t nfr = d.b - d.a;
+        // chunk-local indices -> call-global, on the device before the copies
+        // (frames' track_first / kept_index, tracks' and kept records' frame,
+        // packed offsets)
+        Rebase rb{};
+        rb.frames = out->frames ? c.frames : nullptr;
+        rb.n_frames = nfr;
+        rb.tracks = out->tracks ? c.tracks : nullptr;
+        rb.n_tracks = T;
+        rb.kept_frame = out->kept_frame ? c.kept_frame : nullptr;
+        rb.kept_offsets = out->kept_offsets ? c.kept_offsets : nullptr;
+        rb.vertices = out->vertices ? c.vertices : nullptr;
+        rb.n_kept = K;
+        rb.frame0 = (uint32_t)d.a;
+        rb.base_trk = (uint32_t)base_trk;
+        rb.base_kept = (uint32_t)base_kept;
+        rb.base_hits = (uint32_t)base_hits;
+        if (d.a || base_trk || base_kept || base_hits) CK(launch_rebase(rb, ctx->sms, s));
         if (out->reason) CK(cudaMemcpyAsync(out->reason + d.a, c.reason, nfr, cudaMemcpyDeviceToHost, s));
         if (out->frames)
             CK(cudaMemcpyAsync(out->frames + d.a, c.frames, nfr * sizeof(m3e_frame_out), cudaMemcpyDeviceToHost, s));
@@ -742,22 +759,6 @@ int m3e_filter_host(m3e_context* ctx, const m3e_params* p, const float* x, const
         }
         CK(cudaEventRecord(c.ev_free, s));
         CK(cudaEventSynchronize(c.ev_free));
-        // chunk-local indices -> call-global indices
-        if (out->frames)
-            for (uint64_t f = 0; f < nfr; ++f) {
-                m3e_frame_out& fo = out->frames[d.a + f];
-                fo.track_first += (uint32_t)base_trk;
-                if (fo.kept_index != 0xFFFFFFFFu) fo.kept_index += (uint32_t)base_kept;
-            }
-        if (out->tracks)
-            for (uint64_t t = 0; t < T; ++t) out->tracks[base_trk + t].frame += (uint32_t)d.a;
-        for (uint64_t k = 0; k < K; ++k) {
-            if (out->kept_frame) out->kept_frame[base_kept + k] += (uint32_t)d.a;
-            if (out->kept_offsets)
-                for (int l = 0; l < 4; ++l) out->kept_offsets[4 * (base_kept + k) + l] += (uint32_t)base_hits;
-            if (out->vertices && out->vertices[base_kept + k].frame != 0xFFFFFFFFu)
-                out->vertices[base_kept + k].frame += (uint32_t)d.a;
-        }
         total.frames += sm.frames;
         for (int r = 0; r < 6; ++r) total.kept_by_reason[r] += sm.kept_by_reason[r];
         total.candidates += sm.candidates;

@@ -1,8 +1,12 @@
 """North-star physics figures measured on the CUDA path's outputs with the
 generator's truth (synth/truth.py): signal-track efficiency, signal-event
 efficiency and the phase-I reduction factor (PAPER.md abstract / Sec. VI:
-tracks ~97%, signal events ~94%, reduction > 100).  Floors are this toy
-generator's values with margin."""
+tracks ~97%, signal events ~94%, reduction > 100).  Signal-track efficiency and
+reduction are held at the paper's targets.  Signal-event efficiency is a known
+gap (~90.5% on this toy against the 94% target), attributed to the paper's own
+rule "If two circles do not intersect, the track triplet is skipped" (Sec. IV-C)
+by tests/test_oracle_pipeline.py::test_signal_event_loss_attribution (DESIGN.md
+"Efficiency"); its floor here is the toy's value with margin."""
 import numpy as np
 import pytest
 
@@ -36,8 +40,8 @@ def test_signal_efficiencies(cfg):
     sc, d, fo, tr = _run("signal_only", 3000, 1201, params)
     e = signal_efficiency(sc, d, fo, tr, cfg["max_tracks"])
     print("signal_only:", e)
-    assert e["signal_track_eff"] >= 0.95
-    assert e["signal_event_eff"] >= 0.85
+    assert e["signal_track_eff"] >= 0.97
+    assert e["signal_event_eff"] >= 0.87
 
 
 def test_phase1_reduction_and_signal(cfg):
@@ -48,4 +52,5 @@ def test_phase1_reduction_and_signal(cfg):
     e = signal_efficiency(sc, d, fo, tr, cfg["max_tracks"])
     print(f"phase1_sig: reduction factor {n / kept:.1f}", e)
     assert n / kept >= 100
-    assert e["signal_event_eff"] >= 0.8
+    assert e["signal_track_eff"] >= 0.97
+    assert e["signal_event_eff"] >= 0.85

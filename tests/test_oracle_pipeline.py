@@ -208,3 +208,37 @@ def test_paper_reduction_factor(P):
     d = synth.generate(synth.preset("phase1_sig", seed=616), 6000)
     r = oracle.results_to_numpy(oracle.process_frames(P, oracle.Frames(d)))
     assert r["keep"].mean() < 0.01
+
+
+def test_signal_event_loss_attribution(P):
+    """Known gap, attributed: north_star asks for >= 94%
+    of signal events; the oracle keeps ~90.5% of frames whose three mu->eee
+    daughters are reconstructible.  tools/efficiency_study.py follows the TRUE
+    triple through Alg. 2-4: ~5% of frames are lost to the paper's rule "If two
+    circles do not intersect, the track triplet is skipped" (Sec. IV-C; the
+    daughters' circles miss by ~0.2 mm after layer-0 scattering), and lifting
+    that one rule (the two circles made tangent, everything else the oracle's)
+    brings the same frames to >= 93.5%."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "efficiency_study", os.path.join(ROOT, "tools", "efficiency_study.py"))
+    es = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(es)
+    sc = synth.preset("signal_only", seed=9101)
+    n = 8000
+    d = synth.generate(sc, n, truth=True)
+    fr = oracle.Frames(d)
+    tot = kept = lifted = no_int = 0
+    for f in range(n):
+        r = es.classify(P, fr, d, sc, f)
+        if r is None:
+            continue
+        tot += 1
+        (cause, det), _, tracks, tri = r
+        kept += cause == "kept"
+        if cause == "no_intersect":
+            no_int += 1
+            lifted += es.lift_no_intersect(P, fr, f, tracks, tri)
+    assert 0.87 <= kept / tot <= 0.93
+    assert 0.03 <= no_int / tot <= 0.07
+    assert (kept + lifted) / tot >= 0.935
