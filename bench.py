@@ -396,10 +396,9 @@ def main():
         if split:
             names = [("select", "m3e::filter_kernel<SELECT_C, BIG=false>", ms_select, in_bytes),
                      ("fit", "m3e::fit_kernel", ms_fit, in_bytes + 32 * tracks),
-                     ("tracks", "m3e::tracks_kernel", ms_tracks, 0),
                      ("vertex", "m3e::vertex_kernel+triple_kernel+vpost_kernel", ms_vertex, 0),
-                     ("finish", "m3e::finish_kernel", ms_filter, 17 * F),
-                     ("pack", "m3e::pack_kernel", ms_pack, out_bytes - 17 * F)]
+                     ("fused_spilled", "m3e::filter_kernel<FULL, BIG=false>", ms_filter, 0),
+                     ("pack", "m3e::pack_kernel", ms_pack, out_bytes)]
         else:
             names = [("filter", "m3e::filter_kernel<FULL, BIG=%s>" % ("true" if big else "false"), ms_filter,
                       in_bytes + out_bytes), ("pack", "m3e::pack_kernel", ms_pack, out_bytes)]
@@ -470,7 +469,7 @@ def main():
                        "parallelism": f"frame-sharded dp{world}", "generation_s": round(t_gen, 1),
                        "physics": phys},
             "roofline": roof,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (8 if split else 2) * a.steps, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (7 if split else 2) * a.steps, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -164,11 +164,11 @@ uint64_t m3e_workspace_bytes(const m3e_context* ctx);
  * stream around each of its kernels (up to 1024 calls); m3e_kernel_times()
  * waits for them and returns the MEAN durations in ms over those calls, then
  * resets the record:
- *   ms[0] selection kernel, ms[1] fit kernel, ms[2] track kernel, ms[3] vertex
- *   kernel (all four 0 when the call ran the single fused filter kernel),
- *   ms[4] output-staging kernel plus the fused filter kernel over warp-batches the
- *   candidate store could not take (the whole path on the fused variant),
- *   ms[5] pack kernel.
+ *   ms[0] selection kernel, ms[1] fit kernel (with the per-frame track stage),
+ *   ms[2] 0 (no separate track kernel), ms[3] vertex kernels (all four 0 when
+ *   the call ran the single fused filter kernel), ms[4] the fused filter kernel
+ *   over warp-batches the candidate store could not take (the whole path on the
+ *   fused variant), ms[5] output kernel (frame records, tracks, kept frames).
  * The split path is the default; M3E_FUSED=1 in the environment at m3e_create
  * selects the single fused kernel (same results). */
 int m3e_set_timing(m3e_context* ctx, int enable);

@@ -124,7 +124,7 @@ struct FlatSel {
 // Cold vertex-stage scratch of one warp, in global memory (L1/L2 resident;
 // touched for ~1.5% of frames), so that it does not cost shared memory.
 struct VScratch {
-    m3e_vertex vtx[32];   // by frame lane: kFB frames of a warp-batch, 32 of a finish-kernel group
+    m3e_vertex vtx[32];   // by frame lane: kFB frames of a warp-batch
     uint32_t vcomb[kMaxCombsCap];
     uint8_t vlist[2][kMaxTracksCap];
 };
@@ -1159,19 +1159,27 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
 }
 
 // ------------------------------------------------------------- pack kernel ----
-// Output packer (north-star row (f)): tile t = warp-batches [256 t, 256 t + 256),
-// one thread per warp-batch for the counts.  The tile's counts are scanned at
-// once, a decoupled look-back over tiles gives its global bases (all counts are
-// final, so it never waits on compute), and then every copy is a flat,
-// thread-strided stream over the tile's output:
-//   tracks  output index d -> its warp-batch by binary search over the tile's
-//           track prefix -> source (the front of the warp-batch's store segment,
-//           or the fused kernel's staging), 32 B each, four in flight per thread;
-//   frames  each frame record's track_first / kept_index made call-global;
-//   kept    the (rare) kept frames: vertex record, packed offsets and hits.
-// Memory bound: reads the staged tracks once, writes the outputs once.
+// Output stage O + packer (north-star row (f)), one pass over tiles of 256
+// warp-batches:
+//   counts  one thread per warp-batch: from the per-frame selection / track /
+//           vertex words (fit and vertex kernels) its output tracks (each frame's
+//           first max_tracks accepted; none for triplet-overflow or invalid
+//           frames), kept frames and their hits; the in-batch prefixes per frame
+//           go to shared memory.  Warp-batches the fused kernel ran (candidate
+//           store full; every warp-batch on the fused variant) bring their counts
+//           and staged outputs in their BatchStat;
+//   bases   the tile's counts are scanned at once and a decoupled look-back over
+//           tiles gives its global bases (every count is final: it never waits on
+//           compute);
+//   frames  every frame record written once with its final track_first /
+//           kept_index (flat, thread-strided), and the reason byte;
+//   tracks  flat over the tile's output: index -> warp-batch by binary search over
+//           the tile's prefix -> the front of its store segment (fit kernel) or
+//           the fused kernel's staging, 32 B each, four in flight per thread;
+//   kept    the kept frames (rare): vertex record, packed offsets and hits.
+// The run summary is accumulated per thread and flushed once per warp.
 #ifndef M3E_PACK_MIN_BLOCKS
-#define M3E_PACK_MIN_BLOCKS 3   // 80 registers, no spills (4 CTAs: 64 registers and spills, 1.23 ms against 1.10)
+#define M3E_PACK_MIN_BLOCKS 3   // 80 registers, no spills (4 CTAs: 64 registers and spills, slower)
 #endif
 struct PackSmem {
     uint32_t wagg[kWarps][3];
@@ -1179,25 +1187,87 @@ struct PackSmem {
     uint32_t tile;
     uint32_t ptrk[kPackTile + 1];   // exclusive prefix of the tile's tracks per warp-batch (+ total)
     uint32_t pkept[kPackTile];      // ... of its kept frames
-    uint32_t src[kPackTile];        // first track's source: store index, or staging index | 1 << 31
+    uint32_t src[kPackTile];        // first track's source: store index, or staging index | 1 << 31 (fused)
+    uint32_t sw[kPackTile * kFB];   // per frame of the tile: selection word,
+    uint32_t fw[kPackTile * kFB];   // track / vertex word,
+    uint16_t ftrk[kPackTile * kFB]; // output tracks -> exclusive prefix inside its warp-batch,
+    uint16_t fhit[kPackTile * kFB]; // hits if kept,
+    uint8_t fkept[kPackTile * kFB]; // kept flag -> exclusive prefix inside its warp-batch
 };
 
-__global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(const KArgs A) {
-    __shared__ PackSmem S;
+size_t pack_smem_bytes() { return sizeof(PackSmem); }
+
+__global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(const __grid_constant__ KArgs A) {
+    extern __shared__ __align__(16) uint8_t pack_smem_raw[];
+    PackSmem& S = *reinterpret_cast<PackSmem*>(pack_smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned lt = (1u << lane) - 1u;
     const m3e_outputs& O = A.out;
+    const DevParams& P = A.P;
     const uint32_t ntiles = (A.nbatch + kPackTile - 1) / kPackTile;
     const uint32_t fb = (uint32_t)A.fb;
+    uint32_t acc[10] = {};   // run summary of this thread: kept_by_reason[6], cand, frames, tracks, hits
+    bool overflow = false;
     for (;;) {
         if (tid == 0) S.tile = atomicAdd(A.ticket + 3, 1u);
         __syncthreads();
         const uint32_t t = S.tile;
         if (t >= ntiles) break;
         const uint32_t b = t * kPackTile + tid;
-        BatchStat bs = {};
-        if (b < A.nbatch) bs = A.bstat[b];
-        // block-wide scan of the three counts: warp-inclusive scans + warp totals
-        uint32_t it = bs.n_trk, ik = bs.n_kept, ih = bs.n_hits;
+        const bool inb = b < A.nbatch;
+        const bool fused = inb && (!A.bsel || A.bsel[b] == kSpilled);   // outputs staged by the fused kernel
+        uint32_t n_trk = 0, n_kept = 0, n_hits = 0, s_kept = 0, src = 0;
+        if (fused) {
+            const BatchStat bs = A.bstat[b];
+            n_trk = bs.n_trk;
+            n_kept = bs.n_kept;
+            n_hits = bs.n_hits;
+            s_kept = bs.s_kept;
+            src = bs.s_trk | 0x80000000u;
+        } else if (inb) {
+            src = A.bsel[b];
+        }
+        S.src[tid] = src;
+        __syncthreads();
+        const uint32_t f0 = t * kPackTile * fb;
+        const uint32_t f1 = min(A.F, (t + 1) * kPackTile * fb);
+        // per frame (coalesced): the words, its output tracks, kept flag and hits
+        for (uint32_t f = f0 + tid; f < f1; f += kThreads) {
+            const uint32_t i = f - f0;
+            if (S.src[i / fb] >> 31) continue;   // the fused kernel's frame
+            const uint32_t sw = A.sel[f], w = A.fw[f];
+            const int reason = (int)(w >> 24);
+            const bool kept = reason != M3E_REASON_NONE;
+            const bool has_tracks = reason != M3E_REASON_TRIPLET_OVERFLOW && reason != M3E_REASON_INVALID;
+            const uint32_t o_trk = has_tracks ? min(w & 0xFFu, (uint32_t)P.max_tracks) : 0u;
+            const uint32_t nh = kept ? A.offsets[4 * (size_t)f + 4] - A.offsets[4 * (size_t)f] : 0u;
+            S.sw[i] = sw;
+            S.fw[i] = w;
+            S.ftrk[i] = (uint16_t)o_trk;
+            S.fhit[i] = (uint16_t)nh;
+            S.fkept[i] = kept ? 1 : 0;
+            acc[reason < 6 ? reason : 5] += 1u;
+            acc[6] += (sw >> 16) == M3E_REASON_NONE ? (sw & 0xFFFFu) : 0u;   // candidates stored
+            acc[7] += 1u;
+            acc[8] += o_trk;
+            acc[9] += nh;
+        }
+        __syncthreads();
+        // per warp-batch: sums, and the per-frame counts turned into in-batch prefixes
+        if (inb && !fused) {
+            const uint32_t nf = min(A.F - b * fb, fb);
+            for (uint32_t j = 0; j < nf; ++j) {
+                const uint32_t i = tid * fb + j;
+                const uint32_t ot = S.ftrk[i], ok = S.fkept[i];
+                S.ftrk[i] = (uint16_t)n_trk;
+                S.fkept[i] = (uint8_t)n_kept;
+                n_trk += ot;
+                n_kept += ok;
+                n_hits += S.fhit[i];
+            }
+        }
+        // block-wide scan of the three counts, then the look-back
+        uint32_t it = n_trk, ik = n_kept, ih = n_hits;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t a = __shfl_up_sync(0xffffffffu, it, o);
@@ -1217,13 +1287,42 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
         }
         uint32_t w0 = 0, w1 = 0, w2 = 0;   // this warp's offset inside the tile
         for (int w = 0; w < warp; ++w) { w0 += S.wagg[w][0]; w1 += S.wagg[w][1]; w2 += S.wagg[w][2]; }
-        S.ptrk[tid] = w0 + it - bs.n_trk;
-        S.pkept[tid] = w1 + ik - bs.n_kept;
-        S.src[tid] = bs.s_trk == kSpilled ? bs.c_base : (bs.s_trk | 0x80000000u);
+        S.ptrk[tid] = w0 + it - n_trk;
+        S.pkept[tid] = w1 + ik - n_kept;
         if (tid == kThreads - 1) S.ptrk[kPackTile] = w0 + it;
         __syncthreads();
         const uint32_t base_trk = S.base[0], base_kept = S.base[1];
-        bool overflow = false;
+        const uint32_t g_kept_b = base_kept + w1 + ik - n_kept, g_hits_b = S.base[2] + w2 + ih - n_hits;
+        // ---- frame records, once, with call-global indices
+        {
+            for (uint32_t f = f0 + tid; f < f1; f += kThreads) {
+                const uint32_t i = f - f0, bl = i / fb;
+                if (S.src[bl] >> 31) {   // fused kernel's record: batch-relative indices
+                    if (O.frames) {
+                        uint2* p = reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(O.frames + f) + 8);
+                        uint2 w = *p;
+                        w.x += base_trk + S.ptrk[bl];
+                        if (w.y != 0xFFFFFFFFu) w.y += base_kept + S.pkept[bl];
+                        *p = w;
+                    }
+                    continue;
+                }
+                const uint32_t sw = S.sw[i], w = S.fw[i];
+                const int reason = (int)(w >> 24);
+                if (O.reason) O.reason[f] = (uint8_t)reason;
+                if (O.frames) {
+                    m3e_frame_out fo;
+                    fo.n_cand = (uint16_t)(sw & 0xFFFFu);
+                    fo.n_tracks = (uint16_t)(w & 0xFFu);
+                    fo.n_combs = (uint16_t)((w >> 16) & 0xFFu);
+                    fo.reason = (uint8_t)reason;
+                    fo.n_neg = (uint8_t)((w >> 8) & 0xFFu);
+                    fo.track_first = base_trk + S.ptrk[bl] + S.ftrk[i];
+                    fo.kept_index = reason != M3E_REASON_NONE ? base_kept + S.pkept[bl] + S.fkept[i] : 0xFFFFFFFFu;
+                    O.frames[f] = fo;
+                }
+            }
+        }
         // ---- tracks: flat over the tile's output, 4 tracks in flight per thread
         if (O.tracks && A.stage_trk) {
             const uint32_t T = S.ptrk[kPackTile];
@@ -1262,103 +1361,112 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
                 }
             }
         }
-        // ---- frame records: warp-batch relative indices -> call global
-        if (O.frames) {
-            const uint32_t f0 = t * kPackTile * fb;
-            const uint32_t f1 = min(A.F, (t + 1) * kPackTile * fb);
-            for (uint32_t fa = f0 + tid; fa < f1; fa += 4 * kThreads) {   // 4 records in flight
-                uint2 w[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t f = fa + u * kThreads;
-                    if (f < f1) w[u] = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(O.frames + f) + 8);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t f = fa + u * kThreads;
-                    if (f >= f1) continue;
-                    const uint32_t bl = (f - f0) / fb;   // {track_first, kept_index} of the record
-                    w[u].x += base_trk + S.ptrk[bl];
-                    if (w[u].y != 0xFFFFFFFFu) w[u].y += base_kept + S.pkept[bl];
-                    *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(O.frames + f) + 8) = w[u];
-                }
-            }
-        }
-        // ---- kept frames (rare): each warp takes its 32 warp-batches that keep any
-        {
-            uint32_t g_hits = S.base[2];
-            for (int w = 0; w < warp; ++w) g_hits += S.wagg[w][2];
-            const uint32_t eb_hits = g_hits + ih - bs.n_hits;   // this lane's warp-batch
-            unsigned todo = __ballot_sync(0xffffffffu, bs.n_kept > 0);
-            while (todo) {
-                const int srcl = __ffs(todo) - 1;
-                todo &= todo - 1;
-                const uint32_t n_kept = __shfl_sync(0xffffffffu, bs.n_kept, srcl);
-                const uint32_t s_kept = __shfl_sync(0xffffffffu, bs.s_kept, srcl);
-                const uint32_t g_kept = base_kept + S.pkept[warp * 32 + srcl];
-                uint32_t gh = __shfl_sync(0xffffffffu, eb_hits, srcl);
-                for (uint32_t k0 = 0; k0 < n_kept; k0 += 32) {
-                    const uint32_t k = k0 + lane;
-                    uint32_t f = 0, nh = 0, lo = 0;
-                    const bool valid = k < n_kept && s_kept + k < A.stage_kept_cap;
-                    KeptRec kr;
+        // ---- kept frames (rare): each warp takes its warp-batches that keep any;
+        // the lanes are that warp-batch's frames (fit path) or its staged records
+        unsigned todo = __ballot_sync(0xffffffffu, n_kept > 0);
+        while (todo) {
+            const int sl = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t bb = t * kPackTile + warp * 32 + sl;
+            const bool bfused = __shfl_sync(0xffffffffu, fused ? 1u : 0u, sl) != 0u;
+            const uint32_t nk = __shfl_sync(0xffffffffu, n_kept, sl);
+            const uint32_t sk = __shfl_sync(0xffffffffu, s_kept, sl);
+            const uint32_t gk = __shfl_sync(0xffffffffu, g_kept_b, sl);
+            uint32_t gh = __shfl_sync(0xffffffffu, g_hits_b, sl);
+            const uint32_t nfb = min(A.F - bb * fb, fb);
+            for (uint32_t k0 = 0; k0 < (bfused ? nk : nfb); k0 += 32) {
+                const uint32_t k = k0 + lane;
+                uint32_t f = 0, nh = 0, lo = 0;
+                bool valid = false;
+                m3e_vertex vx;
+                if (bfused) {   // staged kept records of the fused kernel
+                    valid = k < nk && sk + k < A.stage_kept_cap;
+                    if (k < nk && !valid) overflow = true;
                     if (valid) {
-                        kr = A.stage_kept[s_kept + k];
+                        const KeptRec kr = A.stage_kept[sk + k];
                         f = kr.frame;
-                        lo = A.offsets[4 * (size_t)f];
-                        nh = A.offsets[4 * (size_t)f + 4] - lo;
+                        vx = kr.v;
                     }
-                    if (k < n_kept && !valid) overflow = true;
-                    uint32_t inc = nh;   // prefix of the kept frames' hit counts
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
-                        if (lane >= o) inc += a;
-                    }
-                    const uint32_t hb = gh + inc - nh;
-                    const uint32_t kidx = g_kept + k;
+                } else if (k < nfb) {   // the warp-batch's frames
+                    f = bb * fb + k;
+                    const uint32_t w = S.fw[(warp * 32 + sl) * fb + k];
+                    const int reason = (int)(w >> 24);
+                    valid = reason != M3E_REASON_NONE;
                     if (valid) {
-                        if (kidx < O.kept_capacity) {
-                            if (O.kept_frame) O.kept_frame[kidx] = f;
-                            if (O.vertices) O.vertices[kidx] = kr.v;
-                            if (O.kept_offsets)
-                                for (int l = 0; l < 4; ++l)
-                                    O.kept_offsets[4 * (size_t)kidx + l] = hb + (A.offsets[4 * (size_t)f + l] - lo);
+                        if (reason == M3E_REASON_VERTEX) {
+                            vx = A.vrec[A.vk[f]];
                         } else {
-                            overflow = true;
+                            vx = m3e_vertex{};
+                            vx.frame = 0xFFFFFFFFu;
                         }
                     }
-                    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-                    if (O.kept_x) {
-                        for (int s2 = 0; s2 < 32; ++s2) {
-                            if (k0 + s2 >= n_kept) break;
-                            const uint32_t fl = __shfl_sync(0xffffffffu, lo, s2);
-                            const uint32_t fn = __shfl_sync(0xffffffffu, nh, s2);
-                            const uint32_t fh = __shfl_sync(0xffffffffu, hb, s2);
-                            for (uint32_t e = lane; e < fn; e += 32) {
-                                const uint32_t dst = fh + e;
-                                if (dst < O.kept_hit_capacity) {
-                                    O.kept_x[dst] = A.x[fl + e];
-                                    O.kept_y[dst] = A.y[fl + e];
-                                    O.kept_z[dst] = A.z[fl + e];
-                                } else {
-                                    overflow = true;
-                                }
+                }
+                const unsigned mk = __ballot_sync(0xffffffffu, valid);
+                if (valid) {
+                    lo = A.offsets[4 * (size_t)f];
+                    nh = A.offsets[4 * (size_t)f + 4] - lo;
+                }
+                const uint32_t inc = warp_incl(nh);   // prefix of the kept frames' hit counts
+                const uint32_t hb = gh + inc - nh;
+                const uint32_t kidx = gk + (bfused ? k : (uint32_t)__popc(mk & lt));
+                if (valid) {
+                    if (kidx < O.kept_capacity) {
+                        if (O.kept_frame) O.kept_frame[kidx] = f;
+                        if (O.vertices) O.vertices[kidx] = vx;
+                        if (O.kept_offsets)
+                            for (int l = 0; l < 4; ++l)
+                                O.kept_offsets[4 * (size_t)kidx + l] = hb + (A.offsets[4 * (size_t)f + l] - lo);
+                    } else {
+                        overflow = true;
+                    }
+                }
+                if (O.kept_x) {
+                    unsigned mm = mk;
+                    while (mm) {
+                        const int s2 = __ffs(mm) - 1;
+                        mm &= mm - 1;
+                        const uint32_t fl = __shfl_sync(0xffffffffu, lo, s2);
+                        const uint32_t fn = __shfl_sync(0xffffffffu, nh, s2);
+                        const uint32_t fh = __shfl_sync(0xffffffffu, hb, s2);
+                        for (uint32_t e = lane; e < fn; e += 32) {
+                            const uint32_t dst = fh + e;
+                            if (dst < O.kept_hit_capacity) {
+                                O.kept_x[dst] = A.x[fl + e];
+                                O.kept_y[dst] = A.y[fl + e];
+                                O.kept_z[dst] = A.z[fl + e];
+                            } else {
+                                overflow = true;
                             }
                         }
                     }
-                    gh += tot;
                 }
-            }
-            // the call's last warp-batch closes the packed offsets
-            if (b == A.nbatch - 1 && O.kept_offsets) {
-                const uint32_t K = base_kept + S.pkept[tid] + bs.n_kept;
-                if (K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = eb_hits + bs.n_hits;
+                gh += __shfl_sync(0xffffffffu, inc, 31);
+                if (!bfused) break;   // a warp-batch has at most 32 frames (fb <= kFB)
             }
         }
-        if (__any_sync(0xffffffffu, overflow) && lane == 0 && O.summary)
-            atomicExch((unsigned long long*)&O.summary->overflow, 1ull);
+        // the call's last warp-batch closes the packed offsets
+        if (inb && b == A.nbatch - 1 && O.kept_offsets) {
+            const uint32_t K = g_kept_b + n_kept;
+            if (K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = g_hits_b + n_hits;
+        }
         __syncthreads();
+    }
+    // run summary: one flush per warp (the fused kernel flushed its own frames)
+    uint32_t sacc[12];
+#pragma unroll
+    for (int r = 0; r < 10; ++r) sacc[r] = warp_sum(acc[r]);
+    sacc[10] = __any_sync(0xffffffffu, overflow) ? 1u : 0u;
+    sacc[11] = 0;
+    if (lane == 0 && O.summary) {
+        uint32_t fl[12];
+        for (int r = 0; r < 6; ++r) fl[r] = sacc[r];
+        fl[6] = sacc[6];
+        fl[7] = sacc[7];
+        fl[8] = sacc[8];
+        fl[9] = sacc[9];
+        fl[10] = sacc[10];
+        fl[11] = 0;
+        flush_summary(O.summary, fl);
     }
 }
 
@@ -1651,70 +1759,9 @@ __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel
     }
 }
 
-// ------------------------------------------- tracks / vertex / finish kernels ----
-// Split path, V + O for the warp-batches fitted by fit_kernel (which also ran
-// the track stage T), as kernels without out-of-line calls in their loops and
-// with their hot code in the instruction cache:
-//   vertex_kernel  V: one warp per listed frame, fp64 (Alg. 4);
-//   finish_kernel  O: frame records in place (warp-batch relative offsets),
-//                  kept-frame records, BatchStat per warp-batch.
-// Results are identical to the fused kernel's stages T, V and O.
-
-// group of G warp-batches of one warp, lane = frame (shared by T and O)
-struct Group {
-    uint32_t g, b, f, gb, cex, cin, nst;
-    int ncand, reason;
-    bool inb, active;
-};
-
-// raw per-lane words of a group, fetched one iteration ahead (software pipelining
-// of the lane-per-frame loops: their loads are independent of the current group)
-struct GroupRaw {
-    uint32_t gb, w, fw;
-};
-
-template <bool kFw>
-__device__ __forceinline__ GroupRaw fetch_group(const KArgs& A, uint32_t g, int fb, int G, int bl, int fl) {
-    const int lane = threadIdx.x & 31;
-    GroupRaw r;
-    r.gb = kSpilled;
-    r.w = 0u;
-    r.fw = 0u;
-    const uint32_t b = g * (uint32_t)G + (uint32_t)bl;
-    const uint32_t f = b * (uint32_t)fb + (uint32_t)(lane - fl);
-    if (bl < G && b < A.nbatch) {
-        r.gb = A.bsel[b];
-        if (f < A.F) {
-            r.w = A.sel[f];
-            if (kFw) r.fw = A.fw[f];
-        }
-    }
-    return r;
-}
-
-__device__ __forceinline__ Group make_group(const KArgs& A, uint32_t g, const GroupRaw& r, int fb, int G, int bl,
-                                            int fl) {
-    const int lane = threadIdx.x & 31;
-    Group q;
-    q.g = g;
-    q.b = g * (uint32_t)G + (uint32_t)bl;
-    q.f = q.b * (uint32_t)fb + (uint32_t)(lane - fl);
-    q.inb = bl < G && q.b < A.nbatch;
-    q.gb = r.gb;
-    q.active = q.inb && q.gb != kSpilled && q.f < A.F;   // spilled warp-batches: fused kernel
-    q.ncand = 0;
-    q.reason = M3E_REASON_NONE;
-    q.nst = 0;
-    if (q.active) {
-        q.ncand = (int)(r.w & 0xFFFFu);
-        q.reason = (int)(r.w >> 16);
-        q.nst = q.reason == M3E_REASON_NONE ? (uint32_t)q.ncand : 0u;
-    }
-    // store entries of the frame: warp-batch base + prefix within the warp-batch
-    q.cex = warp_incl(q.nst) - q.nst;
-    q.cin = q.cex + q.nst;
-    return q;
-}
+// ------------------------------------------------------------- vertex kernels ----
+// Split path, V for the frames the fit kernel's track stage listed (the output
+// stage O is the pack kernel); results identical to the fused kernel's stage V.
 
 // V, three kernels over the frames the track stage listed (Alg. 4,
 // Sec. IV-C; same arithmetic and order as vertex_frame):
@@ -1941,123 +1988,6 @@ __global__ void __launch_bounds__(kThreads) vpost_kernel(const __grid_constant__
     }
 }
 
-struct FinishSmem {
-    uint32_t acc[kWarps][12];
-};
-
-#ifndef M3E_FINISH_MIN_BLOCKS
-#define M3E_FINISH_MIN_BLOCKS 4   // measured 6 / 5 / 4: 0.30 / 0.27 / 0.25 ms (40 registers spill)
-#endif
-__global__ void __launch_bounds__(kThreads, M3E_FINISH_MIN_BLOCKS) finish_kernel(const __grid_constant__ KArgs A) {
-    __shared__ FinishSmem S;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const DevParams& P = A.P;
-    if (lane < 12) S.acc[warp][lane] = 0u;
-    __syncwarp();
-    const m3e_outputs& O = A.out;
-    const int fb = A.fb, G = 32 / fb, bl = lane / fb, fl = bl * fb;
-    const uint32_t ngroups = (A.nbatch + G - 1) / G;
-    bool overflow = false;
-    // static round-robin over groups, the next group's words fetched ahead
-    const uint32_t nw = gridDim.x * kWarps;
-    uint32_t g = blockIdx.x * kWarps + warp;
-    GroupRaw rn = fetch_group<true>(A, g, fb, G, bl, fl);
-    for (; g < ngroups; g += nw) {
-        const uint32_t fwv = rn.fw;
-        const Group q = make_group(A, g, rn, fb, G, bl, fl);
-        rn = fetch_group<true>(A, g + nw, fb, G, bl, fl);
-        int ntrk = 0, nneg = 0, ncomb = 0, reason = q.reason;
-        if (q.active) {
-            const uint32_t w = fwv;
-            ntrk = (int)(w & 0xFFu);
-            nneg = (int)((w >> 8) & 0xFFu);
-            ncomb = (int)((w >> 16) & 0xFFu);
-            reason = (int)(w >> 24);
-        }
-        const bool kept = q.active && reason != M3E_REASON_NONE;
-        const bool has_tracks = q.active && reason != M3E_REASON_TRIPLET_OVERFLOW && reason != M3E_REASON_INVALID;
-        const uint32_t o_trk = has_tracks ? (uint32_t)min(ntrk, P.max_tracks) : 0u;
-        const uint32_t o_kept = kept ? 1u : 0u;
-        uint32_t o_hits = 0;
-        if (kept) o_hits = A.offsets[4 * (size_t)q.f + 4] - A.offsets[4 * (size_t)q.f];
-        const uint32_t i_trk = warp_incl(o_trk), i_kept = warp_incl(o_kept), i_hits = warp_incl(o_hits);
-        const uint32_t e_trk = i_trk - o_trk, e_kept = i_kept - o_kept, e_hits = i_hits - o_hits;
-        const uint32_t t_trk = __shfl_sync(0xffffffffu, i_trk, 31), t_kept = __shfl_sync(0xffffffffu, i_kept, 31);
-        const uint32_t t_hits = __shfl_sync(0xffffffffu, i_hits, 31);
-        // a warp-batch's output tracks (each frame's first max_tracks accepted) are
-        // the front of its store segment (fit kernel): the pack kernel copies them
-        uint32_t s_kept = 0;
-        if (lane == 0 && t_kept) s_kept = atomicAdd(A.ticket + 2, t_kept);
-        s_kept = __shfl_sync(0xffffffffu, s_kept, 0);
-        const uint32_t b_trk = __shfl_sync(0xffffffffu, e_trk, fl), b_kept = __shfl_sync(0xffffffffu, e_kept, fl);
-        const uint32_t b_hits = __shfl_sync(0xffffffffu, e_hits, fl);
-        if (q.active) {
-            if (O.reason) O.reason[q.f] = (uint8_t)reason;
-            if (O.frames) {
-                m3e_frame_out fo;
-                fo.n_cand = (uint16_t)q.ncand;
-                fo.n_tracks = (uint16_t)ntrk;
-                fo.n_combs = (uint16_t)ncomb;
-                fo.reason = (uint8_t)reason;
-                fo.n_neg = (uint8_t)nneg;
-                fo.track_first = e_trk - b_trk;
-                fo.kept_index = kept ? e_kept - b_kept : 0xFFFFFFFFu;
-                O.frames[q.f] = fo;
-            }
-            if (kept) {
-                const uint32_t k = s_kept + e_kept;
-                if (k < A.stage_kept_cap) {
-                    KeptRec kr;
-                    kr.frame = q.f;
-                    kr.pad = 0;
-                    if (reason == M3E_REASON_VERTEX) {
-                        kr.v = A.vrec[A.vk[q.f]];
-                    } else {
-                        kr.v = m3e_vertex{};
-                        kr.v.frame = 0xFFFFFFFFu;
-                    }
-                    A.stage_kept[k] = kr;
-                } else {
-                    overflow = true;
-                }
-            }
-        }
-        // BatchStat of each fitted warp-batch (written by its first lane)
-        const int ll = fl + fb - 1;   // last lane of the warp-batch (frames past F are inactive: 0)
-        const uint32_t l_trk = __shfl_sync(0xffffffffu, i_trk, ll & 31);
-        const uint32_t l_kept = __shfl_sync(0xffffffffu, i_kept, ll & 31);
-        const uint32_t l_hits = __shfl_sync(0xffffffffu, i_hits, ll & 31);
-        if (q.inb && q.gb != kSpilled && lane == fl) {
-            BatchStat bs;
-            bs.n_trk = l_trk - b_trk;
-            bs.n_kept = l_kept - b_kept;
-            bs.n_hits = l_hits - b_hits;
-            bs.s_trk = kSpilled;   // kSpilled: its tracks are the front of its store segment
-            bs.s_kept = s_kept + b_kept;
-            bs.nf = min(A.F - q.b * (uint32_t)fb, (uint32_t)fb);
-            bs.c_base = q.gb;
-            bs.c_n = bs.n_trk;
-            A.bstat[q.b] = bs;
-        }
-        // run summary (per-warp counters in shared memory)
-        uint32_t kr[6];
-#pragma unroll
-        for (int r = 0; r < 6; ++r) kr[r] = __popc(__ballot_sync(0xffffffffu, q.active && reason == r));
-        const uint32_t c_cand = warp_sum(q.nst), c_frames = __popc(__ballot_sync(0xffffffffu, q.active));
-        if (lane == 0) {
-            for (int r = 0; r < 6; ++r) S.acc[warp][r] += kr[r];
-            S.acc[warp][6] += c_cand;
-            S.acc[warp][7] += c_frames;
-            S.acc[warp][8] += t_trk;
-            S.acc[warp][9] += t_hits;
-        }
-        __syncwarp();
-    }
-    if (__any_sync(0xffffffffu, overflow) && lane == 0) S.acc[warp][10] = 1u;
-    __syncwarp();
-    if (lane == 0 && A.out.summary) flush_summary(A.out.summary, S.acc[warp]);
-}
-
 // host path: add the chunk's bases to its device outputs before they are copied
 __global__ void rebase_kernel(const Rebase r) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -2080,11 +2010,6 @@ __global__ void rebase_kernel(const Rebase r) {
 
 cudaError_t launch_rebase(const Rebase& r, int sms, cudaStream_t s) {
     rebase_kernel<<<sms * 4, kThreads, 0, s>>>(r);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s) {
-    finish_kernel<<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -2115,11 +2040,6 @@ int vertex_blocks_per_sm() {
     return n > 0 ? n : 1;
 }
 
-int finish_blocks_per_sm() {
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, finish_kernel, kThreads, 0) != cudaSuccess) return 1;
-    return n > 0 ? n : 1;
-}
 
 cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s) {
     const size_t smem = 2 * kFitWarps * sizeof(FitSlot) + kFitWarps * sizeof(FitPre);
@@ -2139,7 +2059,10 @@ int fit_blocks_per_sm() {
 }
 
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s) {
-    pack_kernel<<<grid, kThreads, 0, s>>>(a);
+    const size_t smem = sizeof(PackSmem);
+    cudaError_t e = cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    pack_kernel<<<grid, kThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

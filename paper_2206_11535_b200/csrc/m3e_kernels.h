@@ -22,7 +22,7 @@ constexpr size_t kVResBytes = 56;         // sizeof(VRes) (phase-2 vertex result
 
 // kModeSelectC: the Selection Cuts alone, candidates written compactly to the
 // candidate store (first kernel of the split production path: select -> fit ->
-// finish -> fused kernel over the spilled warp-batches only -> pack)
+// vertex -> fused kernel over the spilled warp-batches only -> pack)
 enum { kModeFull = 0, kModeSelect = 1, kModeFit = 2, kModeVertex = 3, kModePack = 4, kModeSelectC = 5 };
 constexpr uint32_t kSpilled = 0xFFFFFFFFu;   // bsel[] entry of a warp-batch whose candidates did not fit
 
@@ -64,10 +64,10 @@ struct KArgs {
     uint32_t* ticket;      // counters (zeroed before the launch): [0] select warp-batch ticket, [1] staged
                            // tracks, [2] staged kept frames, [3] pack-kernel tile ticket, [4] filter
                            // warp-batch ticket, [5] spilled warp-batches, [6..7] candidate-store fill (u64),
-                           // [8] fit-kernel unit ticket, [9] vertex-list fill, [10] finish-kernel
+                           // [8] fit-kernel unit ticket, [9] vertex-list fill, [10] (unused)
                            // group ticket, [11] triple-list fill
     uint32_t* bticket;     // this launch's warp-batch ticket (ticket + 0 or ticket + 4)
-    // candidate store of the split path (kModeSelectC writes, fit_kernel / finish_kernel read)
+    // candidate store of the split path (kModeSelectC writes, fit_kernel reads)
     uint32_t* spill_out;   // kModeSelectC: appends the warp-batches that did not fit (count in ticket[5])
     uint32_t* spill_list;  // kModeFull, non-NULL: process only these warp-batches
     uint4* cand_g;         // {first hit of the frame, frame, offsets of h1 | h2 << 16 and of h0 inside the
@@ -78,7 +78,7 @@ struct KArgs {
     uint64_t cand_cap;     // entries of cand_g (< 2^32)
     uint32_t* sel;         // [F] per frame: n_cand | reason << 16
     uint32_t* fw;          // [F] per frame after the track stage: n_tracks | n_neg << 8 | n_combs << 16 |
-                           // reason << 24 (fit_kernel writes, vertex_kernel updates, finish_kernel reads)
+                           // reason << 24 (fit_kernel writes, vertex_kernel updates, pack_kernel reads)
     uint32_t* vk;          // [F] vertex_kernel: list position of a frame's vertex (reason VERTEX only)
     uint2* vlist;          // frames for the vertex stage {frame, first store entry}, count in ticket[9]
     m3e_vertex* vrec;      // vertex of vlist entry k
@@ -137,8 +137,6 @@ cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStre
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s);
 int fit_blocks_per_sm();
-cudaError_t launch_finish(const KArgs& a, int grid, cudaStream_t s);
-int finish_blocks_per_sm();
 cudaError_t launch_vertex(const KArgs& a, int grid, int sms, cudaStream_t s);
 int vertex_blocks_per_sm();
 int triple_blocks_per_sm();

@@ -392,7 +392,6 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     const int grid = (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * bps);
     const int sgrid = split ? (int)std::min<uint64_t>(nbatch, (uint64_t)ctx->sms * blocks_per_sm(kModeSelectC, big))
                             : 0;
-    const int fgrid = split ? ctx->sms * finish_blocks_per_sm() : 0;
     const int vgrid = split ? ctx->sms * vertex_blocks_per_sm() : 0;   // its warps own vscratch / pool slots
     rc = ensure_ws(ctx, w, nbatch, p, fb, std::max(std::max(grid, sgrid), vgrid));
     if (rc) return rc;
@@ -463,7 +462,6 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         if (tm) CK(cudaEventRecord(ev[3], s));
         CK(launch_vertex(a, vgrid, ctx->sms, s));
         if (tm) CK(cudaEventRecord(ev[4], s));
-        CK(launch_finish(a, fgrid, s));
         a.spill_list = w.spill;   // the fused kernel takes only the spilled warp-batches
         a.bticket = w.ticket + 4;
     } else if (tm) {
