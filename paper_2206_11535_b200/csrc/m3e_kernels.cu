@@ -1231,26 +1231,38 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
         __syncthreads();
         const uint32_t f0 = t * kPackTile * fb;
         const uint32_t f1 = min(A.F, (t + 1) * kPackTile * fb);
-        // per frame (coalesced): the words, its output tracks, kept flag and hits
-        for (uint32_t f = f0 + tid; f < f1; f += kThreads) {
-            const uint32_t i = f - f0;
-            if (S.src[i / fb] >> 31) continue;   // the fused kernel's frame
-            const uint32_t sw = A.sel[f], w = A.fw[f];
-            const int reason = (int)(w >> 24);
-            const bool kept = reason != M3E_REASON_NONE;
-            const bool has_tracks = reason != M3E_REASON_TRIPLET_OVERFLOW && reason != M3E_REASON_INVALID;
-            const uint32_t o_trk = has_tracks ? min(w & 0xFFu, (uint32_t)P.max_tracks) : 0u;
-            const uint32_t nh = kept ? A.offsets[4 * (size_t)f + 4] - A.offsets[4 * (size_t)f] : 0u;
-            S.sw[i] = sw;
-            S.fw[i] = w;
-            S.ftrk[i] = (uint16_t)o_trk;
-            S.fhit[i] = (uint16_t)nh;
-            S.fkept[i] = kept ? 1 : 0;
-            acc[reason < 6 ? reason : 5] += 1u;
-            acc[6] += (sw >> 16) == M3E_REASON_NONE ? (sw & 0xFFFFu) : 0u;   // candidates stored
-            acc[7] += 1u;
-            acc[8] += o_trk;
-            acc[9] += nh;
+        // per frame (coalesced): the words, its output tracks, kept flag and hits;
+        // the loads of four strided frames issued before any is used
+        for (uint32_t fa = f0 + tid; fa < f1; fa += 4 * kThreads) {
+            uint32_t swv[4], wv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t f = fa + u * kThreads;
+                const bool on = f < f1 && !(S.src[(f - f0) / fb] >> 31);   // not the fused kernel's frame
+                swv[u] = on ? A.sel[f] : 0xFFFFFFFFu;
+                wv[u] = on ? A.fw[f] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t f = fa + u * kThreads;
+                if (swv[u] == 0xFFFFFFFFu) continue;
+                const uint32_t i = f - f0, sw = swv[u], w = wv[u];
+                const int reason = (int)(w >> 24);
+                const bool kept = reason != M3E_REASON_NONE;
+                const bool has_tracks = reason != M3E_REASON_TRIPLET_OVERFLOW && reason != M3E_REASON_INVALID;
+                const uint32_t o_trk = has_tracks ? min(w & 0xFFu, (uint32_t)P.max_tracks) : 0u;
+                const uint32_t nh = kept ? A.offsets[4 * (size_t)f + 4] - A.offsets[4 * (size_t)f] : 0u;
+                S.sw[i] = sw;
+                S.fw[i] = w;
+                S.ftrk[i] = (uint16_t)o_trk;
+                S.fhit[i] = (uint16_t)nh;
+                S.fkept[i] = kept ? 1 : 0;
+                acc[reason < 6 ? reason : 5] += 1u;
+                acc[6] += (sw >> 16) == M3E_REASON_NONE ? (sw & 0xFFFFu) : 0u;   // candidates stored
+                acc[7] += 1u;
+                acc[8] += o_trk;
+                acc[9] += nh;
+            }
         }
         __syncthreads();
         // per warp-batch: sums, and the per-frame counts turned into in-batch prefixes
