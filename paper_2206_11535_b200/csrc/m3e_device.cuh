@@ -89,6 +89,13 @@ M3E_HD float2 fma2(float2 a, float2 b, float2 c) {
     return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
 #endif
 }
+M3E_HD float2 add2(float2 a, float2 b) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000 && M3E_PACKED
+    return __fadd2_rn(a, b);
+#else
+    return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
 M3E_HD float2 sqrt2(float2 a) { return make_float2(fsqrt(a.x), fsqrt(a.y)); }
 M3E_HD float2 rcp2(float2 a) { return make_float2(rcp(a.x), rcp(a.y)); }
 
@@ -682,6 +689,7 @@ struct FitOut {
 };
 
 // h0, h1, h2 given; F supplies the frame's layer-3 hits (F.s[3], F.n[3])
+template <bool kPairs = true>
 M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, float3 h1, float3 h2, float rtc) {
     FitOut o;
     o.status = 0; o.hit3 = -1;
@@ -693,14 +701,41 @@ M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, flo
     float3 pred;
     if (!extrapolate(P, h1, h2, T1, pred)) { o.status = 2; return o; }
     if (F.n[3] == 0) { o.status = 3; return o; }
-    // find_closest_layer3_hit: 3D Euclidean, lowest index on ties (R10)
+    // find_closest_layer3_hit: 3D Euclidean, lowest index on ties (R10); every
+    // distance rounded as (dx = x - px) dx dx, fma dy dy, fma dz dz and compared
+    // in index order.  kPairs (phase-I frames, ~6 layer-3 hits that differ between
+    // the lanes' frames): two hits per iteration in packed fp32, half the
+    // divergent trip count; big frames (~56 hits, the same frame on every lane):
+    // one hit per iteration, fewer instructions per hit
     float best = kInfF;
     int bi = 0;
-    for (int i = 0; i < F.n[3]; ++i) {
-        const float3 h = hit(F, 3, i);
-        const float ex = h.x - pred.x, ey = h.y - pred.y, ez = h.z - pred.z;
-        const float d2 = ex * ex + ey * ey + ez * ez;
-        if (d2 < best) { best = d2; bi = i; }
+    {
+        const int n3 = F.n[3];
+        const float* x3 = F.x + F.s[3];
+        const float* y3 = F.y + F.s[3];
+        const float* z3 = F.z + F.s[3];
+        if constexpr (kPairs) {
+            int i = 0;
+            for (; i + 1 < n3; i += 2) {
+                const float2 ex = f2(x3[i] - pred.x, x3[i + 1] - pred.x);
+                const float2 ey = f2(y3[i] - pred.y, y3[i + 1] - pred.y);
+                const float2 ez = f2(z3[i] - pred.z, z3[i + 1] - pred.z);
+                const float2 d2 = fma2(ez, ez, fma2(ey, ey, mul2(ex, ex)));
+                if (d2.x < best) { best = d2.x; bi = i; }
+                if (d2.y < best) { best = d2.y; bi = i + 1; }
+            }
+            if (i < n3) {
+                const float ex = x3[i] - pred.x, ey = y3[i] - pred.y, ez = z3[i] - pred.z;
+                const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+                if (d2 < best) { best = d2; bi = i; }
+            }
+        } else {
+            for (int i = 0; i < n3; ++i) {
+                const float ex = x3[i] - pred.x, ey = y3[i] - pred.y, ez = z3[i] - pred.z;
+                const float d2 = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+                if (d2 < best) { best = d2; bi = i; }
+            }
+        }
     }
     o.hit3 = bi;
     const float3 h3 = hit(F, 3, bi);
@@ -734,8 +769,9 @@ M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, flo
     return o;
 }
 
+template <bool kPairs = true>
 M3E_HD FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, int i2, float rtc) {
-    return fit_candidate_h(P, F, hit(F, 0, i0), hit(F, 1, i1), hit(F, 2, i2), rtc);
+    return fit_candidate_h<kPairs>(P, F, hit(F, 0, i0), hit(F, 1, i1), hit(F, 2, i2), rtc);
 }
 
 // ------------------------------------------------------------- Vertex Fit ----

@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
                         rt = crt[slot];
                     }
                     const Frame Fv = frame_view(A, W, buf, j);
-                    o = fit_candidate(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
+                    o = fit_candidate<!BIG>(P, Fv, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u, rt);
                 }
                 if constexpr (MODE == kModeFit) {   // per-candidate record (stage tap)
                     if (valid) {
@@ -1628,6 +1628,7 @@ __device__ __forceinline__ void fit_frames(const KArgs& A, FitSlot& S) {
 #define M3E_FIT_MIN_BLOCKS 3   // 80 registers (no spills), 24 warps per SM
 #endif
 constexpr int kFitWarps = M3E_FIT_WARPS;
+template <bool BIG>   // BIG: calls of big frames (phase II), the layer-3 search one hit at a time
 __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel(const __grid_constant__ KArgs A) {
     extern __shared__ __align__(16) uint8_t fit_smem_raw[];
     FitSlot* R = reinterpret_cast<FitSlot*>(fit_smem_raw) + 2 * (threadIdx.x >> 5);   // the warp's two slots
@@ -1720,7 +1721,7 @@ __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel
             const float3 h1 = make_float3(F.x[o1], F.y[o1], F.z[o1]);
             const float3 h2 = make_float3(F.x[o2], F.y[o2], F.z[o2]);
             // r_tc of the selection (Eq. 5, same fp32 code as the selection's)
-            o = fit_candidate_h(P, F, h0, h1, h2, circle_radius(h0, h1, h2));
+            o = fit_candidate_h<!BIG>(P, F, h0, h1, h2, circle_radius(h0, h1, h2));
             e.z = (o1 - (uint32_t)F.s[1]) | ((o2 - (uint32_t)F.s[2]) << 16);   // layer-local h1 | h2
         }
         const bool acc = o.status == 0;
@@ -2053,20 +2054,26 @@ int vertex_blocks_per_sm() {
 }
 
 
-cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s) {
+template <bool BIG>
+static cudaError_t launch_fit_t(const KArgs& a, int grid, cudaStream_t s) {
     const size_t smem = 2 * kFitWarps * sizeof(FitSlot) + kFitWarps * sizeof(FitPre);
-    cudaError_t e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(fit_kernel<BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    fit_kernel<<<grid, 32 * kFitWarps, smem, s>>>(a);
+    fit_kernel<BIG><<<grid, 32 * kFitWarps, smem, s>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_fit(const KArgs& a, bool big, int grid, cudaStream_t s) {
+    return big ? launch_fit_t<true>(a, grid, s) : launch_fit_t<false>(a, grid, s);
 }
 
 int fit_blocks_per_sm() {
     int n = 0;
     const size_t smem = 2 * kFitWarps * sizeof(FitSlot) + kFitWarps * sizeof(FitPre);
-    if (cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(fit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fit_kernel, 32 * kFitWarps, smem) != cudaSuccess) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fit_kernel<false>, 32 * kFitWarps, smem) != cudaSuccess)
+        return 1;
     return n > 0 ? n : 1;
 }
 

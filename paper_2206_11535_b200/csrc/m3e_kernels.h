@@ -135,7 +135,7 @@ cudaError_t launch_rebase(const Rebase& r, int sms, cudaStream_t s);
 size_t smem_bytes();
 cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);
-cudaError_t launch_fit(const KArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_fit(const KArgs& a, bool big, int grid, cudaStream_t s);
 int fit_blocks_per_sm();
 cudaError_t launch_vertex(const KArgs& a, int grid, int sms, cudaStream_t s);
 int vertex_blocks_per_sm();

@@ -457,7 +457,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         a.tri = w.tri;
         a.tres = reinterpret_cast<VRes*>(w.tres);
         a.tri_cap = ctx->tri_cap ? std::min<uint64_t>(ctx->tri_cap, w.tri_n) : w.tri_n;
-        CK(launch_fit(a, ctx->sms * fit_blocks_per_sm(), s));   // F + T (track stage)
+        CK(launch_fit(a, big, ctx->sms * fit_blocks_per_sm(), s));   // F + T (track stage)
         if (tm) CK(cudaEventRecord(ev[2], s));
         if (tm) CK(cudaEventRecord(ev[3], s));
         CK(launch_vertex(a, vgrid, ctx->sms, s));
@@ -467,7 +467,9 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     } else if (tm) {
         for (int k = 1; k <= 4; ++k) CK(cudaEventRecord(ev[k], s));
     }
-    CK(launch_filter(mode, big, a, grid, s));
+    // (split path: only the warp-batches the store could not take, none at phase I:
+    // one CTA per SM is plenty and keeps the empty launch short)
+    CK(launch_filter(mode, big, a, split ? std::min(grid, ctx->sms) : grid, s));
     if (tm) CK(cudaEventRecord(ev[5], s));
     if (packs) {
         const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
