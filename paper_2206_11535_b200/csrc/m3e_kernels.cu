@@ -1506,6 +1506,9 @@ struct __align__(16) FitSlot {
     uint32_t offs[4 * kFB + 4];   // layer offsets of the warp-batch's frames (+ end)
     uint32_t selw[kFB];           // its frames' selection words (cp.async)
     uint64_t bar;
+    const float* px;              // hit arrays as seen by a global hit index: the staged window
+    const float* py;              // shifted by its first hit (generic addresses), or the inputs
+    const float* pz;              // in HBM for a warp-batch larger than the window
     uint32_t b, f0, nf, winlo;    // warp-batch, its frames, first staged hit (0xFFFFFFFF: from HBM)
     uint32_t sbase, n, t, nacc;   // store segment, its entries, entries consumed, output tracks written
     int cnt[kFB], neg[kFB], pos[kFB];   // per frame: accepted, stored e-, stored e+
@@ -1568,6 +1571,10 @@ __device__ __forceinline__ void fit_assign(const KArgs& A, FitSlot& S, FitPre& D
             const uint32_t wlo = lo & ~3u, whi = (hi + 3u) & ~3u;
             const bool inw = whi - wlo <= (uint32_t)kFitHCap;
             S.winlo = inw ? wlo : 0xFFFFFFFFu;
+            const uintptr_t sh = (uintptr_t)wlo * sizeof(float);
+            S.px = inw ? reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(S.hx) - sh) : A.x;
+            S.py = inw ? reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(S.hy) - sh) : A.y;
+            S.pz = inw ? reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(S.hz) - sh) : A.z;
             S.sbase = sb;
             S.n = n;
             S.offs[4 * nf] = hi;
@@ -1696,17 +1703,9 @@ __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel
             // the entry locates the triplet's hits: {first hit of the frame, frame,
             // offsets of h1 | h2 << 16, offset of h0} (inside the frame)
             Frame F;
-            const uint32_t wlo = L.winlo;
-            if (wlo != 0xFFFFFFFFu) {
-                const uint32_t d = e.x - wlo;
-                F.x = L.hx + d;
-                F.y = L.hy + d;
-                F.z = L.hz + d;
-            } else {
-                F.x = A.x + e.x;
-                F.y = A.y + e.x;
-                F.z = A.z + e.x;
-            }
+            F.x = L.px + e.x;
+            F.y = L.py + e.x;
+            F.z = L.pz + e.x;
             const uint32_t* of = L.offs + 4 * j;
             F.s[0] = 0;
             F.s[1] = (int)(of[1] - of[0]);
