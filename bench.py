@@ -365,7 +365,7 @@ def main():
         torch.cuda.synchronize(dev)
         sme = re_.summary_np()
         phys = signal_efficiency(synth.preset(a.workload, seed=a.seed), de, re_.frames_np(n_e),
-                                 re_.tracks_np(int(sme["tracks"])), params.max_tracks)
+                                 re_.tracks_np(int(sme["track_slots"])), params.max_tracks)
         phys["sample_frames"] = n_e
         del re_, de
 
@@ -400,7 +400,7 @@ def main():
                      ("fit", "m3e::fit_kernel", ms_fit, in_bytes + 32 * tracks),
                      ("vertex", "m3e::vertex_kernel+triple_kernel+vpost_kernel", ms_vertex, 0),
                      ("fused_spilled", "m3e::filter_kernel<FULL, BIG=false>", ms_filter, 0),
-                     ("pack", "m3e::pack_kernel", ms_pack, out_bytes)]
+                     ("pack", "m3e::pack_kernel", ms_pack, out_bytes - 32 * tracks)]   # (the fit writes the tracks)
         else:
             names = [("filter", "m3e::filter_kernel<FULL, BIG=%s>" % ("true" if big else "false"), ms_filter,
                       in_bytes + out_bytes), ("pack", "m3e::pack_kernel", ms_pack, out_bytes)]

@@ -122,6 +122,7 @@ typedef struct m3e_summary {
     uint64_t kept_hits;      /* hits written to the packed output */
     uint64_t vertices;
     uint64_t overflow;       /* 1 if an output capacity was exceeded */
+    uint64_t track_slots;    /* extent of the track array: slots used by `tracks` (>= tracks) */
 } m3e_summary;
 
 /* outputs of one filter call (all [dev] for m3e_filter, [host] for m3e_filter_host;
@@ -129,7 +130,15 @@ typedef struct m3e_summary {
 typedef struct m3e_outputs {
     uint8_t* reason;              /* [F] M3E_REASON_* per frame (the accept flags) */
     m3e_frame_out* frames;        /* [F] */
-    m3e_track* tracks;            /* [track_capacity], frame-ordered */
+    m3e_track* tracks;            /* [track_capacity], frame-ordered with unused slots: frame f's
+                                     tracks are tracks[track_first .. track_first + min(n_tracks,
+                                     max_tracks)); the frames are grouped in warp-batches of
+                                     consecutive frames, each owning sum over its frames of
+                                     min(n_cand, max_tracks) slots (0 for triplet-overflow /
+                                     invalid frames) whose tail past its last track is marked unused
+                                     (frame = 0xFFFFFFFF, other bytes 0).  The array's extent is
+                                     summary.track_slots <= sum over frames of min(n_cand,
+                                     max_tracks); track_capacity must cover it. */
     uint64_t track_capacity;
     m3e_vertex* vertices;         /* [kept_capacity], vertices[kept_index]; .frame = 0xFFFFFFFF
                                      for frames kept for another reason */
@@ -177,7 +186,9 @@ int m3e_kernel_times(m3e_context* ctx, float ms[6]);
 /* Full hot path on device-resident input (the call bench.py times): Selection
  * Cuts -> triplet fit -> tracks -> vertex selection -> output staging -> pack for
  * frames [0, F), nine kernel launches on `stream`.
- * Outputs [dev]; frames, tracks, vertices and kept frames in frame order. */
+ * Outputs [dev]; frames, tracks, vertices and kept frames in frame order (the
+ * track array with unused slots, see m3e_outputs.tracks: the fit kernel writes
+ * every track straight into its final slot, no reordering copy). */
 int m3e_filter(m3e_context* ctx, const m3e_params* p, const float* x, const float* y, const float* z,
                const uint32_t* offsets, uint64_t F, uint64_t H, const m3e_outputs* out, void* stream);
 

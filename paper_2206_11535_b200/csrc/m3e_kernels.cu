@@ -98,6 +98,18 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
     return v;
 }
 
+// output track slots: a warp-batch owns bslot[b] consecutive slots of out.tracks
+// from tbase[b]; its tracks fill the front, the rest are marked unused
+// (frame = 0xFFFFFFFF, every other byte 0)
+__device__ __forceinline__ void write_unused_slot(m3e_track* p) {
+    uint4* d = reinterpret_cast<uint4*>(p);
+    d[0] = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+    d[1] = make_uint4(0u, 0u, 0u, 0u);
+}
+// a frame's first track for the vertex stage: an out.tracks index, or kInFitG |
+// a fit_g index (no track output requested, or the caller's capacity exceeded)
+constexpr uint32_t kInFitG = 0x80000000u;
+
 // ----------------------------------------------------------- shared state ----
 // per-frame results of the warp-batch being processed
 struct BatchState {
@@ -518,6 +530,7 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
     const uint32_t ls = warp_incl(lc) - lc;
     const uint32_t sp_i = warp_incl(ns);
     const uint32_t tot = __shfl_sync(0xffffffffu, sp_i, 31);
+    const uint32_t nslot = warp_sum(min(ns, (uint32_t)P.max_tracks));   // its output track slots
     if (isf) {
         A.sel[f0 + lane] = (uint32_t)count | ((uint32_t)reason << 16);
         S.pl[lane] = make_uint4(ls, sp_i - ns, sp, ns);
@@ -549,6 +562,7 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
     if (lane == 0) {
         A.bsel[b] = fits ? (uint32_t)base : kSpilled;
         A.bcnt[b] = fits ? tot : 0u;
+        A.bslot[b] = nslot;
         if (!fits) A.spill_out[atomicAdd(A.ticket + 5, 1u)] = b;   // for the fused kernel
     }
     return true;
@@ -677,6 +691,7 @@ __device__ __forceinline__ void flush_summary(m3e_summary* sm, const uint32_t* a
     if (acc[9]) atomicAdd((u64*)&sm->kept_hits, (u64)acc[9]);
     if (acc[M3E_REASON_VERTEX]) atomicAdd((u64*)&sm->vertices, (u64)acc[M3E_REASON_VERTEX]);
     if (acc[10]) atomicExch((u64*)&sm->overflow, 1ull);
+    if (acc[11]) atomicAdd((u64*)&sm->track_slots, (u64)acc[11]);
 }
 
 // ------------------------------------------------------------------ kernel ----
@@ -866,9 +881,12 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
                 }
                 A.cand_g[base + e] = c;
             }
+            const uint32_t nslot =
+                warp_sum(lane < nf ? min((uint32_t)B.nstored[lane], (uint32_t)P.max_tracks) : 0u);
             if (lane == 0) {
                 A.bsel[b] = fits ? (uint32_t)base : kSpilled;
                 A.bcnt[b] = fits ? tot : 0u;
+                A.bslot[b] = nslot;
                 if (!fits) A.spill_out[atomicAdd(A.ticket + 5, 1u)] = b;   // for the fused kernel
             }
         }
@@ -1116,6 +1134,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
                     }
                 }
             }
+            // its track slots: sum over frames of min(stored candidates, max_tracks), as
+            // the selection kernel counts them
+            const uint32_t nslot =
+                warp_sum(lane < nf ? min((uint32_t)B.nstored[lane], (uint32_t)P.max_tracks) : 0u);
             if (lane == 0) {
                 BatchStat bs;
                 bs.n_trk = nt;
@@ -1124,8 +1146,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
                 bs.s_trk = s_trk;
                 bs.s_kept = s_kept;
                 bs.nf = nf;
-                bs.c_base = 0;
-                bs.c_n = 0;
+                bs.n_slot = nslot;
+                bs.pad = 0;
                 A.bstat[b] = bs;
             }
             // run summary: per-warp counters in shared memory, flushed once at the end
@@ -1156,6 +1178,92 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
         __syncwarp();
         if (lane == 0 && A.out.summary) flush_summary(A.out.summary, W.acc);
     }
+}
+
+// -------------------------------------------------------- slot scan kernel ----
+// Between the selection and the fit kernel: every warp-batch's first slot in the
+// output track array, tbase[b] = sum of bslot over the warp-batches before b
+// (warp-batch order = frame order), so that the fit kernel writes each accepted
+// track straight into its final place (the track array is frame-ordered; a
+// warp-batch's rejected candidates leave unused slots at the end of its range).
+// Single pass: tiles of kScanTile warp-batches claimed in order by a ticket, a
+// block scan, and a decoupled look-back over the tiles' {tag, sum} words.
+__device__ __forceinline__ void st_volatile_v2(uint2* p, uint2 v) {
+    asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ uint2 ld_volatile_v2(const uint2* p) {
+    uint2 v;
+    asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads) slot_scan_kernel(const __grid_constant__ KArgs A) {
+    __shared__ uint32_t wsum[kWarps];
+    __shared__ uint32_t s_tile, s_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t ntiles = (A.nbatch + kScanTile - 1) / kScanTile;
+    const uint32_t tagA = (A.epoch << 2) | 1u, tagI = (A.epoch << 2) | 2u;
+    for (;;) {
+        if (tid == 0) s_tile = atomicAdd(A.ticket + 12, 1u);
+        __syncthreads();
+        const uint32_t t = s_tile;
+        if (t >= ntiles) break;
+        const uint32_t b0 = t * kScanTile + tid * kScanItems;
+        uint32_t v[kScanItems];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            v[i] = b0 + i < A.nbatch ? A.bslot[b0 + i] : 0u;
+            sum += v[i];
+        }
+        const uint32_t inc = warp_incl(sum);
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        uint32_t woff = 0, agg = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            woff += w < warp ? wsum[w] : 0u;
+            agg += wsum[w];
+        }
+        if (warp == 0) {
+            uint32_t ex = 0;
+            if (t == 0) {
+                if (lane == 0) st_volatile_v2(A.sstatus, make_uint2(tagI, agg));
+            } else {
+                if (lane == 0) st_volatile_v2(A.sstatus + t, make_uint2(tagA, agg));
+                int j = (int)t - 1;
+                for (;;) {
+                    const int idx = j - lane;
+                    uint2 st = make_uint2(tagI, 0u);   // virtual inclusive zero before tile 0
+                    if (idx >= 0) {
+                        do {
+                            st = ld_volatile_v2(A.sstatus + idx);
+                        } while (st.x != tagA && st.x != tagI);
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, st.x == tagI);
+                    const int k = m ? __ffs(m) - 1 : 32;   // nearest predecessor with an inclusive prefix
+                    ex += warp_sum(lane <= k ? st.y : 0u);
+                    if (m) break;
+                    j -= 32;
+                }
+                if (lane == 0) st_volatile_v2(A.sstatus + t, make_uint2(tagI, ex + agg));
+            }
+            if (lane == 0) s_base = ex;
+        }
+        __syncthreads();
+        uint32_t run = s_base + woff + inc - sum;
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            if (b0 + i < A.nbatch) A.tbase[b0 + i] = run;
+            run += v[i];
+        }
+        __syncthreads();   // s_tile / wsum reused by the next tile
+    }
+}
+
+cudaError_t launch_slot_scan(const KArgs& a, int grid, cudaStream_t s) {
+    slot_scan_kernel<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------- pack kernel ----
@@ -1206,7 +1314,8 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
     const DevParams& P = A.P;
     const uint32_t ntiles = (A.nbatch + kPackTile - 1) / kPackTile;
     const uint32_t fb = (uint32_t)A.fb;
-    uint32_t acc[10] = {};   // run summary of this thread: kept_by_reason[6], cand, frames, tracks, hits
+    uint32_t acc[12] = {};   // run summary of this thread: kept_by_reason[6], cand, frames, tracks, hits,
+                             // -, track slots
     bool overflow = false;
     for (;;) {
         if (tid == 0) S.tile = atomicAdd(A.ticket + 3, 1u);
@@ -1216,17 +1325,22 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
         const uint32_t b = t * kPackTile + tid;
         const bool inb = b < A.nbatch;
         const bool fused = inb && (!A.bsel || A.bsel[b] == kSpilled);   // outputs staged by the fused kernel
-        uint32_t n_trk = 0, n_kept = 0, n_hits = 0, s_kept = 0, src = 0;
+        // n_slot: the warp-batch's slots in out.tracks (the selection kernel's count, which
+        // the slot scan and the fit kernel used; the fused kernel's on the fused variant)
+        uint32_t n_trk = 0, n_kept = 0, n_hits = 0, s_kept = 0, src = 0, n_slot = 0, f_trk = 0;
         if (fused) {
             const BatchStat bs = A.bstat[b];
-            n_trk = bs.n_trk;
+            f_trk = bs.n_trk;
             n_kept = bs.n_kept;
             n_hits = bs.n_hits;
             s_kept = bs.s_kept;
+            n_slot = A.bslot ? A.bslot[b] : bs.n_slot;
             src = bs.s_trk | 0x80000000u;
         } else if (inb) {
             src = A.bsel[b];
+            n_slot = A.bslot[b];
         }
+        acc[11] += n_slot;
         S.src[tid] = src;
         __syncthreads();
         const uint32_t f0 = t * kPackTile * fb;
@@ -1278,8 +1392,9 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
                 n_hits += S.fhit[i];
             }
         }
-        // block-wide scan of the three counts, then the look-back
-        uint32_t it = n_trk, ik = n_kept, ih = n_hits;
+        // block-wide scan of the three counts (track slots, kept frames, their hits),
+        // then the look-back
+        uint32_t it = n_slot, ik = n_kept, ih = n_hits;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t a = __shfl_up_sync(0xffffffffu, it, o);
@@ -1299,11 +1414,17 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
         }
         uint32_t w0 = 0, w1 = 0, w2 = 0;   // this warp's offset inside the tile
         for (int w = 0; w < warp; ++w) { w0 += S.wagg[w][0]; w1 += S.wagg[w][1]; w2 += S.wagg[w][2]; }
-        S.ptrk[tid] = w0 + it - n_trk;
+        S.ptrk[tid] = w0 + it - n_slot;
         S.pkept[tid] = w1 + ik - n_kept;
         if (tid == kThreads - 1) S.ptrk[kPackTile] = w0 + it;
         __syncthreads();
         const uint32_t base_trk = S.base[0], base_kept = S.base[1];
+        const uint32_t g_slot_b = base_trk + S.ptrk[tid];   // this warp-batch's first slot
+        // the fit kernel wrote the tracks of warp-batches whose slots fit the capacity
+        // into out.tracks; the others are missing from it
+        if (O.tracks && inb && !fused && n_trk > 0 &&
+            (uint64_t)g_slot_b + n_slot > min(O.track_capacity, (uint64_t)kInFitG))
+            overflow = true;
         const uint32_t g_kept_b = base_kept + w1 + ik - n_kept, g_hits_b = S.base[2] + w2 + ih - n_hits;
         // ---- frame records, once, with call-global indices
         {
@@ -1335,40 +1456,28 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
                 }
             }
         }
-        // ---- tracks: flat over the tile's output, 4 tracks in flight per thread
+        // ---- tracks of the fused kernel's warp-batches (staged; none at phase I): one
+        // warp per warp-batch, its slots = staged tracks, then unused-slot marks
         if (O.tracks && A.stage_trk) {
-            const uint32_t T = S.ptrk[kPackTile];
-            for (uint32_t d0 = tid; d0 < T; d0 += 4 * kThreads) {
-                uint4 v[4][2];
-                uint32_t dst[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t d = d0 + u * kThreads;
-                    dst[u] = 0xFFFFFFFFu;
-                    if (d < T) {
-                        int lo = 0, hi = kPackTile - 1;   // last warp-batch with ptrk <= d
-                        while (lo < hi) {
-                            const int mid = (lo + hi + 1) >> 1;
-                            if (S.ptrk[mid] <= d) lo = mid; else hi = mid - 1;
-                        }
-                        const uint32_t sr = S.src[lo], k = d - S.ptrk[lo];
-                        const uint4* s4 = (sr & 0x80000000u)
-                                              ? reinterpret_cast<const uint4*>(A.stage_trk + (sr & 0x7FFFFFFFu) + k)
-                                              : reinterpret_cast<const uint4*>(A.fit_g + sr + k);
-                        v[u][0] = s4[0];
-                        v[u][1] = s4[1];
-                        dst[u] = base_trk + d;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (dst[u] == 0xFFFFFFFFu) continue;
-                    if (dst[u] < O.track_capacity) {
-                        uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst[u]);
-                        d4[0] = v[u][0];
-                        d4[1] = v[u][1];
-                    } else {
+            unsigned todo = __ballot_sync(0xffffffffu, fused && n_slot > 0);
+            while (todo) {
+                const int sl = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const uint32_t nt = __shfl_sync(0xffffffffu, f_trk, sl);
+                const uint32_t ns = __shfl_sync(0xffffffffu, n_slot, sl);
+                const uint32_t st = __shfl_sync(0xffffffffu, src, sl) & 0x7FFFFFFFu;
+                const uint32_t g = __shfl_sync(0xffffffffu, g_slot_b, sl);
+                for (uint32_t k = lane; k < max(ns, nt); k += 32) {
+                    const uint32_t dst = g + k;
+                    if (dst >= O.track_capacity || k >= ns || st + k >= A.stage_trk_cap) {
                         overflow = true;
+                    } else if (k < nt) {
+                        const uint4* s4 = reinterpret_cast<const uint4*>(A.stage_trk + st + k);
+                        uint4* d4 = reinterpret_cast<uint4*>(O.tracks + dst);
+                        d4[0] = s4[0];
+                        d4[1] = s4[1];
+                    } else {
+                        write_unused_slot(O.tracks + dst);
                     }
                 }
             }
@@ -1466,20 +1575,9 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
     // run summary: one flush per warp (the fused kernel flushed its own frames)
     uint32_t sacc[12];
 #pragma unroll
-    for (int r = 0; r < 10; ++r) sacc[r] = warp_sum(acc[r]);
+    for (int r = 0; r < 12; ++r) sacc[r] = warp_sum(acc[r]);
     sacc[10] = __any_sync(0xffffffffu, overflow) ? 1u : 0u;
-    sacc[11] = 0;
-    if (lane == 0 && O.summary) {
-        uint32_t fl[12];
-        for (int r = 0; r < 6; ++r) fl[r] = sacc[r];
-        fl[6] = sacc[6];
-        fl[7] = sacc[7];
-        fl[8] = sacc[8];
-        fl[9] = sacc[9];
-        fl[10] = sacc[10];
-        fl[11] = 0;
-        flush_summary(O.summary, fl);
-    }
+    if (lane == 0 && O.summary) flush_summary(O.summary, sacc);
 }
 
 // ------------------------------------------------------------ fit kernel ----
@@ -1509,15 +1607,19 @@ struct __align__(16) FitSlot {
     const float* px;              // hit arrays as seen by a global hit index: the staged window
     const float* py;              // shifted by its first hit (generic addresses), or the inputs
     const float* pz;              // in HBM for a warp-batch larger than the window
+    m3e_track* td;                // where its output tracks go: out.tracks + its first slot, or the
+                                  // front of its store segment in fit_g (no track output requested)
     uint32_t b, f0, nf, winlo;    // warp-batch, its frames, first staged hit (0xFFFFFFFF: from HBM)
     uint32_t sbase, n, t, nacc;   // store segment, its entries, entries consumed, output tracks written
+    uint32_t tcode, nslot;        // its first track for the vertex stage (kInFitG | fit_g index, or the
+                                  // out.tracks index), its slots in out.tracks (0: tracks in fit_g)
     int cnt[kFB], neg[kFB], pos[kFB];   // per frame: accepted, stored e-, stored e+
 };
 
 // descriptor words of the warp's next warp-batch, fetched ahead by cp.async:
-// {first hit, end hit, store segment, its entries}
+// {first hit, end hit, store segment, its entries, first track slot, track slots}
 struct FitPre {
-    uint32_t w[4];
+    uint32_t w[6];
 };
 
 __device__ __forceinline__ void prefetch_bulk_l2(const void* p, uint32_t bytes) {
@@ -1532,12 +1634,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // lanes 0-3: start fetching the descriptor words of warp-batch b (none if b >= nbatch)
 __device__ __forceinline__ void fit_prefetch(const KArgs& A, FitPre& D, uint32_t b) {
     const int lane = threadIdx.x & 31;
-    if (b < A.nbatch && lane < 4) {
+    if (b < A.nbatch && lane < 6) {
         const uint32_t f0 = b * (uint32_t)A.fb;
         const uint32_t nf = min(A.F - f0, (uint32_t)A.fb);
         const uint32_t* src = lane == 0 ? A.offsets + 4 * (size_t)f0
                             : lane == 1 ? A.offsets + 4 * (size_t)(f0 + nf)
-                            : lane == 2 ? A.bsel + b : A.bcnt + b;
+                            : lane == 2 ? A.bsel + b
+                            : lane == 3 ? A.bcnt + b
+                            : lane == 4 ? A.tbase + b : A.bslot + b;
         cp_async4(&D.w[lane], src);
     }
     cp_async_commit();
@@ -1577,6 +1681,15 @@ __device__ __forceinline__ void fit_assign(const KArgs& A, FitSlot& S, FitPre& D
             S.pz = inw ? reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(S.hz) - sh) : A.z;
             S.sbase = sb;
             S.n = n;
+            // tracks straight into their final slots when the caller asked for them and
+            // the warp-batch's slot range fits its capacity (else into fit_g; the pack
+            // kernel reports the overflow)
+            const uint32_t tb = D.w[4], ns = D.w[5];
+            const bool to_out = A.out.tracks != nullptr && sb != kSpilled &&
+                                (uint64_t)tb + ns <= min(A.out.track_capacity, (uint64_t)kInFitG);
+            S.td = to_out ? A.out.tracks + tb : A.fit_g + (sb == kSpilled ? 0u : sb);
+            S.tcode = to_out ? tb : (kInFitG | (sb == kSpilled ? 0u : sb));
+            S.nslot = to_out ? ns : 0u;
             S.offs[4 * nf] = hi;
             if (n) prefetch_bulk_l2(A.cand_g + sb, n * (uint32_t)sizeof(uint4));
             const uint32_t hb = inw ? (whi - wlo) * 4u : 0u, ob = nf * 16u;
@@ -1614,9 +1727,14 @@ __device__ __forceinline__ void fit_frames(const KArgs& A, FitSlot& S) {
         A.fw[S.f0 + lane] = (uint32_t)min(c, P.max_tracks + 1) | ((uint32_t)min(nneg, 255) << 8) |
                             ((uint32_t)reason << 24);
     }
-    // the frame's first output track: segment base + prefix of the stored counts
+    // the frame's first output track: the warp-batch's first track + prefix of the
+    // stored counts
     const uint32_t stored = active ? (uint32_t)min(c, P.max_tracks) : 0u;
-    const uint32_t cs = S.sbase + warp_incl(stored) - stored;
+    const uint32_t cs = S.tcode + warp_incl(stored) - stored;
+    // the warp-batch's unused slots in out.tracks (its rejected candidates'): marked
+#ifndef M3E_NO_MARK
+    for (uint32_t k = S.nacc + (uint32_t)lane; k < S.nslot; k += 32) write_unused_slot(S.td + k);
+#endif
     // frames for the vertex stage (Alg. 4 needs two e+ and one e-)
     const bool need = active && reason == M3E_REASON_NONE && npos >= 2 && nneg >= 1;
     const unsigned m = __ballot_sync(0xffffffffu, need);
@@ -1747,7 +1865,7 @@ __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel
             tr.cos_theta01 = o.cth01;
             tr.cx = o.cx;
             tr.cy = o.cy;
-            A.fit_g[L.sbase + L.nacc + __popc(ms & (inX ? mx : ~mx) & lt)] = tr;
+            L.td[L.nacc + __popc(ms & (inX ? mx : ~mx) & lt)] = tr;
         }
         __syncwarp();
         if (valid && lane == __ffs(grp) - 1) {
@@ -1788,6 +1906,10 @@ __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel
 //   vpost_kernel   one thread per listed frame: the passing triple with the
 //                  smallest chi2 (earliest on ties) is the frame's vertex.
 // A frame whose triples do not fit the list runs vertex_frame in place.
+__device__ __forceinline__ const m3e_track* vtracks(const KArgs& A, uint32_t code) {
+    return (code & kInFitG) ? A.fit_g + (code & ~kInFitG) : A.out.tracks + code;
+}
+
 struct VRes {
     double x, y, z, chi2, tdist, ptot;
     int pass, pad;
@@ -1817,8 +1939,9 @@ __global__ void __launch_bounds__(kThreads, 4) vertex_kernel(const __grid_consta
     uint2* cmb = S.cmb[warp];
     for (uint32_t k = (uint32_t)gwarp; k < n; k += gridDim.x * kWarps) {
         const uint2 e = A.vlist[k];
-        const uint32_t f = e.x, cs = e.y;
-        // the frame's output tracks, contiguous from cs (fit kernel)
+        const uint32_t f = e.x;
+        // the frame's output tracks, contiguous from e.y (fit kernel)
+        const m3e_track* ft = vtracks(A, e.y);
         const uint32_t nj = min(A.fw[f] & 0xFFu, (uint32_t)P.max_tracks);
         // accepted tracks (track index = rank among the frame's accepted entries,
         // the first max_tracks only) split by charge, in track order
@@ -1828,9 +1951,8 @@ __global__ void __launch_bounds__(kThreads, 4) vertex_kernel(const __grid_consta
             float kap = 0.0f;
             bool acc = false;
             if (c < nj) {
-                const m3e_track* t = A.fit_g + cs + c;
-                acc = t->frame != kSpilled;
-                kap = t->kappa;
+                acc = true;
+                kap = ft[c].kappa;
             }
             const unsigned m = __ballot_sync(0xffffffffu, acc);
             const int ti = nt + __popc(m & lt_mask);
@@ -1897,10 +2019,10 @@ __global__ void __launch_bounds__(kThreads, 4) vertex_kernel(const __grid_consta
             int m_ = 0;
             for (uint32_t k0 = 0; k0 < nj; k0 += 32) {
                 const uint32_t c = k0 + lane;
-                const bool acc = c < nj && A.fit_g[cs + c].frame != kSpilled;
+                const bool acc = c < nj;
                 const unsigned m = __ballot_sync(0xffffffffu, acc);
                 const int p = m_ + __popc(m & lt_mask);
-                if (acc && p < P.max_tracks) pool[p] = A.fit_g[cs + c];
+                if (acc && p < P.max_tracks) pool[p] = ft[c];
                 m_ += __popc(m);
             }
             __syncwarp();
@@ -1952,9 +2074,10 @@ __global__ void __launch_bounds__(kThreads, M3E_TRIPLE_MIN_BLOCKS) triple_kernel
         Fv.y = A.y + g0;
         Fv.z = A.z + g0;
         Fv.s[0] = 0;
-        const VTrk T0 = make_vtrk(SP, A.fit_g[v.y + (e.y & 1023u)], Fv);
-        const VTrk T1 = make_vtrk(SP, A.fit_g[v.y + ((e.y >> 10) & 1023u)], Fv);
-        const VTrk T2 = make_vtrk(SP, A.fit_g[v.y + ((e.y >> 20) & 1023u)], Fv);
+        const m3e_track* ft = vtracks(A, v.y);
+        const VTrk T0 = make_vtrk(SP, ft[e.y & 1023u], Fv);
+        const VTrk T1 = make_vtrk(SP, ft[(e.y >> 10) & 1023u], Fv);
+        const VTrk T2 = make_vtrk(SP, ft[(e.y >> 20) & 1023u], Fv);
         const VResult r = vertex_triple_inl(SP, T0, T1, T2);
         VRes o;
         o.x = r.x; o.y = r.y; o.z = r.z;
@@ -2011,7 +2134,8 @@ __global__ void rebase_kernel(const Rebase r) {
             if (fo.kept_index != 0xFFFFFFFFu) fo.kept_index += r.base_kept;
         }
     if (r.tracks)
-        for (uint64_t i = i0; i < r.n_tracks; i += stride) r.tracks[i].frame += r.frame0;
+        for (uint64_t i = i0; i < r.n_tracks; i += stride)
+            if (r.tracks[i].frame != 0xFFFFFFFFu) r.tracks[i].frame += r.frame0;   // (unused slots stay marked)
     for (uint64_t i = i0; i < r.n_kept; i += stride) {
         if (r.kept_frame) r.kept_frame[i] += r.frame0;
         if (r.kept_offsets)

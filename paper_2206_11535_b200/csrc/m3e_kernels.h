@@ -41,7 +41,9 @@ struct BatchStat {
     uint32_t s_trk, s_kept;          // staging offsets of its tracks / kept-frame records; s_trk =
                                      // kSpilled: its tracks are the front of its store segment
     uint32_t nf;                     // frames in the warp-batch
-    uint32_t c_base, c_n;            // its store segment and output tracks there (split path)
+    uint32_t n_slot;                 // its track slots (sum over frames of min(stored candidates,
+                                     // max_tracks)): the extent it takes in the output track array
+    uint32_t pad;
 };
 
 // kept-frame record staged by the filter kernel (64 B)
@@ -89,6 +91,11 @@ struct KArgs {
     uint64_t tri_cap;      // entries of tri / tres
     uint32_t* bsel;        // [nbatch] first store entry of the warp-batch, or kSpilled
     uint32_t* bcnt;        // [nbatch] its store entries
+    uint32_t* bslot;       // [nbatch] its track slots: sum over its frames of min(stored candidates,
+                           // max_tracks), an upper bound of its output tracks (selection kernel)
+    uint32_t* tbase;       // [nbatch] exclusive prefix of bslot in warp-batch order (slot_scan_kernel): the
+                           // warp-batch's first slot in out.tracks
+    uint2* sstatus;        // slot_scan_kernel decoupled look-back, one 8 B word per tile
     uint4* status;         // pack-kernel decoupled look-back, one 16 B word per tile
     uint32_t epoch;        // launch epoch tag of the status words (never 0)
     BatchStat* bstat;      // [nbatch]
@@ -135,6 +142,9 @@ cudaError_t launch_rebase(const Rebase& r, int sms, cudaStream_t s);
 size_t smem_bytes();
 cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);
+constexpr int kScanItems = 8;                          // warp-batches per thread of slot_scan_kernel
+constexpr int kScanTile = kThreads * kScanItems;       // warp-batches per tile (CTA iteration)
+cudaError_t launch_slot_scan(const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_fit(const KArgs& a, bool big, int grid, cudaStream_t s);
 int fit_blocks_per_sm();
 cudaError_t launch_vertex(const KArgs& a, int grid, int sms, cudaStream_t s);

@@ -75,7 +75,12 @@ struct Workspace {
     uint32_t* bsel = nullptr;           // per-warp-batch store offsets of the split path
     uint32_t* bcnt = nullptr;           // per-warp-batch store entries
     uint32_t* spill = nullptr;          // warp-batches the store could not take
+    uint32_t* bslot = nullptr;          // per-warp-batch output track slots
+    uint32_t* tbase = nullptr;          // ... and its first slot (slot scan)
     size_t bsel_n = 0;
+    uint2* sstatus = nullptr;           // slot-scan look-back words, one per scan tile
+    size_t sstatus_n = 0;
+    bool sstatus_fresh = false;
     bool status_fresh = false;          // status words allocated, not yet zeroed
     size_t bytes = 0;
 };
@@ -135,6 +140,9 @@ void free_ws(Workspace& w) {
     cudaFree(w.bsel);
     cudaFree(w.bcnt);
     cudaFree(w.spill);
+    cudaFree(w.bslot);
+    cudaFree(w.tbase);
+    cudaFree(w.sstatus);
     cudaFree(w.pair_scratch);
     cudaFree(w.vscratch);
     cudaFree(w.bstat);
@@ -248,6 +256,7 @@ int ensure_ws(m3e_context* c, Workspace& w, uint64_t nbatch, const m3e_params* p
         w.status_fresh = true;   // zeroed on the launch stream before its first use (run_mode)
         w.bytes += n * sizeof(uint4);
         w.epoch = 0;
+        w.sstatus_fresh = true;   // epochs restart: no stale slot-scan tag may match either
     }
     const size_t ps = (size_t)fb * p->cuts_max, ts = (size_t)fb * p->max_tracks;
     if (w.pool_ctas < ctas || w.pool_stride < ps || w.trk_stride < ts) {
@@ -327,13 +336,27 @@ int ensure_split(Workspace& w, uint64_t F, uint64_t nbatch, uint64_t per_frame, 
         cudaFree(w.bsel);
         cudaFree(w.bcnt);
         cudaFree(w.spill);
-        w.bytes -= 3 * w.bsel_n * sizeof(uint32_t);
+        cudaFree(w.bslot);
+        cudaFree(w.tbase);
+        w.bytes -= 5 * w.bsel_n * sizeof(uint32_t);
         w.bsel_n = 0;
         CK(cudaMalloc(&w.bsel, nbatch * sizeof(uint32_t)));
         CK(cudaMalloc(&w.bcnt, nbatch * sizeof(uint32_t)));
         CK(cudaMalloc(&w.spill, nbatch * sizeof(uint32_t)));
+        CK(cudaMalloc(&w.bslot, nbatch * sizeof(uint32_t)));
+        CK(cudaMalloc(&w.tbase, nbatch * sizeof(uint32_t)));
         w.bsel_n = nbatch;
-        w.bytes += 3 * nbatch * sizeof(uint32_t);
+        w.bytes += 5 * nbatch * sizeof(uint32_t);
+    }
+    const uint64_t nst = (nbatch + kScanTile - 1) / kScanTile;
+    if (w.sstatus_n < nst) {
+        cudaFree(w.sstatus);
+        w.bytes -= w.sstatus_n * sizeof(uint2);
+        const size_t n = std::max<size_t>(nst, 1024);
+        CK(cudaMalloc(&w.sstatus, n * sizeof(uint2)));
+        w.sstatus_n = n;
+        w.sstatus_fresh = true;   // zeroed on the launch stream before its first use
+        w.bytes += n * sizeof(uint2);
     }
     return M3E_OK;
 }
@@ -429,6 +452,10 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         CK(cudaMemsetAsync(w.status, 0, w.status_n * sizeof(uint4), s));
         w.status_fresh = false;
     }
+    if (split && w.sstatus_fresh) {
+        CK(cudaMemsetAsync(w.sstatus, 0, w.sstatus_n * sizeof(uint2), s));
+        w.sstatus_fresh = false;
+    }
     if (a.out.summary) CK(cudaMemsetAsync(a.out.summary, 0, sizeof(m3e_summary), s));
     const bool tm = ctx->timing && &w == &ctx->ws[0] && ctx->tev_used + kNEv <= ctx->tev.size();
     cudaEvent_t* ev = tm ? &ctx->tev[ctx->tev_used] : nullptr;
@@ -440,8 +467,14 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         sa.sel = w.sel;
         sa.bsel = w.bsel;
         sa.bcnt = w.bcnt;
+        sa.bslot = w.bslot;
         sa.spill_out = w.spill;
         CK(launch_filter(kModeSelectC, big, sa, sgrid, s));
+        // every warp-batch's first slot in out.tracks (frame order), for the fit kernel
+        sa.tbase = w.tbase;
+        sa.sstatus = w.sstatus;
+        CK(launch_slot_scan(sa, (int)std::min<uint64_t>((nbatch + kScanTile - 1) / kScanTile,
+                                                        (uint64_t)ctx->sms * 4), s));
         if (tm) CK(cudaEventRecord(ev[1], s));
         a.cand_g = w.cand_g;
         a.fit_g = w.fit_g;
@@ -449,6 +482,8 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         a.sel = w.sel;
         a.bsel = w.bsel;
         a.bcnt = w.bcnt;
+        a.bslot = w.bslot;
+        a.tbase = w.tbase;
         a.fw = w.fw;
         a.vk = w.vk;
         a.vlist = w.vlist;
@@ -711,7 +746,7 @@ int m3e_filter_host(m3e_context* ctx, const m3e_params* p, const float* x, const
         const m3e_summary sm = *c.h_summary;
         uint64_t K = 0;
         for (int r = 1; r < 6; ++r) K += sm.kept_by_reason[r];
-        const uint64_t Hk = sm.kept_hits, T = sm.tracks;
+        const uint64_t Hk = sm.kept_hits, T = sm.track_slots;   // the chunk's track-array extent
         if (sm.overflow) return fail(M3E_ERR_CAPACITY, "device chunk capacity exceeded");
         if ((out->kept_frame || out->vertices || out->kept_offsets) && base_kept + K > out->kept_capacity)
             return fail(M3E_ERR_CAPACITY, "kept_capacity too small");
@@ -763,6 +798,7 @@ int m3e_filter_host(m3e_context* ctx, const m3e_params* p, const float* x, const
         for (int r = 0; r < 6; ++r) total.kept_by_reason[r] += sm.kept_by_reason[r];
         total.candidates += sm.candidates;
         total.tracks += sm.tracks;
+        total.track_slots += sm.track_slots;
         total.kept_hits += sm.kept_hits;
         total.vertices += sm.vertices;
         base_trk += T;
@@ -828,4 +864,4 @@ static_assert(sizeof(m3e_frame_out) == 16, "m3e_frame_out layout");
 static_assert(sizeof(m3e_track) == 32, "m3e_track layout");
 static_assert(sizeof(m3e_vertex) == 56, "m3e_vertex layout");
 static_assert(sizeof(m3e_fit_record) == 40, "m3e_fit_record layout");
-static_assert(sizeof(m3e_summary) == 96, "m3e_summary layout");
+static_assert(sizeof(m3e_summary) == 104, "m3e_summary layout");

@@ -56,9 +56,9 @@ FIT_DTYPE = np.dtype([("status", "u1"), ("pad", "u1"), ("hit3", "<u2"), ("kappa1
                       ("chi2", "<f4"), ("cos_theta01", "<f4"), ("cx", "<f4"), ("cy", "<f4")])
 SUMMARY_DTYPE = np.dtype([("frames", "<u8"), ("kept_by_reason", "<u8", (6,)), ("candidates", "<u8"),
                           ("tracks", "<u8"), ("kept_hits", "<u8"), ("vertices", "<u8"),
-                          ("overflow", "<u8")])
+                          ("overflow", "<u8"), ("track_slots", "<u8")])
 assert FRAME_DTYPE.itemsize == 16 and TRACK_DTYPE.itemsize == 32 and VERTEX_DTYPE.itemsize == 56
-assert FIT_DTYPE.itemsize == 40 and SUMMARY_DTYPE.itemsize == 96
+assert FIT_DTYPE.itemsize == 40 and SUMMARY_DTYPE.itemsize == 104
 
 _lib = None
 
@@ -262,7 +262,7 @@ class Result:
         self.kept_x = torch.zeros(kh, dtype=torch.float32, device=device)
         self.kept_y = torch.zeros(kh, dtype=torch.float32, device=device)
         self.kept_z = torch.zeros(kh, dtype=torch.float32, device=device)
-        self.summary = torch.zeros(96, **u8)
+        self.summary = torch.zeros(SUMMARY_DTYPE.itemsize, **u8)
         self.outputs = make_outputs(reason=self.reason, frames=self.frames, tracks=self.tracks,
                                     track_capacity=self.track_capacity, vertices=self.vertices,
                                     kept_frame=self.kept_frame, kept_offsets=self.kept_offsets,

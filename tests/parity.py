@@ -36,6 +36,31 @@ CHI2_DOMAIN = 1000.0
 VERTEX_ABS = 1e-9   # fp64 vertex stage on identical float32 tracks: rounding only
 
 
+def check_track_layout(P, frames_np, tracks_np, sm):
+    """The output track array's layout (include/m3e.h, m3e_outputs.tracks): frame
+    f's min(n_tracks, max_tracks) tracks (none for triplet-overflow / invalid
+    frames) at tracks[track_first ...], frame-ordered; every other slot of the
+    extent summary.track_slots is marked unused (frame 0xFFFFFFFF, other bytes
+    0); the extent is at most sum over frames of min(n_cand, max_tracks)."""
+    T = int(sm["track_slots"])
+    assert len(tracks_np) == T
+    reason = frames_np["reason"].astype(np.int64)
+    live = (reason != 1) & (reason != 5)
+    nt = np.where(live, np.minimum(frames_np["n_tracks"].astype(np.int64), P.max_tracks), 0)
+    assert int(nt.sum()) == int(sm["tracks"])
+    assert T <= int(np.where(live, np.minimum(frames_np["n_cand"].astype(np.int64), P.max_tracks), 0).sum())
+    tf = frames_np["track_first"].astype(np.int64)
+    assert np.all(np.diff(tf) >= 0) and np.all(tf[:-1] + nt[:-1] <= tf[1:])
+    assert len(tf) == 0 or tf[-1] + nt[-1] <= T
+    used = np.zeros(T, bool)
+    idx = np.repeat(tf, nt) + (np.arange(int(nt.sum())) - np.repeat(np.cumsum(nt) - nt, nt))
+    used[idx] = True
+    fidx = np.repeat(np.arange(len(tf), dtype=np.int64), nt)
+    assert np.array_equal(tracks_np["frame"][idx].astype(np.int64), fidx)
+    raw = tracks_np.view(np.uint32).reshape(T, 8)[~used]
+    assert np.all(raw[:, 0] == 0xFFFFFFFF) and not np.any(raw[:, 1:])
+
+
 def near(v, thr, band=REL_BAND):
     return abs(v - thr) <= band * abs(thr)
 

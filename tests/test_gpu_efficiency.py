@@ -30,7 +30,7 @@ def _run(cfg_name, n, seed, params):
     torch.cuda.synchronize()
     sm = res.summary_np()
     fo = res.frames_np(n)
-    tr = res.tracks_np(int(sm["tracks"]))
+    tr = res.tracks_np(int(sm["track_slots"]))
     ctx.close()
     return sc, d, fo, tr
 

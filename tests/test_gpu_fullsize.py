@@ -7,7 +7,7 @@ import pytest
 
 import oracle
 import synth
-from parity import compare_outputs
+from parity import check_track_layout, compare_outputs
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -49,16 +49,14 @@ def test_fullsize_phase1_second(cfg):
     reason = res.reason.cpu().numpy()
     frames_np = res.frames_np(F)
     T = int(sm["tracks"])
-    tracks_np = res.tracks_np(T)
+    tracks_np = res.tracks_np(int(sm["track_slots"]))
     # properties at any size
     assert np.array_equal(reason, frames_np["reason"])
     assert np.array_equal(np.bincount(reason, minlength=6), sm["kept_by_reason"])
     ntr = np.minimum(frames_np["n_tracks"].astype(np.int64), P.max_tracks)
     ntr[frames_np["reason"] == m3e.REASON_TRIPLET_OVERFLOW] = 0
     assert int(ntr.sum()) == T
-    first = frames_np["track_first"].astype(np.int64)
-    assert first[0] == 0 and np.array_equal(first[1:], np.cumsum(ntr)[:-1])
-    assert np.all(np.diff(tracks_np["frame"].astype(np.int64)) >= 0)
+    check_track_layout(P, frames_np, tracks_np, sm)
     kept = np.nonzero(reason)[0]
     K = len(kept)
     assert np.array_equal(res.kept_frame[:K].cpu().numpy().view(np.uint32).astype(np.int64), kept)
@@ -94,7 +92,7 @@ def test_phase2_sampled(cfg):
     sm = res.summary_np()
     assert not int(sm["overflow"])
     frames_np = res.frames_np(n)
-    tracks_np = res.tracks_np(int(sm["tracks"]))
+    tracks_np = res.tracks_np(int(sm["track_slots"]))
     sample = np.random.default_rng(2).choice(n, 400, replace=False)
     tally = _check_frames(P, oracle.Frames(d), res, frames_np, tracks_np, sample, "configs[4]")
     assert len(tally.frames) <= max(2, 5e-3 * len(sample))

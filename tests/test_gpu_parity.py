@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 import synth
-from parity import (CHI2_DOMAIN, REL_KAPPA, Tally, chi2_marginal, combo_is_marginal, compare_outputs, layer3_tie,
+from parity import (CHI2_DOMAIN, check_track_layout, REL_KAPPA, Tally, chi2_marginal, combo_is_marginal, compare_outputs, layer3_tie,
                     near, rel_close, unpack)
 
 torch = pytest.importorskip("torch")
@@ -224,7 +224,8 @@ def _compare_full(P, fr, res, n, name=""):
     (tests/parity.py); returns the tally of near-threshold items"""
     sm = res.summary_np()
     K = int(sum(sm["kept_by_reason"][1:]))
-    tally = compare_outputs(P, fr, res.frames_np(n), res.tracks_np(int(sm["tracks"])), res.vertices_np(K),
+    check_track_layout(P, res.frames_np(n), res.tracks_np(int(sm["track_slots"])), sm)
+    tally = compare_outputs(P, fr, res.frames_np(n), res.tracks_np(int(sm["track_slots"])), res.vertices_np(K),
                             range(n))
     print(tally.report(name))
     return tally
@@ -240,7 +241,7 @@ def test_full_parity(ctx, gp, P, name, n, seed):
     sm = res.summary_np()
     assert int(sm["overflow"]) == 0
     frames_np = res.frames_np(n)
-    tracks_np = res.tracks_np(int(sm["tracks"]))
+    tracks_np = res.tracks_np(int(sm["track_slots"]))
     tally = _compare_full(P, fr, res, n, name)
     assert len(tally.frames) <= max(1, 2e-3 * n)
     if name in ("phase1_sig", "signal_only"):
@@ -262,11 +263,8 @@ def test_full_parity(ctx, gp, P, name, n, seed):
         lo, hi = off[4 * f], off[4 * f + 4]
         assert np.array_equal(koff[4 * k:4 * k + 4] - koff[4 * k], off[4 * f:4 * f + 4] - lo)
         assert np.array_equal(kx[koff[4 * k]:koff[4 * k] + (hi - lo)], d["x"][lo:hi])
-    # frame-ordered tracks
-    tf = frames_np["track_first"].astype(np.int64)
-    assert np.all(np.diff(tf) >= 0)
-    if len(tracks_np):
-        assert np.all(np.diff(tracks_np["frame"].astype(np.int64)) >= 0)
+    # frame-ordered tracks with unused slots (m3e.h m3e_outputs.tracks)
+    check_track_layout(P, frames_np, tracks_np, sm)
 
 
 @pytest.mark.parametrize("fused", ["0", "1"])
@@ -292,7 +290,7 @@ def test_track_overflow_parity(cfg, monkeypatch, fused):
 
 def _outputs(res, n):
     sm = res.summary_np()
-    T, K = int(sm["tracks"]), int(sum(sm["kept_by_reason"][1:]))
+    T, K = int(sm["track_slots"]), int(sum(sm["kept_by_reason"][1:]))
     return (res.reason.cpu().numpy()[:n].copy(), res.frames_np(n).copy(), res.tracks_np(T).copy(),
             res.kept_frame.cpu().numpy()[:K].copy(), res.vertices_np(K).copy(), sm.copy())
 
@@ -437,7 +435,7 @@ def test_flat_selection_dense_frame(ctx, gp, P, cfg):
     assert len(tally.frames) <= 1
 
 
-def test_host_path_matches_device(ctx, gp):
+def test_host_path_matches_device(ctx, gp, P):
     """m3e_filter_host (chunked, two streams) == m3e_filter on the same frames."""
     n = 5000
     d, fr, df = _gen("phase1_sig", n, 501)
@@ -461,10 +459,25 @@ def test_host_path_matches_device(ctx, gp):
     small.close()
     sm = res.summary_np()
     assert np.array_equal(reason, res.reason.cpu().numpy()[:n])
-    assert np.array_equal(frames, res.frames_np(n))
-    T = int(sm["tracks"])
-    assert int(summ[0]["tracks"]) == T
-    assert np.array_equal(tracks[:T], res.tracks_np(T))
+    # the track array's slot layout follows each call's warp-batches (chunks of 1234
+    # frames split warp-batches differently than one call): every frame field but
+    # track_first equal, each frame's tracks equal, both layouts valid
+    fd = res.frames_np(n)
+    for k in m3e.FRAME_DTYPE.names:
+        if k != "track_first":
+            assert np.array_equal(frames[k], fd[k]), k
+    T, Th = int(sm["track_slots"]), int(summ[0]["track_slots"])
+    assert int(summ[0]["tracks"]) == int(sm["tracks"])
+    td = res.tracks_np(T)
+    check_track_layout(P, frames, tracks[:Th], summ[0])
+    check_track_layout(P, fd, td, sm)
+    nt = np.where((fd["reason"] != 1) & (fd["reason"] != 5),
+                  np.minimum(fd["n_tracks"].astype(np.int64), gp.max_tracks), 0)
+    ih = np.repeat(frames["track_first"].astype(np.int64), nt) + np.arange(int(nt.sum())) - \
+        np.repeat(np.cumsum(nt) - nt, nt)
+    idv = np.repeat(fd["track_first"].astype(np.int64), nt) + np.arange(int(nt.sum())) - \
+        np.repeat(np.cumsum(nt) - nt, nt)
+    assert np.array_equal(tracks[ih], td[idv])
     K = int(np.count_nonzero(reason))
     assert np.array_equal(kept_frame[:K], res.kept_frame.cpu().numpy()[:K].view(np.uint32))
     assert np.array_equal(kept_off[:4 * K + 1], res.kept_offsets.cpu().numpy()[:4 * K + 1].view(np.uint32))

@@ -114,3 +114,59 @@ def test_injected_bugs_fail(P, data, bug):
         vx["z"][int(fo["kept_index"][f])] += 1e-6
     with pytest.raises(AssertionError):
         compare_outputs(P, fr, fo, tr, vx, range(n), Tally())
+
+
+def _gapped(P, fo, tr, fb=8):
+    """the fake outputs re-laid out as the CUDA path lays out its track array:
+    warp-batches of fb frames, each owning sum min(n_cand, max_tracks) slots,
+    its tracks at the front, the rest marked unused"""
+    fo = fo.copy()
+    live = (fo["reason"] != 1) & (fo["reason"] != 5)
+    nt = np.where(live, np.minimum(fo["n_tracks"].astype(np.int64), P.max_tracks), 0)
+    ns = np.where(live, np.minimum(fo["n_cand"].astype(np.int64), P.max_tracks), 0)
+    out, pos = [], 0
+    for b0 in range(0, len(fo), fb):
+        slots = int(ns[b0:b0 + fb].sum())
+        batch = []
+        for f in range(b0, min(len(fo), b0 + fb)):
+            fo["track_first"][f] = pos + len(batch)
+            i = int(fo["track_first"][f]) - pos
+            src = tr[int(np.cumsum(nt)[f] - nt[f]):int(np.cumsum(nt)[f])]
+            batch.extend(src)
+            assert i + len(src) == len(batch)
+        mark = np.zeros(1, TRACK_DTYPE)[0]
+        mark["frame"] = 0xFFFFFFFF
+        batch.extend([mark] * (slots - len(batch)))
+        out.extend(batch)
+        pos += slots
+    sm = {"track_slots": pos, "tracks": int(nt.sum())}
+    return fo, np.array(out, TRACK_DTYPE), sm
+
+
+@pytest.mark.parametrize("bug", [None, "marker", "frame", "extent", "order"])
+def test_track_layout_check(P, data, bug):
+    """check_track_layout accepts the gapped frame-ordered layout and rejects a
+    dirty unused slot, a track filed under the wrong frame, a wrong extent, or
+    frames out of order"""
+    from parity import check_track_layout
+    fr, n, fo, tr, vx = data["phase1_sig"]
+    fo, tg, sm = _gapped(P, fo, tr)
+    assert len(tg) > sm["tracks"]   # the layout really has unused slots
+    if bug is None:
+        check_track_layout(P, fo, tg, sm)
+        tally = compare_outputs(P, fr, fo, tg, vx, range(n))
+        assert len(tally.frames) <= 2
+        return
+    if bug == "marker":
+        i = int(np.nonzero(tg["frame"] == 0xFFFFFFFF)[0][0])
+        tg["kappa"][i] = 1.0
+    elif bug == "frame":
+        i = int(np.nonzero(tg["frame"] != 0xFFFFFFFF)[0][3])
+        tg["frame"][i] += 1
+    elif bug == "extent":
+        sm = dict(sm, track_slots=sm["track_slots"] + 1)
+    elif bug == "order":
+        f = int(np.nonzero(fo["n_tracks"] > 0)[0][1])
+        fo["track_first"][f] = 0
+    with pytest.raises(AssertionError):
+        check_track_layout(P, fo, tg, sm)

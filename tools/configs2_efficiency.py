@@ -85,7 +85,7 @@ def main():
     torch.cuda.synchronize()
     sm = res.summary_np()
     g_frames = res.frames_np(n)
-    g_tracks = res.tracks_np(int(sm["tracks"]))
+    g_tracks = res.tracks_np(int(sm["track_slots"]))
     g_eff = signal_efficiency(sc, d, g_frames, g_tracks, cfg["max_tracks"])
     g_kept = int(np.count_nonzero(g_frames["reason"]))
     ctx.close()
