@@ -196,6 +196,19 @@ struct DevParams {
     double e_window, rlim, sig_pix2, chi2v_max, tdist_max, ptot_max, target_r, target_half;
 };
 
+// Delta-lambda (Eq. 2-3) of (i0, i1, i2) as z2 / dr12 - u(i0, i1) with the pair term
+//   u = z1 (1/dr12 + 1/dr01) - z0 / dr01 = z1 / dr12 + (z1 - z0) / dr01,
+// both with a pinned operation order so that every walk of the Selection Cuts
+// (per frame, flat, pair-factorised, mask-factorised) takes identical decisions:
+// pass iff |fma(z2, 1/dr12, -u)| <= dl_max
+M3E_HD float pair_u(const DevParams& P, float z0, float z1) {
+#ifdef __CUDA_ARCH__
+    return __fmaf_rn(z1, P.inv_dr12, __fmul_rn(__fsub_rn(z1, z0), P.inv_dr01));
+#else
+    return fmaf(z1, P.inv_dr12, (z1 - z0) * P.inv_dr01);
+#endif
+}
+
 struct Frame {                  // one frame's hits, pointers to its first hit
     const float* x;
     const float* y;
@@ -314,8 +327,7 @@ __device__ __forceinline__ int select_frame_warp(const DevParams& P, const Frame
             const bool pass = (j0 < n0) & (cos_sep(F.x[g0], F.y[g0], F.x[g1], F.y[g1], P.inv_r0r1) >= P.c01_min);
             const unsigned m = __ballot_sync(0xffffffffu, pass);
             // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
-            const float z1 = F.z[g1];
-            const float u = z1 * P.inv_dr12 + (z1 - F.z[g0]) * P.inv_dr01;
+            const float u = pair_u(P, F.z[g0], F.z[g1]);
             if (pass) pl[pn + __popc(m & lt_mask)] = make_uint2((uint32_t)j0 | ((uint32_t)j1 << 10), __float_as_uint(u));
             pn += __popc(m);
             pnext += 32;
@@ -386,9 +398,10 @@ __device__ __forceinline__ bool pass_rt(const DevParams& P, const Frame& F, int 
 }
 
 // ballot-compact the pairs (ia in layer la, ib in layer lb) passing cos Phi >= cmin
-// in row-major order (ia outer), with t = (z_b - z_a) / (r_b - r_a); returns the
-// count (> cap: overflow, lists incomplete)
-__device__ __forceinline__ int pair_list(const Frame& F, int la, int lb, float inv_rr, float cmin, float inv_dr,
+// in row-major order (ia outer), with t = u(ia, ib) (kU: layers 0, 1) or z_b
+// (layers 1, 2); returns the count (> cap: overflow, lists incomplete)
+template <bool kU>
+__device__ __forceinline__ int pair_list(const DevParams& P, const Frame& F, int la, int lb, float inv_rr, float cmin,
                                          uint32_t* lst, float* tv, int cap) {
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -404,7 +417,7 @@ __device__ __forceinline__ int pair_list(const Frame& F, int la, int lb, float i
         if (ia < na) {
             const int ga = F.s[la] + ia, gb = F.s[lb] + ib;
             pass = cos_sep(F.x[ga], F.y[ga], F.x[gb], F.y[gb], inv_rr) >= cmin;
-            t = (F.z[gb] - F.z[ga]) * inv_dr;
+            t = kU ? pair_u(P, F.z[ga], F.z[gb]) : F.z[gb];
         }
         const unsigned m = __ballot_sync(0xffffffffu, pass);
         const int pos = cnt + __popc(m & lt_mask);
@@ -431,24 +444,25 @@ __device__ __forceinline__ int pair_list(const Frame& F, int la, int lb, float i
 // Returns -1 if a list exceeds kPairCapG (caller falls back to select_frame_warp).
 // Out of line: phase-I frames never take it, so its code stays out of the I-cache.
 static __device__ __noinline__ int select_frame_big(const DevParams* __restrict__ Pp, const Frame& Fin, uint32_t* q,
-                                                    uint32_t* X, CandSink sink, int cap) {
+                                                    uint32_t* X, const CandSink& sink_in, int cap) {
     const DevParams& P = *Pp;
-    // the frame view in registers: the caller's copy is in local memory (its address
-    // is passed), and the list stores below could alias it, forcing a reload of
-    // every field on every access
+    // the frame view and the sink in registers: the caller's copies are in local
+    // memory (their addresses are passed), and the list stores below could alias
+    // them, forcing a reload of every field on every access
     const Frame F = Fin;
+    const CandSink sink = sink_in;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int n1 = F.n[1];
     uint32_t* l01 = X;
-    float* t01 = reinterpret_cast<float*>(X + cap);
+    float* u01 = reinterpret_cast<float*>(X + cap);    // u(i0, i1) of list 1
     uint32_t* l12 = X + 2 * cap;
-    float* t12 = reinterpret_cast<float*>(X + 3 * cap);
+    float* z12 = reinterpret_cast<float*>(X + 3 * cap);   // z2 of list 2
     uint32_t* off12 = X + 4 * cap;                 // n1 + 1 entries
     uint32_t* wpre = off12 + (kMaxLayerHits + 2);  // cap + 1 entries
-    const int c01 = pair_list(F, 0, 1, P.inv_r0r1, P.c01_min, P.inv_dr01, l01, t01, cap);
+    const int c01 = pair_list<true>(P, F, 0, 1, P.inv_r0r1, P.c01_min, l01, u01, cap);
     if (c01 > cap) return -1;
-    const int c12 = pair_list(F, 1, 2, P.inv_r1r2, P.c12_min, P.inv_dr12, l12, t12, cap);
+    const int c12 = pair_list<false>(P, F, 1, 2, P.inv_r1r2, P.c12_min, l12, z12, cap);
     if (c12 > cap) return -1;
     __syncwarp();
     for (int i1 = lane; i1 <= n1; i1 += 32) {      // off12[i1] = lower bound of i1 in list 2
@@ -506,7 +520,7 @@ static __device__ __noinline__ int select_frame_big(const DevParams* __restrict_
             const int i1 = (a >> 10) & 1023u;
             const int k = (int)off12[i1] + (int)(e - (long long)wpre[lo]);
             const int i2 = (l12[k] >> 10) & 1023u;
-            pass = fabsf(t12[k] - t01[lo]) <= P.dl_max;
+            pass = fabsf(fmaf(z12[k], P.inv_dr12, -u01[lo])) <= P.dl_max;
             pk = (a & 1023u) | ((uint32_t)i1 << 10) | ((uint32_t)i2 << 20);
         }
         const unsigned m = __ballot_sync(0xffffffffu, pass);

@@ -110,6 +110,8 @@ __device__ __forceinline__ void write_unused_slot(m3e_track* p) {
 // a fit_g index (no track output requested, or the caller's capacity exceeded)
 constexpr uint32_t kInFitG = 0x80000000u;
 
+__device__ __forceinline__ bool below(uint32_t i, uint32_t lim) { return i < lim; }
+
 // ----------------------------------------------------------- shared state ----
 // per-frame results of the warp-batch being processed
 struct BatchState {
@@ -141,6 +143,26 @@ struct VScratch {
     uint8_t vlist[2][kMaxTracksCap];
 };
 
+// Shared state of select_frame_mask (selection kernel, big-frame calls); it overlays
+// the shared-memory candidate array and the other walks' state, so that kernel keeps
+// every candidate in global memory.  NW = 64-bit words per mask: frames of up to 64
+// (NW = 1) or kMask2Hits (NW = 2) hits in layers 1 and 2
+constexpr int kMask2Hits = 96;
+template <int NW> struct MaskSel;
+template <> struct MaskSel<1> {
+    unsigned long long m12[64];   // Phi_12 mask of layer-1 hit i1 over layer 2 (bit i2)
+    unsigned long long pm[65];    // layer 2 in z order: pm[r] = the hits of z-rank < r
+    float zs[64];                 // layer-2 z, ascending
+    uint8_t ord[64];              // layer-2 hit of z-rank r
+    uint2 pl[64];                 // Phi_01 pair list {i0 | i1 << 10, u(i0, i1)}
+};
+template <> struct MaskSel<2> {   // (m12: the warp's global scratch, L1 / L2)
+    unsigned long long pm[kMask2Hits + 1][2];
+    float zs[kMask2Hits];
+    uint8_t ord[kMask2Hits];
+    uint2 pl[64];
+};
+
 struct __align__(16) WarpSmem {
     float hx[kNBuf][kHCap];
     float hy[kNBuf][kHCap];
@@ -148,13 +170,19 @@ struct __align__(16) WarpSmem {
     uint32_t offs[kNBuf][4 * kFB + 4];
     uint64_t bar[kNBuf];
     uint32_t b_batch[kNBuf], b_winlo[kNBuf], b_winhi[kNBuf];
-    uint32_t cidx[kCandSmem];        // candidates (flat warp-batch index < kCandSmem)
     union {
-        struct {                     // per-frame selection (select_frame_warp) and the fused stages
-            float crt[kCandSmem];
-            uint2 pl[64];            // Phi_01 pair list: {i0 | i1 << 10, u(i0, i1)}
+        struct {
+            uint32_t cidx[kCandSmem];        // candidates (flat warp-batch index < kCandSmem)
+            union {
+                struct {                     // per-frame selection (select_frame_warp) and the fused stages
+                    float crt[kCandSmem];
+                    uint2 pl[64];            // Phi_01 pair list: {i0 | i1 << 10, u(i0, i1)}
+                };
+                FlatSel fl;                  // warp-batch-flat selection (select_batch_flat)
+            };
         };
-        FlatSel fl;                  // warp-batch-flat selection (select_batch_flat)
+        MaskSel<1> ms1;                      // mask-factorised big-frame selection (select_frame_mask)
+        MaskSel<2> ms2;
     };
     BatchState st;
     uint32_t pref[kFB + 1];          // candidates: exclusive prefix
@@ -162,6 +190,11 @@ struct __align__(16) WarpSmem {
     uint32_t q[64];                  // Delta-lambda + Phi_12 survivors (selection FIFO)
     uint32_t acc[12];                // run summary: kept_by_reason[6], cand, frames, tracks, hits, overflow
 };
+
+// the mask walks' state fits the space of the candidate array and the other walks'
+static_assert(sizeof(MaskSel<1>) <= kCandSmem * 4 + kCandSmem * 4 + 64 * 8 &&
+                  sizeof(MaskSel<2>) <= kCandSmem * 4 + kCandSmem * 4 + 64 * 8,
+              "mask-walk state larger than the space it overlays");
 
 struct Smem {
     WarpSmem w[kWarps];
@@ -506,8 +539,7 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             for (uint32_t t = 0; t < take; ++t) {
                 const int k = ffs_t(rem) - 1;
                 // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
-                const float z1 = hz[t1 + k];
-                const float u = z1 * P.inv_dr12 + (z1 - z0) * P.inv_dr01;
+                const float u = pair_u(P, z0, hz[t1 + k]);
                 S.pl[pos++] = make_uint4((uint32_t)g0 | ((uint32_t)(t1 + k) << 8) | ehi, __float_as_uint(u), m2, 0u);
                 rem &= rem - (MT)1;
             }
@@ -566,6 +598,243 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
         if (!fits) A.spill_out[atomicAdd(A.ticket + 5, 1u)] = b;   // for the fused kernel
     }
     return true;
+}
+
+// Selection Cuts (Alg. 2, Eq. 2-5) of one big frame (phase-II occupancy, up to 64
+// (NW = 1) or kMask2Hits (NW = 2) hits in layers 1 and 2; whole warp), factorised by
+// the hits each cut depends on so that no (i0, i1, i2) combination is evaluated
+// arithmetically:
+//   1. Phi_12 depends on (i1, i2) only: one lane per layer-1 hit computes its mask
+//      over layer 2, m12[i1] (n1 n2 tests instead of one per (i0, i1, i2));
+//   2. Delta-lambda = fma(z2, 1/dr12, -u(i0, i1)) is non-decreasing in z2 (for a
+//      given pair), so the layer-2 hits passing it form a contiguous run in z
+//      order: layer 2 is ranked by z once, with prefix masks pm[r] of the r lowest;
+//   3. one lane per (i0) row: the Phi_01 mask over layer 1, its set bits emitted in
+//      order to the pair list with u(i0, i1);
+//   4. one lane per listed pair: two binary searches over the sorted z give the
+//      run [lo, hi) with the very predicate |fma(z2, 1/dr12, -u)| <= dl_max, and the
+//      pair's layer-2 survivors are m12[i1] & pm[hi] & ~pm[lo]; their set bits go in
+//      order to the FIFO, whose full 32s are tested for the r_t window (Eq. 5).
+// Every decision is the per-hit fp32 test of the other walks (cos_sep2, pair_u,
+// pass_rtc_sq), so survivor set and (i0, i1, i2) order are those of Alg. 2 and the
+// other walks' (R3 overflow: stops past cuts_max).  Candidates i0 | i1 << 10 |
+// i2 << 20 go to out[pos], pos < cuts_max; returns min(#survivors, cuts_max + 1).
+// gm12: NW = 2 only, the warp's global scratch for m12 (n1 x 2 words).
+template <int NW>
+__device__ __forceinline__ int select_frame_mask(const DevParams& P, const Frame& F, MaskSel<NW>& M,
+                                                 unsigned long long* gm12, uint32_t* q, uint32_t* out) {
+    typedef unsigned long long u64;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int n0 = F.n[0], n1 = F.n[1], n2 = F.n[2];
+    if (n0 == 0 || n1 == 0 || n2 == 0) return 0;
+    const float *X = F.x, *Y = F.y, *Z = F.z;
+    const int s0 = F.s[0], s1 = F.s[1], s2 = F.s[2];
+    auto m12 = [&](int i1, int w) -> u64& {
+        if constexpr (NW == 1) return M.m12[i1];
+        else return gm12[2 * i1 + w];
+    };
+    auto pm = [&](int r, int w) -> u64& {
+        if constexpr (NW == 1) return M.pm[r];
+        else return M.pm[r][w];
+    };
+    // mask of the first n hits, word w
+    auto fullw = [](int n, int w) -> u64 {
+        const int b = n - 64 * w;
+        return b >= 64 ? ~0ull : (b <= 0 ? 0ull : (1ull << b) - 1ull);
+    };
+    // cut bits of hit a against layer-l hits k0.. (four per step, two per packed op);
+    // reads past the layer's end stay inside the window / input slack and are masked
+    auto row = [&](float xa, float ya, int sl, int nl, float inv, float cmin, u64 (&m)[NW]) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) m[w] = 0ull;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const int kend = min(nl - 64 * w, 64);
+            for (int k0 = 0; k0 < kend; k0 += 4) {
+#pragma unroll
+                for (int h = 0; h < 4; h += 2) {
+                    const int k = k0 + h, g = sl + 64 * w + k;
+                    const float2 c = cos_sep2(xa, ya, make_float2(X[g], X[g + 1]), make_float2(Y[g], Y[g + 1]), inv);
+                    const float2 d = __fadd2_rn(c, make_float2(-cmin, -cmin));   // c >= cmin: sign bit
+                    const uint32_t fail = (__float_as_uint(d.x) >> 31) | ((__float_as_uint(d.y) >> 30) & 2u);
+                    m[w] |= (u64)(fail ^ 3u) << k;
+                }
+            }
+            m[w] &= fullw(nl, w);
+        }
+    };
+    // 1. Phi_12 rows
+    for (int i1 = lane; i1 < n1; i1 += 32) {
+        u64 m[NW];
+        row(X[s1 + i1], Y[s1 + i1], s2, n2, P.inv_r1r2, P.c12_min, m);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) m12(i1, w) = m[w];
+    }
+    // 2. layer 2 ranked by z (ties by index), prefix masks in rank order
+    for (int i2 = lane; i2 < n2; i2 += 32) {
+        const float z = Z[s2 + i2];
+        int r = 0;
+        for (int k = 0; k < n2; ++k) {
+            const float zk = Z[s2 + k];
+            r += (int)((zk < z) | ((zk == z) & (k < i2)));
+        }
+        M.zs[r] = z;
+        M.ord[r] = (uint8_t)i2;
+    }
+    __syncwarp();
+    {   // lane l: ranks RPL l .. RPL l + RPL - 1 (RPL = 2 NW), an inclusive OR-scan per word
+        constexpr int RPL = 2 * NW;
+        u64 part[NW], inc[NW], ex[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) part[w] = 0ull;
+        const int r0 = RPL * lane;
+#pragma unroll
+        for (int t = 0; t < RPL; ++t)
+            if (r0 + t < n2) {
+                const int i = M.ord[r0 + t];
+                part[i >> 6] |= 1ull << (i & 63);
+            }
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            inc[w] = part[w];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u64 t = __shfl_up_sync(0xffffffffu, inc[w], o);
+                if (lane >= o) inc[w] |= t;
+            }
+            ex[w] = __shfl_up_sync(0xffffffffu, inc[w], 1);
+            if (lane == 0) {
+                ex[w] = 0ull;
+                pm(0, w) = 0ull;
+            }
+        }
+        // pm[r0 + t + 1] = ex | bits of ranks r0 .. r0 + t
+#pragma unroll
+        for (int t = 0; t < RPL; ++t)
+            if (r0 + t < n2) {
+                const int i = M.ord[r0 + t];
+                ex[i >> 6] |= 1ull << (i & 63);
+#pragma unroll
+                for (int w = 0; w < NW; ++w) pm(r0 + t + 1, w) = ex[w];
+            }
+    }
+    __syncwarp();
+    int count = 0, qn = 0, pn = 0;
+    // r_t window for q[0..n) (n <= 32); true once the frame overflows
+    auto drain = [&](int n) -> bool {
+        const uint32_t pk = q[min(lane, n - 1)];
+        const bool pass = lane < n && pass_rtc_sq(P, F, pk & 1023u, (pk >> 10) & 1023u, (pk >> 20) & 1023u);
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        const int pos = count + __popc(m & lt);
+        if (pass && pos < P.cuts_max) out[pos] = pk;
+        count += __popc(m);
+        return count > P.cuts_max;
+    };
+    // ordered emission of the set bits of every lane's mask (lower lanes first, word 0
+    // first) into list L (capacity 64, fill n); `sink(k, pos)` writes bit k at pos;
+    // `flush()` runs whenever >= 32 are listed and returns true on overflow
+    auto emit = [&](u64 (&rem)[NW], int& n, auto sink, auto flush) -> bool {
+        for (;;) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) c += (uint32_t)__popcll(rem[w]);
+            const uint32_t inc = warp_incl(c), exc = inc - c;
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            const uint32_t fr = 64u - (uint32_t)n;
+            const uint32_t take = exc >= fr ? 0u : min(c, fr - exc);
+            uint32_t pos = (uint32_t)n + exc;
+            for (uint32_t t = 0; t < take; ++t) {
+                int k;
+                if (NW == 1 || rem[0]) {
+                    k = __ffsll(rem[0]) - 1;
+                    rem[0] &= rem[0] - 1ull;
+                } else {
+                    k = 64 + __ffsll(rem[NW - 1]) - 1;
+                    rem[NW - 1] &= rem[NW - 1] - 1ull;
+                }
+                sink(k, pos++);
+            }
+            n += (int)min(tot, fr);
+            __syncwarp();
+            if (flush()) return true;
+            if (tot <= fr) return false;
+        }
+    };
+    // the first K = min(pn, 32) listed pairs: their layer-2 survivors, in order, to
+    // the FIFO; true once the frame overflows
+    auto expand = [&]() -> bool {
+        const int K = min(pn, 32);
+        u64 rem[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) rem[w] = 0ull;
+        uint32_t pe = 0;
+        if (lane < K) {
+            const uint2 e = M.pl[lane];
+            pe = e.x;
+            const float u = __uint_as_float(e.y);
+            int lo = 0, hi = n2;   // first z-rank with fma(z, 1/dr12, -u) >= -dl_max
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (fmaf(M.zs[mid], P.inv_dr12, -u) < -P.dl_max) lo = mid + 1; else hi = mid;
+            }
+            int lo2 = lo, hi2 = n2;   // first z-rank with fma(z, 1/dr12, -u) > dl_max
+            while (lo2 < hi2) {
+                const int mid = (lo2 + hi2) >> 1;
+                if (fmaf(M.zs[mid], P.inv_dr12, -u) > P.dl_max) hi2 = mid; else lo2 = mid + 1;
+            }
+            const int i1 = (int)((e.x >> 10) & 1023u);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) rem[w] = m12(i1, w) & pm(lo2, w) & ~pm(lo, w);
+        }
+        __syncwarp();
+        {   // drop the K expanded pairs
+            const uint2 v = lane < pn - K ? M.pl[K + lane] : make_uint2(0u, 0u);
+            __syncwarp();
+            if (lane < pn - K) M.pl[lane] = v;
+            pn -= K;
+            __syncwarp();
+        }
+        return emit(rem, qn, [&](int k, uint32_t pos) { q[pos] = pe | ((uint32_t)k << 20); },
+                    [&]() -> bool {
+                        while (qn >= 32) {
+                            if (drain(32)) return true;
+                            const uint32_t v = lane < qn - 32 ? q[32 + lane] : 0u;
+                            __syncwarp();
+                            if (lane < qn - 32) q[lane] = v;
+                            qn -= 32;
+                            __syncwarp();
+                        }
+                        return false;
+                    });
+    };
+    // 3. rows, 32 per step: Phi_01 masks, pairs emitted in order
+    for (int r0 = 0; r0 < n0; r0 += 32) {
+        const int i0 = r0 + lane;
+        u64 rem[NW];
+        float z0 = 0.0f;
+        if (i0 < n0) {
+            z0 = Z[s0 + i0];
+            row(X[s0 + i0], Y[s0 + i0], s1, n1, P.inv_r0r1, P.c01_min, rem);
+        } else {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) rem[w] = 0ull;
+        }
+        if (emit(rem, pn,
+                 [&](int k, uint32_t pos) {
+                     M.pl[pos] = make_uint2((uint32_t)i0 | ((uint32_t)k << 10), __float_as_uint(pair_u(P, z0, Z[s1 + k])));
+                 },
+                 [&]() -> bool {
+                     while (pn >= 32)
+                         if (expand()) return true;
+                     return false;
+                 }))
+            return P.cuts_max + 1;
+    }
+    while (pn > 0)
+        if (expand()) return P.cuts_max + 1;
+    if (qn > 0 && drain(qn)) return P.cuts_max + 1;
+    return count;
 }
 
 // Vertex selection of frame j (Sec. IV-C, Alg. 4; whole warp), out of line: it
@@ -729,6 +998,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
     m3e_fit_record* crec;
     m3e_track* ctrk_base;
     constexpr bool kFlat = MODE == kModeFull || MODE == kModeSelectC;   // flat warp-batch candidate index
+    // candidates below this flat index stay in shared memory (W.cidx); the big-frame
+    // selection kernel keeps them all in global memory (its mask walk overlays W.cidx)
+    constexpr uint32_t kCandS = (BIG && MODE == kModeSelectC) ? 0u : (uint32_t)kCandSmem;
     if constexpr (kFlat) {
         cidx = A.pool_idx + gwarp * A.pool_stride;
         crt = A.pool_rt + gwarp * A.pool_stride;
@@ -761,9 +1033,6 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
         bool flat_done = false;
         if constexpr (MODE == kModeSelectC && !M3E_NO_FLAT_SELECT) {
             flat_done = select_batch_flat<uint32_t>(A, W, b, f0, nf, cidx);
-            if constexpr (BIG) {
-                if (!flat_done) flat_done = select_batch_flat<unsigned long long>(A, W, b, f0, nf, cidx);
-            }
         }
         if constexpr (MODE == kModeFull || MODE == kModeSelect || MODE == kModeSelectC) {
           if (!flat_done) {
@@ -779,7 +1048,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
                     auto emit = [&](int pos, uint32_t packed, float rt) {
                         if constexpr (kFlat) {
                             const uint32_t fi = cbase + (uint32_t)pos;
-                            if (fi < (uint32_t)kCandSmem) {
+                            if (below(fi, kCandS)) {
                                 W.cidx[fi] = packed;
                                 W.crt[fi] = rt;
                             } else {
@@ -792,10 +1061,25 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
                         }
                     };
                     count = -1;
-                    if (BIG && (long long)Fv.n[0] * Fv.n[1] * Fv.n[2] > kBigCombos && A.pair_scratch) {
+                    if constexpr (BIG && MODE == kModeSelectC) {
+                        // big frames of up to 96 hits in layers 1 and 2: the mask-factorised walk
+                        if (Fv.n[1] <= 64 && Fv.n[2] <= 64) {
+                            count = select_frame_mask<1>(P, Fv, W.ms1, nullptr, W.q, cidx + cbase);
+                            __syncwarp();
+                        } else if (Fv.n[1] <= kMask2Hits && Fv.n[2] <= kMask2Hits && A.pair_scratch) {
+                            count = select_frame_mask<2>(
+                                P, Fv, W.ms2,
+                                reinterpret_cast<unsigned long long*>(
+                                    (reinterpret_cast<uintptr_t>(A.pair_scratch + gwarp * kPairWords) + 7) & ~(uintptr_t)7),
+                                W.q,
+                                cidx + cbase);
+                            __syncwarp();
+                        }
+                    }
+                    if (count < 0 && BIG && (long long)Fv.n[0] * Fv.n[1] * Fv.n[2] > kBigCombos && A.pair_scratch) {
                         CandSink sk;
                         if constexpr (kFlat) {
-                            sk = CandSink{W.cidx, W.crt, cidx, crt, cbase, (uint32_t)kCandSmem};
+                            sk = CandSink{W.cidx, W.crt, cidx, crt, cbase, kCandS};
                         } else {
                             sk = CandSink{ci, cr, ci, cr, 0u, 0u};
                         }
@@ -871,7 +1155,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
             for (uint32_t e = lane; e < nw; e += 32) {
                 uint4 c = make_uint4(0u, kSpilled, 0u, 0u);
                 if (fits) {
-                    const uint32_t pk = e < (uint32_t)kCandSmem ? W.cidx[e] : cidx[e];
+                    const uint32_t pk = below(e, kCandS) ? W.cidx[e] : cidx[e];
                     const int j = find_frame(W.pref, nf, e);
                     const uint32_t* of = W.offs[buf] + 4 * j;
                     c.x = of[0];                                  // frame's first hit
