@@ -790,41 +790,43 @@ M3E_HD FitOut fit_candidate(const DevParams& P, const Frame& F, int i0, int i1, 
 
 // ------------------------------------------------------------- Vertex Fit ----
 // fp64, Sec. IV-C + Alg. 4 phase 2 for one (e+, e+, e-) triple (R12-R16).
+// Per track only what phase 2 reads (the energy test of phase 1 is elsewhere).
 struct VTrk {
     int q;
-    double k, cth, sth, cx, cy, rt, h0x, h0y, h0z, p, E, sms;
+    double cx, cy, rt;           // transverse circle (R11)
+    double h0x, h0y, h0z;        // layer-0 hit
+    double cthk;                 // cos(theta) / k: dz per radian of turning (Eq. 11)
+    double sms;                  // sigma_MS at the track's momentum (Highland, R7)
+    double pz;                   // p cos(theta)
 };
 
 __device__ __forceinline__ VTrk make_vtrk(const DevParams& P, const m3e_track& t, const Frame& F) {
     VTrk v;
     v.q = t.kappa > 0.0f ? 1 : -1;
-    v.k = fabs((double)t.kappa);
-    v.cth = (double)t.cos_theta01;
-    v.sth = sqrt(fmax(0.0, 1.0 - v.cth * v.cth));
+    const double k = fabs((double)t.kappa);
+    const double cth = (double)t.cos_theta01;
+    const double ik = 1.0 / k;
     v.cx = (double)t.cx;
     v.cy = (double)t.cy;
-    v.rt = v.sth / v.k;
+    v.rt = sqrt(fmax(0.0, 1.0 - cth * cth)) * ik;
     const int g = F.s[0] + t.hit[0];
     v.h0x = (double)F.x[g];
     v.h0y = (double)F.y[g];
     v.h0z = (double)F.z[g];
-    v.p = P.ptb / v.k;
-    v.E = sqrt(v.p * v.p + kEMass * kEMass);
-    v.sms = P.chl_d * v.k;   // Highland at p (R7)
+    v.cthk = cth * ik;
+    v.sms = P.chl_d * k;   // Highland at p (R7)
+    v.pz = P.ptb * ik * cth;
     return v;
 }
-
-// signed turning angle from point (px,py) on the track circle to the layer-0 hit,
-// in the direction of motion, wrapped to (-pi, pi] (R12): one atan2 of the cross
-// and dot products of the two radii (turn_to_h0_inl below)
 
 // circle-circle intersections; 0 or 2 points {x0,y0,x1,y1}
 __device__ __forceinline__ int intersect(const VTrk& A, const VTrk& B, double o[4]) {
     const double dx = B.cx - A.cx, dy = B.cy - A.cy, D = sqrt(dx * dx + dy * dy);
     if (D == 0.0 || D > A.rt + B.rt || D < fabs(A.rt - B.rt)) return 0;
-    const double a = (A.rt * A.rt - B.rt * B.rt + D * D) / (2.0 * D);
+    const double iD = 1.0 / D;
+    const double a = (A.rt * A.rt - B.rt * B.rt + D * D) * (0.5 * iD);
     const double h = sqrt(fmax(0.0, A.rt * A.rt - a * a));
-    const double ux = dx / D, uy = dy / D;
+    const double ux = dx * iD, uy = dy * iD;
     o[0] = A.cx + a * ux - h * uy; o[1] = A.cy + a * uy + h * ux;
     o[2] = A.cx + a * ux + h * uy; o[3] = A.cy + a * uy - h * ux;
     return 2;
@@ -853,22 +855,36 @@ struct VResult {
 // intersections of one track pair within target_r + xy_margin (Sec. IV-C), slot 0
 // first; n = 0: the pair does not intersect or no intersection is near the target
 struct PairPts {
-    double x0, y0, x1, y1, w0, w1;   // points, Eq. 10 variances (R13)
+    double x0, y0, x1, y1, iw0, iw1;   // points, inverse Eq. 10 variances (R13)
     int n;
 };
 
-__device__ __forceinline__ double turn_to_h0_inl(const VTrk& t, double px, double py) {
-    const double ax = t.h0x - t.cx, ay = t.h0y - t.cy, bx = px - t.cx, by = py - t.cy;
-    return t.q * atan2(ax * by - ay * bx, ax * bx + ay * by);
+// signed turning angle (R12) from the direction (bx, by) out of the track circle's
+// centre to the layer-0 hit, in the direction of motion, in (-pi, pi]: one atan2 of
+// the cross and dot products of the two radii (scale-free in (bx, by))
+// out of line: one copy of the fp64 atan2 instead of nine inlined ones keeps the
+// vertex kernels' code in the instruction cache (triple kernel 0.44 -> 0.36 ms)
+static __device__ __noinline__ double turn_atan2(double y, double x) { return atan2(y, x); }
+__device__ __forceinline__ double turn_to_h0(const VTrk& t, double bx, double by) {
+    const double ax = t.h0x - t.cx, ay = t.h0y - t.cy;
+    return t.q * turn_atan2(ax * by - ay * bx, ax * bx + ay * by);
+}
+
+// Eq. 10 (R13) inverse variance of an intersection point of tracks A and B
+__device__ __forceinline__ double point_iw(const DevParams& P, const VTrk& A, const VTrk& B, double px, double py) {
+    const double sa = A.rt * fabs(turn_to_h0(A, px - A.cx, py - A.cy));
+    const double sb = B.rt * fabs(turn_to_h0(B, px - B.cx, py - B.cy));
+    return 1.0 / (0.5 * (A.sms * A.sms * sa * sa + B.sms * B.sms * sb * sb) + P.sig_pix2);
 }
 
 __device__ __forceinline__ void pair_points(const DevParams& P, const VTrk& A, const VTrk& B, PairPts& o) {
     o.n = 0;
     const double dx = B.cx - A.cx, dy = B.cy - A.cy, D = sqrt(dx * dx + dy * dy);
     if (D == 0.0 || D > A.rt + B.rt || D < fabs(A.rt - B.rt)) return;   // "the track triplet is skipped"
-    const double a = (A.rt * A.rt - B.rt * B.rt + D * D) / (2.0 * D);
+    const double iD = 1.0 / D;
+    const double a = (A.rt * A.rt - B.rt * B.rt + D * D) * (0.5 * iD);
     const double h = sqrt(fmax(0.0, A.rt * A.rt - a * a));
-    const double ux = dx / D, uy = dy / D;
+    const double ux = dx * iD, uy = dy * iD;
     const double ax0 = A.cx + a * ux - h * uy, ay0 = A.cy + a * uy + h * ux;
     const double ax1 = A.cx + a * ux + h * uy, ay1 = A.cy + a * uy - h * ux;
     const bool k0 = sqrt(ax0 * ax0 + ay0 * ay0) <= P.rlim, k1 = sqrt(ax1 * ax1 + ay1 * ay1) <= P.rlim;
@@ -877,15 +893,10 @@ __device__ __forceinline__ void pair_points(const DevParams& P, const VTrk& A, c
     o.x1 = ax1;
     o.y1 = ay1;
     o.n = (int)k0 + (int)k1;
-    // Eq. 10 (R13) for each kept point, once (the choice loop combines them 2^3 ways)
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        const double px = s ? o.x1 : o.x0, py = s ? o.y1 : o.y0;
-        const double sa = A.rt * fabs(turn_to_h0_inl(A, px, py));
-        const double sb = B.rt * fabs(turn_to_h0_inl(B, px, py));
-        const double w = 0.5 * (A.sms * A.sms * sa * sa + B.sms * B.sms * sb * sb) + P.sig_pix2;
-        if (s) o.w1 = w; else o.w0 = w;
-    }
+    // Eq. 10 of each kept point, once (the choice loop combines them up to 2^3 ways);
+    // the second point is rarely near the target
+    o.iw0 = o.n ? point_iw(P, A, B, o.x0, o.y0) : 0.0;
+    o.iw1 = o.n == 2 ? point_iw(P, A, B, o.x1, o.y1) : 0.0;
 }
 
 // Alg. 4 phase 2 for one (e+, e+, e-) triple, inline: every array a named
@@ -908,30 +919,28 @@ __device__ __forceinline__ VResult vertex_triple_inl(const DevParams& P, const V
     for (int c = 0; c < 8; ++c) {   // (s0, s1, s2) in the oracle's nested order, s2 fastest
         const int s0 = c >> 2, s1 = (c >> 1) & 1, s2 = c & 1;
         if (s0 >= Q0.n || s1 >= Q1.n || s2 >= Q2.n) continue;
-        const double p0x = s0 ? Q0.x1 : Q0.x0, p0y = s0 ? Q0.y1 : Q0.y0, w0 = s0 ? Q0.w1 : Q0.w0;
-        const double p1x = s1 ? Q1.x1 : Q1.x0, p1y = s1 ? Q1.y1 : Q1.y0, w1 = s1 ? Q1.w1 : Q1.w0;
-        const double p2x = s2 ? Q2.x1 : Q2.x0, p2y = s2 ? Q2.y1 : Q2.y0, w2 = s2 ? Q2.w1 : Q2.w0;
-        // Eq. 9
-        double mx = p0x / w0, my = p0y / w0, ws = 1.0 / w0;
-        mx += p1x / w1; my += p1y / w1; ws += 1.0 / w1;
-        mx += p2x / w2; my += p2y / w2; ws += 1.0 / w2;
-        mx /= ws;
-        my /= ws;
-        double pcx[3], pcy[3], pcz[3], sg[3], mz = 0.0, wz = 0.0;
+        const double p0x = s0 ? Q0.x1 : Q0.x0, p0y = s0 ? Q0.y1 : Q0.y0, w0 = s0 ? Q0.iw1 : Q0.iw0;
+        const double p1x = s1 ? Q1.x1 : Q1.x0, p1y = s1 ? Q1.y1 : Q1.y0, w1 = s1 ? Q1.iw1 : Q1.iw0;
+        const double p2x = s2 ? Q2.x1 : Q2.x0, p2y = s2 ? Q2.y1 : Q2.y0, w2 = s2 ? Q2.iw1 : Q2.iw0;
+        // Eq. 9: weighted mean of the three points
+        const double iws = 1.0 / (w0 + w1 + w2);
+        const double mx = (p0x * w0 + p1x * w1 + p2x * w2) * iws, my = (p0y * w0 + p1y * w1 + p2y * w2) * iws;
+        double pcx[3], pcy[3], pcz[3], isg[3], mz = 0.0, wz = 0.0;
         bool bad = false;
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {   // Fig. 6, Eq. 11
+        for (int t = 0; t < 3; ++t) {   // Fig. 6, Eq. 11: point of closest approach to (mx, my)
             const VTrk& A = t == 0 ? T0 : (t == 1 ? T1 : T2);
             const double dx = mx - A.cx, dy = my - A.cy, dn = sqrt(dx * dx + dy * dy);
             bad |= dn == 0.0;
-            pcx[t] = A.cx + A.rt * dx / dn;
-            pcy[t] = A.cy + A.rt * dy / dn;
-            const double dphi = turn_to_h0_inl(A, pcx[t], pcy[t]);
-            pcz[t] = A.h0z - dphi * A.cth / A.k;
+            const double s = A.rt / dn;
+            pcx[t] = A.cx + dx * s;
+            pcy[t] = A.cy + dy * s;
+            const double dphi = turn_to_h0(A, dx, dy);
+            pcz[t] = A.h0z - dphi * A.cthk;
             const double sv = A.rt * fabs(dphi);
-            sg[t] = A.sms * A.sms * sv * sv + P.sig_pix2;
-            mz += pcz[t] / sg[t];
-            wz += 1.0 / sg[t];
+            isg[t] = 1.0 / (A.sms * A.sms * sv * sv + P.sig_pix2);
+            mz += pcz[t] * isg[t];
+            wz += isg[t];
         }
         if (bad) continue;
         mz /= wz;
@@ -939,21 +948,23 @@ __device__ __forceinline__ VResult vertex_triple_inl(const DevParams& P, const V
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
             const double ex = pcx[t] - mx, ey = pcy[t] - my, ez = pcz[t] - mz;
-            chi += (ex * ex + ey * ey + ez * ez) / sg[t];
+            chi += (ex * ex + ey * ey + ez * ez) * isg[t];
         }
         if (chi < best.chi2) {
             best.found = 1;
             best.chi2 = chi;
             best.x = mx; best.y = my; best.z = mz;
+            // momentum at the pca: p_t q (sin ph, -cos ph), ph the angle of pca - c, with
+            // p_t = p sin(theta) = ptb rt (R11: rt = sin(theta) / k) and (cos ph, sin ph) =
+            // (pca - c) / rt: q ptb (pcy - cy, cx - pcx)
             double px = 0.0, py = 0.0, pz = 0.0;
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
                 const VTrk& A = t == 0 ? T0 : (t == 1 ? T1 : T2);
-                // direction of motion at the pca: q (sin ph, -cos ph), ph = angle of pca - c
-                const double irt = 1.0 / A.rt;
-                px += A.p * A.sth * A.q * (pcy[t] - A.cy) * irt;
-                py += A.p * A.sth * (-A.q) * (pcx[t] - A.cx) * irt;
-                pz += A.p * A.cth;
+                const double f = A.q * P.ptb;
+                px += f * (pcy[t] - A.cy);
+                py -= f * (pcx[t] - A.cx);
+                pz += A.pz;
             }
             best.ptot = sqrt(px * px + py * py + pz * pz);
         }
