@@ -296,12 +296,11 @@ def _outputs(res, n):
 
 
 def test_phase2_split_and_fused_agree(gp, monkeypatch):
-    """Phase-II frames (~220 hits) take the split path too (64-bit row masks in
-    the selection, store sized for ~330 candidates per frame, a triple list of up
-    to 32 per frame): byte-identical to the fused kernel on this set, also with a
-    store that forces spills.  (The fused kernel's big-frame walk evaluates
-    Delta-lambda as a difference of pair slopes, so on other data the two may
-    differ for a combination within an ulp of the cut: 1 frame in 1e6.)"""
+    """Phase-II frames (~220 hits) take the split path too (the mask-factorised
+    selection walk, store sized for ~330 candidates per frame, a triple list of up
+    to 32 per frame): byte-identical to the fused kernel (pair-list walk), also
+    with a store that forces spills.  Every walk evaluates each cut with the same
+    fp32 expression (cos_sep, pair_u), so the candidate lists agree exactly."""
     n = 80
     d, fr, df = _gen("phase2_stress", n, 731)
     outs = []
@@ -318,6 +317,41 @@ def test_phase2_split_and_fused_agree(gp, monkeypatch):
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert np.array_equal(a, b)
+
+
+def test_dense_frames_mask_walks(gp, P, monkeypatch):
+    """Frames denser than phase II (1.2e9 and 1.7e9 mu/s: ~67 / ~95 hits per layer)
+    drive the selection kernel's mask walks with 64-bit (n1, n2 <= 64) and 128-bit
+    (<= 96) masks and the pair-list walk beyond: item by item against the oracle,
+    and byte-identical to the fused kernel, which takes the pair-list walk for
+    every big frame."""
+    for rate, n, seed in ((1.2e9, 40, 741), (1.7e9, 12, 742)):
+        sc = synth.SynthConfig(muon_rate=rate, seed=seed)
+        d = synth.generate(sc, n)
+        fr, df = oracle.Frames(d), m3e.DeviceFrames(d)
+        cnt = np.diff(d["offsets"].astype(np.int64)).reshape(-1, 4)
+        m = np.maximum(cnt[:, 1], cnt[:, 2])
+        print(f"rate {rate:.2g}: frames with max(n1, n2) <= 64 / <= 96 / > 96:",
+              int((m <= 64).sum()), int(((m > 64) & (m <= 96)).sum()), int((m > 96).sum()))
+        outs = []
+        for env in [{}, {"M3E_FUSED": "1"}]:
+            monkeypatch.delenv("M3E_FUSED", raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            c = m3e.Context(0)
+            res = m3e.run_filter(c, gp, df)
+            torch.cuda.synchronize()
+            if not env:
+                tally = _compare_full(P, fr, res, n, f"dense {rate:.2g}")
+                assert len(tally.frames) <= 1
+            outs.append(_outputs(res, n))
+            c.close()
+        for a, b in zip(outs[0], outs[1]):
+            assert np.array_equal(a, b)
+        if rate < 1.5e9:
+            assert ((m > 64) & (m <= 96)).sum() >= n // 4 and (m <= 64).sum() >= 2
+        else:
+            assert (m > 96).sum() >= 1
 
 
 def test_vertex_triple_list_full(gp, monkeypatch):

@@ -40,6 +40,9 @@ def short_name(name: str) -> str:
     if "filter_kernel<0" in name or "filter_kernel<(int)0" in name:
         big = "true" if ("true" in name or ", 1>" in name) else "false"
         return f"m3e::filter_kernel<FULL, BIG={big}>"
+    if "fit_kernel<" in name:   # fit_kernel<BIG>: the phase-I variant is bench.py's "m3e::fit_kernel"
+        big = "true" in name or "<1>" in name or "(bool)1" in name
+        return "m3e::fit_kernel<BIG>" if big else "m3e::fit_kernel"
     base = name.split("(")[0]
     return base if base.startswith("m3e::") else "m3e::" + base
 
