@@ -1593,7 +1593,6 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
     extern __shared__ __align__(16) uint8_t pack_smem_raw[];
     PackSmem& S = *reinterpret_cast<PackSmem*>(pack_smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const unsigned lt = (1u << lane) - 1u;
     const m3e_outputs& O = A.out;
     const DevParams& P = A.P;
     const uint32_t ntiles = (A.nbatch + kPackTile - 1) / kPackTile;
@@ -1766,93 +1765,39 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
                 }
             }
         }
-        // ---- kept frames (rare): each warp takes its warp-batches that keep any;
-        // the lanes are that warp-batch's frames (fit path) or its staged records
-        unsigned todo = __ballot_sync(0xffffffffu, n_kept > 0);
-        while (todo) {
-            const int sl = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const uint32_t bb = t * kPackTile + warp * 32 + sl;
-            const bool bfused = __shfl_sync(0xffffffffu, fused ? 1u : 0u, sl) != 0u;
-            const uint32_t nk = __shfl_sync(0xffffffffu, n_kept, sl);
-            const uint32_t sk = __shfl_sync(0xffffffffu, s_kept, sl);
-            const uint32_t gk = __shfl_sync(0xffffffffu, g_kept_b, sl);
-            uint32_t gh = __shfl_sync(0xffffffffu, g_hits_b, sl);
-            const uint32_t nfb = min(A.F - bb * fb, fb);
-            for (uint32_t k0 = 0; k0 < (bfused ? nk : nfb); k0 += 32) {
-                const uint32_t k = k0 + lane;
-                uint32_t f = 0, nh = 0, lo = 0;
-                bool valid = false;
-                m3e_vertex vx;
-                if (bfused) {   // staged kept records of the fused kernel
-                    valid = k < nk && sk + k < A.stage_kept_cap;
-                    if (k < nk && !valid) overflow = true;
-                    if (valid) {
-                        const KeptRec kr = A.stage_kept[sk + k];
-                        f = kr.frame;
-                        vx = kr.v;
-                    }
-                } else if (k < nfb) {   // the warp-batch's frames
-                    f = bb * fb + k;
-                    const uint32_t w = S.fw[(warp * 32 + sl) * fb + k];
-                    const int reason = (int)(w >> 24);
-                    valid = reason != M3E_REASON_NONE;
-                    if (valid) {
-                        if (reason == M3E_REASON_VERTEX) {
-                            vx = A.vrec[A.vk[f]];
-                        } else {
-                            vx = m3e_vertex{};
-                            vx.frame = 0xFFFFFFFFu;
-                        }
-                    }
-                }
-                const unsigned mk = __ballot_sync(0xffffffffu, valid);
-                if (valid) {
-                    lo = A.offsets[4 * (size_t)f];
-                    nh = A.offsets[4 * (size_t)f + 4] - lo;
-                }
-                const uint32_t inc = warp_incl(nh);   // prefix of the kept frames' hit counts
-                const uint32_t hb = gh + inc - nh;
-                const uint32_t kidx = gk + (bfused ? k : (uint32_t)__popc(mk & lt));
-                if (valid) {
-                    if (kidx < O.kept_capacity) {
-                        if (O.kept_frame) O.kept_frame[kidx] = f;
-                        if (O.vertices) O.vertices[kidx] = vx;
-                        if (O.kept_offsets)
-                            for (int l = 0; l < 4; ++l)
-                                O.kept_offsets[4 * (size_t)kidx + l] = hb + (A.offsets[4 * (size_t)f + l] - lo);
-                    } else {
+        // ---- kept frames (rare): each one's {frame, first packed hit, vertex source}
+        // listed at its kept index; kept_kernel copies them (no dependent loads here:
+        // a slow warp would hold the whole tile at its barriers)
+        if (inb && n_kept > 0) {
+            uint32_t kidx = g_kept_b, hb = g_hits_b;
+            if (fused) {   // the fused kernel's staged kept records
+                for (uint32_t j = 0; j < n_kept; ++j, ++kidx) {
+                    if (s_kept + j >= A.stage_kept_cap || kidx >= O.kept_capacity) {
                         overflow = true;
+                        continue;
                     }
+                    const uint32_t f = A.stage_kept[s_kept + j].frame;
+                    A.kept_rec[kidx] = make_uint4(f, hb, 0x80000000u | (s_kept + j), 0u);
+                    hb += A.offsets[4 * (size_t)f + 4] - A.offsets[4 * (size_t)f];
                 }
-                if (O.kept_x) {
-                    unsigned mm = mk;
-                    while (mm) {
-                        const int s2 = __ffs(mm) - 1;
-                        mm &= mm - 1;
-                        const uint32_t fl = __shfl_sync(0xffffffffu, lo, s2);
-                        const uint32_t fn = __shfl_sync(0xffffffffu, nh, s2);
-                        const uint32_t fh = __shfl_sync(0xffffffffu, hb, s2);
-                        for (uint32_t e = lane; e < fn; e += 32) {
-                            const uint32_t dst = fh + e;
-                            if (dst < O.kept_hit_capacity) {
-                                O.kept_x[dst] = A.x[fl + e];
-                                O.kept_y[dst] = A.y[fl + e];
-                                O.kept_z[dst] = A.z[fl + e];
-                            } else {
-                                overflow = true;
-                            }
-                        }
-                    }
+            } else {
+                const uint32_t nf = min(A.F - b * fb, fb);
+                for (uint32_t j = 0; j < nf; ++j) {
+                    const uint32_t i = tid * fb + j, r = S.fw[i] >> 24;
+                    if (r == M3E_REASON_NONE) continue;
+                    if (kidx < O.kept_capacity) A.kept_rec[kidx] = make_uint4(b * fb + j, hb, r, 0u);
+                    else overflow = true;
+                    ++kidx;
+                    hb += S.fhit[i];
                 }
-                gh += __shfl_sync(0xffffffffu, inc, 31);
-                if (!bfused) break;   // a warp-batch has at most 32 frames (fb <= kFB)
             }
         }
-        // the call's last warp-batch closes the packed offsets
-        if (inb && b == A.nbatch - 1 && O.kept_offsets) {
+        // the call's last warp-batch closes the packed offsets and publishes the
+        // kept-frame count for kept_kernel
+        if (inb && b == A.nbatch - 1) {
             const uint32_t K = g_kept_b + n_kept;
-            if (K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = g_hits_b + n_hits;
+            if (O.kept_offsets && K <= O.kept_capacity) O.kept_offsets[4 * (size_t)K] = g_hits_b + n_hits;
+            A.ticket[13] = K;
         }
         __syncthreads();
     }
@@ -1862,6 +1807,57 @@ __global__ void __launch_bounds__(kThreads, M3E_PACK_MIN_BLOCKS) pack_kernel(con
     for (int r = 0; r < 12; ++r) sacc[r] = warp_sum(acc[r]);
     sacc[10] = __any_sync(0xffffffffu, overflow) ? 1u : 0u;
     if (lane == 0 && O.summary) flush_summary(O.summary, sacc);
+}
+
+// ------------------------------------------------------------- kept kernel ----
+// The kept frames listed by the pack kernel (kept_rec[k] = {frame, first packed hit,
+// vertex source}), one warp each: frame index, packed layer offsets, vertex record
+// (the vertex stage's, the fused kernel's staged one, or none) and the hits, SoA.
+__global__ void __launch_bounds__(kThreads) kept_kernel(const __grid_constant__ KArgs A) {
+    const int lane = threadIdx.x & 31;
+    const m3e_outputs& O = A.out;
+    const uint32_t K = min(*reinterpret_cast<const volatile uint32_t*>(A.ticket + 13), (uint32_t)O.kept_capacity);
+    bool overflow = false;
+    for (uint32_t k = (blockIdx.x * kThreads + threadIdx.x) >> 5; k < K; k += (gridDim.x * kThreads) >> 5) {
+        const uint4 r = A.kept_rec[k];
+        const uint32_t f = r.x, hb = r.y;
+        const uint32_t lo = A.offsets[4 * (size_t)f];
+        const uint32_t nh = A.offsets[4 * (size_t)f + 4] - lo;
+        if (lane == 0) {
+            if (O.kept_frame) O.kept_frame[k] = f;
+            if (O.vertices) {
+                m3e_vertex vx;
+                if (r.z & 0x80000000u) {
+                    vx = A.stage_kept[r.z & 0x7FFFFFFFu].v;
+                } else if (r.z == M3E_REASON_VERTEX) {
+                    vx = A.vrec[A.vk[f]];
+                } else {
+                    vx = m3e_vertex{};
+                    vx.frame = 0xFFFFFFFFu;
+                }
+                O.vertices[k] = vx;
+            }
+        }
+        if (O.kept_offsets && lane < 4) O.kept_offsets[4 * (size_t)k + lane] = hb + (A.offsets[4 * (size_t)f + lane] - lo);
+        if (O.kept_x)
+            for (uint32_t e = lane; e < nh; e += 32) {
+                const uint32_t dst = hb + e;
+                if (dst < O.kept_hit_capacity) {
+                    O.kept_x[dst] = A.x[lo + e];
+                    O.kept_y[dst] = A.y[lo + e];
+                    O.kept_z[dst] = A.z[lo + e];
+                } else {
+                    overflow = true;
+                }
+            }
+    }
+    if (__any_sync(0xffffffffu, overflow) && lane == 0 && O.summary)
+        atomicExch(reinterpret_cast<unsigned long long*>(&O.summary->overflow), 1ull);
+}
+
+cudaError_t launch_kept(const KArgs& a, int grid, cudaStream_t s) {
+    kept_kernel<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ fit kernel ----

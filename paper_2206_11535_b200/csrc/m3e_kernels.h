@@ -67,7 +67,8 @@ struct KArgs {
                            // tracks, [2] staged kept frames, [3] pack-kernel tile ticket, [4] filter
                            // warp-batch ticket, [5] spilled warp-batches, [6..7] candidate-store fill (u64),
                            // [8] fit-kernel unit ticket, [9] vertex-list fill, [10] (unused)
-                           // group ticket, [11] triple-list fill
+                           // group ticket, [11] triple-list fill, [12] slot-scan tile ticket, [13] kept
+                           // frames (pack kernel -> kept kernel)
     uint32_t* bticket;     // this launch's warp-batch ticket (ticket + 0 or ticket + 4)
     // candidate store of the split path (kModeSelectC writes, fit_kernel reads)
     uint32_t* spill_out;   // kModeSelectC: appends the warp-batches that did not fit (count in ticket[5])
@@ -103,6 +104,8 @@ struct KArgs {
     uint64_t stage_trk_cap;
     KeptRec* stage_kept;   // staged kept-frame records
     uint64_t stage_kept_cap;
+    uint4* kept_rec;       // [out.kept_capacity] pack -> kept kernel: {frame, first packed hit, vertex
+                           // source: reason, or 1 << 31 | stage_kept index}, count in ticket[13]
     // per-CTA scratch (MODE_FULL)
     uint32_t* pool_idx;
     float* pool_rt;
@@ -142,6 +145,7 @@ cudaError_t launch_rebase(const Rebase& r, int sms, cudaStream_t s);
 size_t smem_bytes();
 cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_kept(const KArgs& a, int grid, cudaStream_t s);
 constexpr int kScanItems = 8;                          // warp-batches per thread of slot_scan_kernel
 constexpr int kScanTile = kThreads * kScanItems;       // warp-batches per tile (CTA iteration)
 cudaError_t launch_slot_scan(const KArgs& a, int grid, cudaStream_t s);

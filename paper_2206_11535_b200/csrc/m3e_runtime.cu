@@ -56,6 +56,7 @@ struct Workspace {
     size_t stage_trk_n = 0;
     KeptRec* stage_kept = nullptr;
     size_t stage_kept_n = 0;
+    uint4* kept_rec = nullptr;          // kept-frame list (pack -> kept kernel)
     uint32_t* pair_scratch = nullptr;   // big-frame selection lists, kPairWords per warp
     int pair_warps = 0;
     void* vscratch = nullptr;           // vertex-stage scratch, kVScratchBytes per warp
@@ -148,6 +149,7 @@ void free_ws(Workspace& w) {
     cudaFree(w.bstat);
     cudaFree(w.stage_trk);
     cudaFree(w.stage_kept);
+    cudaFree(w.kept_rec);
     cudaFree(w.ticket);
     cudaFree(w.status);
     cudaFree(w.pool_idx);
@@ -371,12 +373,15 @@ int ensure_stage(Workspace& w, uint64_t trk, uint64_t kept) {
         w.stage_trk_n = trk;
         w.bytes += trk * sizeof(m3e_track);
     }
-    if (w.stage_kept_n < kept) {
+    if (w.stage_kept_n < kept || !w.kept_rec) {
         cudaFree(w.stage_kept);
-        w.bytes -= w.stage_kept_n * sizeof(KeptRec);
+        cudaFree(w.kept_rec);
+        w.bytes -= w.stage_kept_n * (sizeof(KeptRec) + sizeof(uint4));
+        kept = std::max<uint64_t>(kept, 1);
         CK(cudaMalloc(&w.stage_kept, kept * sizeof(KeptRec)));
+        CK(cudaMalloc(&w.kept_rec, kept * sizeof(uint4)));
         w.stage_kept_n = kept;
-        w.bytes += kept * sizeof(KeptRec);
+        w.bytes += kept * (sizeof(KeptRec) + sizeof(uint4));
     }
     return M3E_OK;
 }
@@ -445,6 +450,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         a.stage_trk = want_trk ? w.stage_trk : nullptr;
         a.stage_trk_cap = want_trk ? a.out.track_capacity : 0;
         a.stage_kept = w.stage_kept;
+        a.kept_rec = w.kept_rec;
         a.stage_kept_cap = a.out.kept_capacity;
     }
     CK(cudaMemsetAsync(w.ticket, 0, 16 * sizeof(uint32_t), s));
@@ -510,6 +516,7 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
         const uint64_t ntiles = (nbatch + kPackTile - 1) / kPackTile;
         const int pgrid = (int)std::min<uint64_t>(ntiles, (uint64_t)ctx->sms * 8);
         CK(launch_pack(a, pgrid, s));
+        CK(launch_kept(a, ctx->sms * 4, s));   // the kept frames the pack kernel listed
     }
     if (tm) {
         CK(cudaEventRecord(ev[6], s));
