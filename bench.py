@@ -400,10 +400,10 @@ def main():
                      ("fit", "m3e::fit_kernel", ms_fit, in_bytes + 32 * tracks),
                      ("vertex", "m3e::vertex_kernel+triple_kernel+vpost_kernel", ms_vertex, 0),
                      ("fused_spilled", "m3e::filter_kernel<FULL, BIG=false>", ms_filter, 0),
-                     ("pack", "m3e::pack_kernel", ms_pack, out_bytes - 32 * tracks)]   # (the fit writes the tracks)
+                     ("pack", "m3e::pack_kernel+kept_kernel", ms_pack, out_bytes - 32 * tracks)]   # (the fit writes the tracks)
         else:
             names = [("filter", "m3e::filter_kernel<FULL, BIG=%s>" % ("true" if big else "false"), ms_filter,
-                      in_bytes + out_bytes), ("pack", "m3e::pack_kernel", ms_pack, out_bytes)]
+                      in_bytes + out_bytes), ("pack", "m3e::pack_kernel+kept_kernel", ms_pack, out_bytes)]
         per = {}
         for key, kn, kt, alg in names:
             e = {"ms": round(kt, 4), "share": round(kt / ms_step, 4), "method_bytes": int(alg)}

@@ -12,7 +12,7 @@ python bench.py > $O/bench_line.json 2> $O/bench_line.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/bench_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-phys > $O/launches.log 2>&1
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,sm__inst_issued.avg.pct_of_peak_sustained_active,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active,launch__registers_per_thread
-ncu --kernel-name-base demangled -k regex:m3e:: -s 24 -c 8 --clock-control none --metrics $M -o $O/traffic \
+ncu --kernel-name-base demangled -k regex:m3e:: -s 27 -c 9 --clock-control none --metrics $M -o $O/traffic \
     python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-phys > $O/traffic.log 2>&1
 python tools/ncu_traffic.py $O/traffic.ncu-rep $O/${R}_bench_traffic.json \
     "ncu --metrics <see tools/capture_profiles.sh> python bench.py --steps 1 --warmup 3 (the step after the warm-up)" > $O/traffic.txt 2>&1
