@@ -37,7 +37,8 @@
 #define M3E_MIN_BLOCKS_SEL 4   // same for the selection kernel of the split path
 #endif
 #ifndef M3E_MIN_BLOCKS_SEL_BIG
-#define M3E_MIN_BLOCKS_SEL_BIG 4   // its big-frame variant (3: 80 registers, no spills, but 30.3 against 28.4 ms per 1e6 phase-II frames)
+#define M3E_MIN_BLOCKS_SEL_BIG 3   // its big-frame variant: 80 registers (the mask walks: 16.5 against 18.2 ms per 1e6
+                                   // phase-II frames at 4 CTAs / 64 registers; the row-mask walk before them: 30.3 / 28.4)
 #endif
 
 namespace m3e {
@@ -693,7 +694,9 @@ __device__ __forceinline__ int select_frame_mask(const DevParams& P, const Frame
         for (int t = 0; t < RPL; ++t)
             if (r0 + t < n2) {
                 const int i = M.ord[r0 + t];
-                part[i >> 6] |= 1ull << (i & 63);
+#pragma unroll
+                for (int w = 0; w < NW; ++w)   // (constant indices: the words stay in registers)
+                    if ((i >> 6) == w) part[w] |= 1ull << (i & 63);
             }
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
@@ -714,7 +717,9 @@ __device__ __forceinline__ int select_frame_mask(const DevParams& P, const Frame
         for (int t = 0; t < RPL; ++t)
             if (r0 + t < n2) {
                 const int i = M.ord[r0 + t];
-                ex[i >> 6] |= 1ull << (i & 63);
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+                    if ((i >> 6) == w) ex[w] |= 1ull << (i & 63);
 #pragma unroll
                 for (int w = 0; w < NW; ++w) pm(r0 + t + 1, w) = ex[w];
             }
@@ -1556,19 +1561,21 @@ cudaError_t launch_slot_scan(const KArgs& a, int grid, cudaStream_t s) {
 //   counts  one thread per warp-batch: from the per-frame selection / track /
 //           vertex words (fit and vertex kernels) its output tracks (each frame's
 //           first max_tracks accepted; none for triplet-overflow or invalid
-//           frames), kept frames and their hits; the in-batch prefixes per frame
-//           go to shared memory.  Warp-batches the fused kernel ran (candidate
-//           store full; every warp-batch on the fused variant) bring their counts
-//           and staged outputs in their BatchStat;
-//   bases   the tile's counts are scanned at once and a decoupled look-back over
-//           tiles gives its global bases (every count is final: it never waits on
-//           compute);
-//   frames  every frame record written once with its final track_first /
-//           kept_index (flat, thread-strided), and the reason byte;
-//   tracks  flat over the tile's output: index -> warp-batch by binary search over
-//           the tile's prefix -> the front of its store segment (fit kernel) or
-//           the fused kernel's staging, 32 B each, four in flight per thread;
-//   kept    the kept frames (rare): vertex record, packed offsets and hits.
+//           frames), its track slots (bslot), kept frames and their hits; the
+//           in-batch prefixes per frame go to shared memory.  Warp-batches the
+//           fused kernel ran (candidate store full; every warp-batch on the fused
+//           variant) bring their counts and staged outputs in their BatchStat;
+//   bases   the tile's {slots, kept frames, hits} are scanned at once and a
+//           decoupled look-back over tiles gives its global bases (every count is
+//           final: it never waits on compute);
+//   frames  every frame record written once with its final track_first (the
+//           warp-batch's first slot + the in-batch prefix: where the fit kernel
+//           put its tracks) and kept_index, and the reason byte;
+//   tracks  only the fused kernel's warp-batches (none at phase I): staged tracks
+//           copied into their slots, the rest of the slots marked unused;
+//   kept    each kept frame listed {frame, first packed hit, vertex source} at its
+//           kept index for kept_kernel, which copies them (no dependent loads here:
+//           a slow warp would hold the tile at its barriers).
 // The run summary is accumulated per thread and flushed once per warp.
 #ifndef M3E_PACK_MIN_BLOCKS
 #define M3E_PACK_MIN_BLOCKS 3   // 80 registers, no spills (4 CTAs: 64 registers and spills, slower)
@@ -1871,12 +1878,15 @@ cudaError_t launch_kept(const KArgs& a, int grid, cudaStream_t s) {
 // the current warp-batch into the next one, so lanes stay dense although a
 // warp-batch holds ~50 candidates.  Accepted tracks are ranked per frame
 // (match_any on slot | frame; candidate order = Alg. 3's order); the first
-// max_tracks of each frame (the tracks a frame outputs, R3) are written
-// compacted to the front of their warp-batch's segment of fit_g, so each frame's
-// output tracks are contiguous there and the pack kernel copies them in one run.
-// Rejected candidates write nothing.  Once a warp-batch is consumed, one lane per
-// frame: track-overflow decision, the frame's track word, and frames with e+ e+
-// e- appended to the vertex list; its slot then takes the next warp-batch.
+// max_tracks of each frame (the tracks a frame outputs, R3) are written straight
+// into their final place: compacted to the front of the warp-batch's slot range
+// in out.tracks (from tbase[b], slot_scan_kernel), so the track array needs no
+// reordering copy; without a track output (or past its capacity) to the front of
+// the warp-batch's store segment in fit_g, for the vertex stage.  Rejected
+// candidates write nothing.  Once a warp-batch is consumed, one lane per frame:
+// track-overflow decision, the frame's track word, and frames with e+ e+ e-
+// appended to the vertex list; the warp-batch's unused slots are marked; its slot
+// then takes the next warp-batch.
 constexpr int kFitHCap = 240;   // hits of a warp-batch staged (larger ones are read from HBM)
 
 struct __align__(16) FitSlot {
@@ -2202,7 +2212,10 @@ struct VertexSmem {
     uint2 cmb[kWarps][kMaxCombsCap];          // passing triples: {offsets a | b << 10 | e << 20, a | b << 8 | e << 16}
 };
 
-__global__ void __launch_bounds__(kThreads, 4) vertex_kernel(const __grid_constant__ KArgs A) {
+#ifndef M3E_VERTEX_MIN_BLOCKS
+#define M3E_VERTEX_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kThreads, M3E_VERTEX_MIN_BLOCKS) vertex_kernel(const __grid_constant__ KArgs A) {
     extern __shared__ __align__(16) uint8_t vsm_raw[];
     VertexSmem& S = *reinterpret_cast<VertexSmem*>(vsm_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
