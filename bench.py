@@ -273,6 +273,7 @@ def main():
     kept_cap = F if a.workload.startswith("phase2") else max(1024, F // 20)
     res = m3e.Result(F, H, track_capacity=trk_cap, kept_capacity=kept_cap, device=dev)
     stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))   # inputs and output buffers were filled there
     in_bytes = 12 * H + 16 * F + 4
 
     def step():

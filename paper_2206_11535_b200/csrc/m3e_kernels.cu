@@ -1088,7 +1088,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
                         } else {
                             sk = CandSink{ci, cr, ci, cr, 0u, 0u};
                         }
-                        count = select_frame_big(&S.P, Fv, W.q, A.pair_scratch + gwarp * kPairWords, sk, kPairCapG);
+                        // (its address is passed: a copy here, so that Fv stays in registers
+                        // instead of being stored to local memory for every frame)
+                        const Frame Fb = Fv;
+                        count = select_frame_big(&S.P, Fb, W.q, A.pair_scratch + gwarp * kPairWords, sk, kPairCapG);
                         __syncwarp();
                     }
                     if (count < 0) {
