@@ -472,7 +472,7 @@ def main():
                        "parallelism": f"frame-sharded dp{world}", "generation_s": round(t_gen, 1),
                        "physics": phys},
             "roofline": roof,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (7 if split else 2) * a.steps, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (9 if split else 3) * a.steps, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
