@@ -182,6 +182,13 @@ uint64_t m3e_workspace_bytes(const m3e_context* ctx);
  * selects the single fused kernel (same results). */
 int m3e_set_timing(m3e_context* ctx, int enable);
 int m3e_kernel_times(m3e_context* ctx, float ms[6]);
+/* Internal index checks (testing).  The check build of the library
+ * (lib/libm3e_check.so, compiled with -DM3E_CHECK; same ABI and results) bounds-
+ * checks the kernels' shared-memory and workspace indices and records the source
+ * line of the first failed check instead of trapping.  Synchronises the device,
+ * sets *line to that line (0: no check failed) and clears it; in the production
+ * library *line = 0xFFFFFFFF (checks not compiled in). */
+int m3e_debug_check(m3e_context* ctx, uint32_t* line);
 
 /* Full hot path on device-resident input (the call bench.py times): Selection
  * Cuts -> triplet fit -> tracks -> vertex selection -> output staging -> pack for

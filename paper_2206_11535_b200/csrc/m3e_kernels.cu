@@ -113,6 +113,17 @@ constexpr uint32_t kInFitG = 0x80000000u;
 
 __device__ __forceinline__ bool below(uint32_t i, uint32_t lim) { return i < lim; }
 
+// Internal index checks of the check build (-DM3E_CHECK, lib/libm3e_check.so): a
+// failed check records its source line (the first one wins) instead of trapping;
+// m3e_debug_check() reads and clears it.  Compiled out of the production library.
+__device__ unsigned int g_m3e_check_line;
+#ifdef M3E_CHECK
+#define M3E_CHECK_IDX(cond) \
+    do { if (!(cond)) atomicCAS(&g_m3e_check_line, 0u, (unsigned int)__LINE__); } while (0)
+#else
+#define M3E_CHECK_IDX(cond) do { } while (0)
+#endif
+
 // ----------------------------------------------------------- shared state ----
 // per-frame results of the warp-batch being processed
 struct BatchState {
@@ -483,6 +494,7 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             uint32_t pos = (uint32_t)qn + exc;
             for (uint32_t t = 0; t < take; ++t) {
                 const uint32_t k = ffs_t(rem) - 1;
+                M3E_CHECK_IDX(pos < 64u && t2 + k < (uint32_t)kHCap);
                 W.q[pos++] = ebase | ((t2 + k) << 16);
                 rem &= rem - (MT)1;
             }
@@ -541,6 +553,7 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
                 const int k = ffs_t(rem) - 1;
                 // Delta-lambda = z2 / dr12 - u(i0, i1), u = z1 (1/dr12 + 1/dr01) - z0 / dr01
                 const float u = pair_u(P, z0, hz[t1 + k]);
+                M3E_CHECK_IDX(pos < 64u && t1 + k < kHCap);
                 S.pl[pos++] = make_uint4((uint32_t)g0 | ((uint32_t)(t1 + k) << 8) | ehi, __float_as_uint(u), m2, 0u);
                 rem &= rem - (MT)1;
             }
@@ -667,6 +680,7 @@ __device__ __forceinline__ int select_frame_mask(const DevParams& P, const Frame
     };
     // 1. Phi_12 rows
     for (int i1 = lane; i1 < n1; i1 += 32) {
+        M3E_CHECK_IDX(n1 <= (NW == 1 ? 64 : kMask2Hits) && n2 <= (NW == 1 ? 64 : kMask2Hits));
         u64 m[NW];
         row(X[s1 + i1], Y[s1 + i1], s2, n2, P.inv_r1r2, P.c12_min, m);
 #pragma unroll
@@ -680,6 +694,7 @@ __device__ __forceinline__ int select_frame_mask(const DevParams& P, const Frame
             const float zk = Z[s2 + k];
             r += (int)((zk < z) | ((zk == z) & (k < i2)));
         }
+        M3E_CHECK_IDX(r < n2 && n2 <= (NW == 1 ? 64 : kMask2Hits));
         M.zs[r] = z;
         M.ord[r] = (uint8_t)i2;
     }
@@ -800,7 +815,10 @@ __device__ __forceinline__ int select_frame_mask(const DevParams& P, const Frame
             pn -= K;
             __syncwarp();
         }
-        return emit(rem, qn, [&](int k, uint32_t pos) { q[pos] = pe | ((uint32_t)k << 20); },
+        return emit(rem, qn, [&](int k, uint32_t pos) {
+                        M3E_CHECK_IDX(pos < 64u && k < n2);
+                        q[pos] = pe | ((uint32_t)k << 20);
+                    },
                     [&]() -> bool {
                         while (qn >= 32) {
                             if (drain(32)) return true;
@@ -827,6 +845,7 @@ __device__ __forceinline__ int select_frame_mask(const DevParams& P, const Frame
         }
         if (emit(rem, pn,
                  [&](int k, uint32_t pos) {
+                     M3E_CHECK_IDX(pos < 64u && k < n1);
                      M.pl[pos] = make_uint2((uint32_t)i0 | ((uint32_t)k << 10), __float_as_uint(pair_u(P, z0, Z[s1 + k])));
                  },
                  [&]() -> bool {
@@ -1865,6 +1884,18 @@ __global__ void __launch_bounds__(kThreads) kept_kernel(const __grid_constant__ 
         atomicExch(reinterpret_cast<unsigned long long*>(&O.summary->overflow), 1ull);
 }
 
+cudaError_t read_check_line(unsigned int* line) {
+#ifdef M3E_CHECK
+    cudaError_t e = cudaMemcpyFromSymbol(line, g_m3e_check_line, sizeof(unsigned int));
+    if (e != cudaSuccess) return e;
+    const unsigned int zero = 0;
+    return cudaMemcpyToSymbol(g_m3e_check_line, &zero, sizeof(unsigned int));
+#else
+    *line = 0xFFFFFFFFu;   // checks not compiled in
+    return cudaSuccess;
+#endif
+}
+
 cudaError_t launch_kept(const KArgs& a, int grid, cudaStream_t s) {
     kept_kernel<<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();
@@ -2108,8 +2139,13 @@ __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel
         o.hit3 = 0;
         uint4 e = make_uint4(0u, 0u, 0u, 0u);
         if (valid) {
+            M3E_CHECK_IDX(L.sbase + idx < A.cand_cap && idx < L.n);
             e = A.cand_g[L.sbase + idx];
             j = (int)(e.y - L.f0);
+            M3E_CHECK_IDX(j >= 0 && (uint32_t)j < L.nf);
+            // a staged frame lies inside the slot's window
+            M3E_CHECK_IDX(L.winlo == 0xFFFFFFFFu ||
+                          (e.x >= L.winlo && e.x - L.winlo + (L.offs[4 * j + 4] - L.offs[4 * j]) <= (uint32_t)kFitHCap));
             key = (inX ? 16 : 0) + j;
             // the entry locates the triplet's hits: {first hit of the frame, frame,
             // offsets of h1 | h2 << 16, offset of h0} (inside the frame)
@@ -2158,6 +2194,7 @@ __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel
             tr.cos_theta01 = o.cth01;
             tr.cx = o.cx;
             tr.cy = o.cy;
+            M3E_CHECK_IDX(L.nslot == 0u || L.nacc + __popc(ms & (inX ? mx : ~mx) & lt) < L.nslot);
             L.td[L.nacc + __popc(ms & (inX ? mx : ~mx) & lt)] = tr;
         }
         __syncwarp();
@@ -2247,6 +2284,8 @@ __global__ void __launch_bounds__(kThreads, M3E_VERTEX_MIN_BLOCKS) vertex_kernel
             float kap = 0.0f;
             bool acc = false;
             if (c < nj) {
+                M3E_CHECK_IDX((e.y & kInFitG) ? (e.y & ~kInFitG) + c < A.cand_cap
+                                              : (uint64_t)e.y + c < A.out.track_capacity);
                 acc = true;
                 kap = ft[c].kappa;
             }

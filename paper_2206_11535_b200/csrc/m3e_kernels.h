@@ -146,6 +146,7 @@ size_t smem_bytes();
 cudaError_t launch_filter(int mode, bool big, const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pack(const KArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_kept(const KArgs& a, int grid, cudaStream_t s);
+cudaError_t read_check_line(unsigned int* line);   // check build: first failed index check (0: none)
 constexpr int kScanItems = 8;                          // warp-batches per thread of slot_scan_kernel
 constexpr int kScanTile = kThreads * kScanItems;       // warp-batches per tile (CTA iteration)
 cudaError_t launch_slot_scan(const KArgs& a, int grid, cudaStream_t s);

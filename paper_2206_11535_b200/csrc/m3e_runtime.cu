@@ -531,6 +531,15 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
 extern "C" {
 
 const char* m3e_version(void) { return "m3e-b200 0.1 (sm_100a)"; }
+
+int m3e_debug_check(m3e_context* ctx, uint32_t* line) {
+    if (!ctx || !line) return fail(M3E_ERR_INVALID_ARGUMENT, "NULL argument");
+    CK(cudaSetDevice(ctx->device));
+    unsigned int l = 0;
+    CK(read_check_line(&l));
+    *line = l;
+    return M3E_OK;
+}
 const char* m3e_last_error(void) { return g_err.c_str(); }
 
 int m3e_create(m3e_context** out, int device, uint64_t max_frames, uint64_t max_hits) {

@@ -78,6 +78,7 @@ def lib():
         L.m3e_workspace_bytes.argtypes = [_vp]
         L.m3e_set_timing.argtypes = [_vp, ctypes.c_int]
         L.m3e_kernel_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_float)]
+        L.m3e_debug_check.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32)]
         P = ctypes.POINTER(Params)
         O = ctypes.POINTER(Outputs)
         L.m3e_filter.argtypes = [_vp, P, _vp, _vp, _vp, _vp, _u64, _u64, O, _vp]
@@ -92,7 +93,7 @@ def lib():
 
 # names of every symbol include/m3e.h declares (checked by the CPU tests)
 EXPORTED = ["m3e_version", "m3e_last_error", "m3e_create", "m3e_destroy", "m3e_workspace_bytes",
-            "m3e_set_timing", "m3e_kernel_times",
+            "m3e_set_timing", "m3e_kernel_times", "m3e_debug_check",
             "m3e_filter", "m3e_filter_host", "m3e_select_triplets", "m3e_fit_tracks",
             "m3e_vertex_select", "m3e_pack_frames"]
 
@@ -171,6 +172,14 @@ class Context:
         ms = (ctypes.c_float * 6)()
         _check(lib().m3e_kernel_times(self._h, ms))
         return tuple(float(v) for v in ms)
+
+    def debug_check(self) -> int:
+        """Source line of the first failed internal index check since the last
+        call (0: none; 0xFFFFFFFF: the library was built without checks), see
+        include/m3e.h m3e_debug_check."""
+        line = ctypes.c_uint32(0)
+        _check(lib().m3e_debug_check(self._h, ctypes.byref(line)))
+        return int(line.value)
 
 
 def make_outputs(**kw) -> Outputs:
