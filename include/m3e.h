@@ -130,7 +130,8 @@ typedef struct m3e_summary {
 typedef struct m3e_outputs {
     uint8_t* reason;              /* [F] M3E_REASON_* per frame (the accept flags) */
     m3e_frame_out* frames;        /* [F] */
-    m3e_track* tracks;            /* [track_capacity], frame-ordered with unused slots: frame f's
+    m3e_track* tracks;            /* [track_capacity] (device: 16-byte aligned), frame-ordered with
+                                     unused slots: frame f's
                                      tracks are tracks[track_first .. track_first + min(n_tracks,
                                      max_tracks)); the frames are grouped in warp-batches of
                                      consecutive frames, each owning sum over its frames of

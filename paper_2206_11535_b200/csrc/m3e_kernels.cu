@@ -2182,20 +2182,15 @@ __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel
         const unsigned mx = __ballot_sync(0xffffffffu, valid && inX);
         const unsigned mn = __ballot_sync(0xffffffffu, st && o.kappa < 0.0f);
         const unsigned mp = __ballot_sync(0xffffffffu, st && o.kappa > 0.0f);
-        if (st) {
-            m3e_track tr;
-            tr.frame = e.y;
-            tr.hit[0] = (uint16_t)e.w;
-            tr.hit[1] = (uint16_t)(e.z & 0xFFFFu);
-            tr.hit[2] = (uint16_t)(e.z >> 16);
-            tr.hit[3] = (uint16_t)o.hit3;
-            tr.kappa = o.kappa;
-            tr.chi2 = o.chi2;
-            tr.cos_theta01 = o.cth01;
-            tr.cx = o.cx;
-            tr.cy = o.cy;
+        if (st) {   // the m3e_track record as two 16 B stores (the array is 16 B aligned)
+            const uint4 w0 = make_uint4(e.y, (e.w & 0xFFFFu) | (e.z << 16), (e.z >> 16) | ((uint32_t)o.hit3 << 16),
+                                        __float_as_uint(o.kappa));
+            const uint4 w1 = make_uint4(__float_as_uint(o.chi2), __float_as_uint(o.cth01), __float_as_uint(o.cx),
+                                        __float_as_uint(o.cy));
             M3E_CHECK_IDX(L.nslot == 0u || L.nacc + __popc(ms & (inX ? mx : ~mx) & lt) < L.nslot);
-            L.td[L.nacc + __popc(ms & (inX ? mx : ~mx) & lt)] = tr;
+            uint4* d4 = reinterpret_cast<uint4*>(L.td + L.nacc + __popc(ms & (inX ? mx : ~mx) & lt));
+            d4[0] = w0;
+            d4[1] = w1;
         }
         __syncwarp();
         if (valid && lane == __ffs(grp) - 1) {

@@ -400,6 +400,8 @@ int run_mode(m3e_context* ctx, Workspace& w, int mode, const m3e_params* p, cons
     if (F >= (1ull << 31)) return fail(M3E_ERR_INVALID_ARGUMENT, "too many frames in one call");
     if (F == 0) return M3E_OK;
     if (!x || !y || !z || !offsets) return fail(M3E_ERR_INVALID_ARGUMENT, "input pointer is NULL");
+    if (a.out.tracks && (reinterpret_cast<uintptr_t>(a.out.tracks) & 15u))
+        return fail(M3E_ERR_INVALID_ARGUMENT, "tracks must be 16-byte aligned");
     const int fb = choose_fb(F, H);
     const uint64_t nbatch = (F + fb - 1) / fb;
     // big-frame variant (pair-factorised selection compiled in) for high occupancy
