@@ -225,14 +225,23 @@ M3E_HD float3 hit(const Frame& F, int layer, int i) {
 // ---------------------------------------------------------------- Eq. 5 ----
 // r_tc = d01 d12 d20 / (2 [(h0 - h1) x (h2 - h1)]_z); > 0 clockwise (R5);
 // collinear -> +inf.
-M3E_HD float circle_radius(float3 h0, float3 h1, float3 h2) {
-    float ax = h0.x - h1.x, ay = h0.y - h1.y, bx = h2.x - h1.x, by = h2.y - h1.y;
-    float cz = ax * by - ay * bx;
-    if (cz == 0.0f) return kInfF;
-    float cx = h2.x - h0.x, cy = h2.y - h0.y;
-    float d01 = fsqrt(ax * ax + ay * ay), d12 = fsqrt(bx * bx + by * by), d20 = fsqrt(cx * cx + cy * cy);
-    return d01 * d12 * d20 * rcp(2.0f * cz);
+// transverse chord lengths (d01, d12) of the two arcs h0 -> h1, h1 -> h2, rounded as
+// fma(dx, dx, dy dy) (the fit's own order)
+M3E_HD float2 chords(float3 h0, float3 h1, float3 h2) {
+    const float2 dx = f2(h1.x - h0.x, h2.x - h1.x), dy = f2(h1.y - h0.y, h2.y - h1.y);
+    return sqrt2(fma2(dx, dx, mul2(dy, dy)));
 }
+// r_tc (Eq. 5) with the chords (d01, d12) = chords(h0, h1, h2) already known (the
+// fit reuses them for its arcs, the extension and the track parameters)
+M3E_HD float circle_radius_d(float3 h0, float3 h1, float3 h2, float2 d) {
+    const float ax = h0.x - h1.x, ay = h0.y - h1.y, bx = h2.x - h1.x, by = h2.y - h1.y;
+    const float cz = ax * by - ay * bx;
+    if (cz == 0.0f) return kInfF;
+    const float cx = h2.x - h0.x, cy = h2.y - h0.y;
+    const float d20 = fsqrt(cx * cx + cy * cy);
+    return d.x * d.y * d20 * rcp(2.0f * cz);
+}
+M3E_HD float circle_radius(float3 h0, float3 h1, float3 h2) { return circle_radius_d(h0, h1, h2, chords(h0, h1, h2)); }
 
 // ------------------------------------------------------- Selection Cuts ----
 // Alg. 2 tests: Delta-lambda (Eq. 2-3) first, then Phi_01, Phi_12 (Eq. 4) and
@@ -558,16 +567,15 @@ struct Triplet {
     float phc[2], kc[2], dphi[2];
 };
 
-M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2, float rtc,
+// d = the transverse chords (d01, d12) of the two arcs (chords())
+M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2, float rtc, float2 d,
                                             Triplet& T) {
     if (!(fabsf(rtc) < kInfF)) return false;
     T.q = rtc > 0.0f ? 1 : -1;
     const float r = fabsf(rtc);
     const float ir = rcp(r);
     // the two arcs h0 -> h1 (.x) and h1 -> h2 (.y) side by side (packed fp32)
-    const float2 dx = f2(h1.x - h0.x, h2.x - h1.x), dy = f2(h1.y - h0.y, h2.y - h1.y);
     const float2 z = f2(h1.z - h0.z, h2.z - h1.z);
-    const float2 d = sqrt2(fma2(dx, dx, mul2(dy, dy)));
     float2 sv = mul2(d, f2s(0.5f * ir));
     sv = f2(fminf(sv.x, 1.0f), fminf(sv.y, 1.0f));
     const float2 phc = mul2(f2s(2.0f), fasin2(sv));
@@ -644,10 +652,10 @@ M3E_HD_CALL bool arc_phi(float d, float z, float k, float start, float& phi) {
 // Sec. IV-B-2 "Using this preliminary helix, the hit position in the fourth
 // layer is estimated" (R9): continue the arc h1 -> h2 of curvature k past h2 to
 // its first crossing of the layer-3 cylinder.
-M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, const Triplet& T, float3& out) {
+// (d = the chord h1 -> h2)
+M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, float d, const Triplet& T, float3& out) {
     const float k = T.khat;
     const float dx = h2.x - h1.x, dy = h2.y - h1.y, z = h2.z - h1.z;
-    const float d = fsqrt(dx * dx + dy * dy);
     float phi;
     if (!arc_phi(d, z, k, T.phc[1] + T.dphi[1] * (k - T.kc[1]), phi)) return false;
     const float ik = rcp(k);
@@ -703,17 +711,19 @@ struct FitOut {
 };
 
 // h0, h1, h2 given; F supplies the frame's layer-3 hits (F.s[3], F.n[3])
+// dc = chords(h0, h1, h2)
 template <bool kPairs = true>
-M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, float3 h1, float3 h2, float rtc) {
+M3E_HD FitOut fit_candidate_hd(const DevParams& P, const Frame& F, float3 h0, float3 h1, float3 h2, float rtc,
+                               float2 dc) {
     FitOut o;
     o.status = 0; o.hit3 = -1;
     o.kappa1 = o.kappa2 = o.var1 = o.var2 = o.kappa = o.chi2 = o.cth01 = o.cx = o.cy = 0.0f;
     Triplet T1, T2;
-    if (!fit_triplet(P, h0, h1, h2, rtc, T1)) { o.status = 1; return o; }
+    if (!fit_triplet(P, h0, h1, h2, rtc, dc, T1)) { o.status = 1; return o; }
     o.kappa1 = T1.q * T1.khat;
     o.var1 = T1.var;
     float3 pred;
-    if (!extrapolate(P, h1, h2, T1, pred)) { o.status = 2; return o; }
+    if (!extrapolate(P, h1, h2, dc.y, T1, pred)) { o.status = 2; return o; }
     if (F.n[3] == 0) { o.status = 3; return o; }
     // find_closest_layer3_hit: 3D Euclidean, lowest index on ties (R10); every
     // distance rounded as (dx = x - px) dx dx, fma dy dy, fma dz dz and compared
@@ -753,7 +763,8 @@ M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, flo
     }
     o.hit3 = bi;
     const float3 h3 = hit(F, 3, bi);
-    if (!fit_triplet(P, h1, h2, h3, circle_radius(h1, h2, h3), T2)) { o.status = 4; return o; }
+    const float2 dc2 = f2(dc.y, fsqrt(fmaf(h3.x - h2.x, h3.x - h2.x, (h3.y - h2.y) * (h3.y - h2.y))));
+    if (!fit_triplet(P, h1, h2, h3, circle_radius_d(h1, h2, h3, dc2), dc2, T2)) { o.status = 4; return o; }
     o.kappa2 = T2.q * T2.khat;
     o.var2 = T2.var;
     // Eq. 8 weighted mean, Eq. 7 global chi2
@@ -766,7 +777,7 @@ M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, flo
     const float k = fabsf(kb);
     const int q = kb > 0.0f ? 1 : -1;
     const float dx = h1.x - h0.x, dy = h1.y - h0.y, z01 = h1.z - h0.z;
-    const float d01 = fsqrt(dx * dx + dy * dy);
+    const float d01 = dc.x;
     float phi01;
     if (!arc_phi<M3E_NEWTON_IT_FINAL>(d01, z01, k, T1.phc[0] + T1.dphi[0] * (k - T1.kc[0]), phi01)) {
         o.status = 6;
@@ -781,6 +792,11 @@ M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, flo
     o.cx = 0.5f * (h0.x + h1.x) + q * off * uy;   // clockwise: centre right of the chord
     o.cy = 0.5f * (h0.y + h1.y) - q * off * ux;
     return o;
+}
+
+template <bool kPairs = true>
+M3E_HD FitOut fit_candidate_h(const DevParams& P, const Frame& F, float3 h0, float3 h1, float3 h2, float rtc) {
+    return fit_candidate_hd<kPairs>(P, F, h0, h1, h2, rtc, chords(h0, h1, h2));
 }
 
 template <bool kPairs = true>

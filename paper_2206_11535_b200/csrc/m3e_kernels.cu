@@ -2070,6 +2070,30 @@ __device__ __forceinline__ void fit_frames(const KArgs& A, FitSlot& S) {
     }
 }
 
+// one stored candidate: the frame's hit arrays x/y/z (pointers to its first hit),
+// its layer offsets `of` (of[4] = end), the hit offsets o0, o1, o2 inside the frame
+template <bool kPairs>
+__device__ __forceinline__ FitOut fit_entry(const DevParams& P, const float* x, const float* y, const float* z,
+                                            const uint32_t* of, uint32_t o0, uint32_t o1, uint32_t o2) {
+    Frame F;
+    F.x = x;
+    F.y = y;
+    F.z = z;
+    F.s[0] = 0;
+    F.s[1] = (int)(of[1] - of[0]);
+    F.s[2] = (int)(of[2] - of[0]);
+    F.s[3] = (int)(of[3] - of[0]);
+    F.n[0] = F.s[1];
+    F.n[1] = F.s[2] - F.s[1];
+    F.n[2] = F.s[3] - F.s[2];
+    F.n[3] = (int)(of[4] - of[3]);
+    const float3 h0 = make_float3(x[o0], y[o0], z[o0]);
+    const float3 h1 = make_float3(x[o1], y[o1], z[o1]);
+    const float3 h2 = make_float3(x[o2], y[o2], z[o2]);
+    // r_tc of the selection (Eq. 5, same fp32 code as the selection's)
+    const float2 dc = chords(h0, h1, h2);
+    return fit_candidate_hd<kPairs>(P, F, h0, h1, h2, circle_radius_d(h0, h1, h2, dc), dc);
+}
 #ifndef M3E_FIT_WARPS
 #define M3E_FIT_WARPS 8        // warps per CTA of the fit kernel
 #endif
@@ -2149,26 +2173,20 @@ __global__ void __launch_bounds__(32 * kFitWarps, M3E_FIT_MIN_BLOCKS) fit_kernel
             key = (inX ? 16 : 0) + j;
             // the entry locates the triplet's hits: {first hit of the frame, frame,
             // offsets of h1 | h2 << 16, offset of h0} (inside the frame)
-            Frame F;
-            F.x = L.px + e.x;
-            F.y = L.py + e.x;
-            F.z = L.pz + e.x;
             const uint32_t* of = L.offs + 4 * j;
-            F.s[0] = 0;
-            F.s[1] = (int)(of[1] - of[0]);
-            F.s[2] = (int)(of[2] - of[0]);
-            F.s[3] = (int)(of[3] - of[0]);
-            F.n[0] = F.s[1];
-            F.n[1] = F.s[2] - F.s[1];
-            F.n[2] = F.s[3] - F.s[2];
-            F.n[3] = (int)(of[4] - of[3]);
             const uint32_t o0 = e.w, o1 = e.z & 0xFFFFu, o2 = e.z >> 16;
-            const float3 h0 = make_float3(F.x[o0], F.y[o0], F.z[o0]);
-            const float3 h1 = make_float3(F.x[o1], F.y[o1], F.z[o1]);
-            const float3 h2 = make_float3(F.x[o2], F.y[o2], F.z[o2]);
-            // r_tc of the selection (Eq. 5, same fp32 code as the selection's)
-            o = fit_candidate_h<!BIG>(P, F, h0, h1, h2, circle_radius(h0, h1, h2));
-            e.z = (o1 - (uint32_t)F.s[1]) | ((o2 - (uint32_t)F.s[2]) << 16);   // layer-local h1 | h2
+            if constexpr (BIG) {
+                // big frames (often past the window): per-slot generic base pointers
+                o = fit_entry<false>(P, L.px + e.x, L.py + e.x, L.pz + e.x, of, o0, o1, o2);
+            } else if (L.winlo != 0xFFFFFFFFu) {
+                // staged frame: the slot's arrays indexed directly, so every hit load
+                // is a shared-memory load with 32-bit addressing (LDS)
+                const uint32_t d = e.x - L.winlo;
+                o = fit_entry<true>(P, L.hx + d, L.hy + d, L.hz + d, of, o0, o1, o2);
+            } else {   // (rare at phase I) a second inlined copy with global loads
+                o = fit_entry<true>(P, A.x + e.x, A.y + e.x, A.z + e.x, of, o0, o1, o2);
+            }
+            e.z = (o1 - (of[1] - of[0])) | ((o2 - (of[2] - of[0])) << 16);   // layer-local h1 | h2
         }
         const bool acc = o.status == 0;
         // per-frame rank among accepted candidates (candidate order); the first
