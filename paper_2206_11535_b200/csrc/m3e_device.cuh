@@ -97,6 +97,17 @@ M3E_HD float2 add2(float2 a, float2 b) {
 #endif
 }
 M3E_HD float2 sqrt2(float2 a) { return make_float2(fsqrt(a.x), fsqrt(a.y)); }
+// 1/sqrt: one MUFU.RSQ (rsqrt.approx.ftz, ~1 ulp) where a square root is only divided by
+M3E_HD float frsqrt(float x) {
+#ifdef __CUDA_ARCH__
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+#else
+    return 1.0f / sqrtf(x);
+#endif
+}
+M3E_HD float2 rsqrt2(float2 a) { return make_float2(frsqrt(a.x), frsqrt(a.y)); }
 M3E_HD float2 rcp2(float2 a) { return make_float2(rcp(a.x), rcp(a.y)); }
 
 #ifndef M3E_FAST_TRIG
@@ -138,9 +149,10 @@ M3E_HD float fatan2(float y, float x) {
 #if M3E_FAST_TRIG
     const float ax = fabsf(x), ay = fabsf(y);
     const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-    const float t = mx > 0.0f ? mn * rcp(mx) : 0.0f;
-    const bool r = t > 0.41421356237f;
-    const float tt = r ? (t - 1.0f) * rcp(t + 1.0f) : t;
+    // t = mn / mx; above tan(pi/8) the reduced argument (t - 1) / (t + 1) =
+    // (mn - mx) / (mn + mx): one reciprocal either way
+    const bool r = mn > 0.41421356237f * mx;
+    const float tt = mx > 0.0f ? (r ? mn - mx : mn) * rcp(r ? mn + mx : mx) : 0.0f;
     const float z = tt * tt;
     float a = (((8.05374449538e-2f * z - 1.38776856032e-1f) * z + 1.99777106478e-1f) * z - 3.33329491539e-1f) * z * tt + tt;
     a = r ? a + 0.78539816340f : a;
@@ -562,7 +574,7 @@ struct Triplet {
     int q;                       // +1 clockwise (e+), -1
     float kref, al_phi, b_phi, al_th, b_th, w_phi, w_th;
     float khat;                  // |kappa_t|
-    float var;                   // sigma^2_kappa,t = 1 / (b_phi^2 w_phi + b_th^2 w_th)
+    float A;                     // 1 / sigma^2_kappa,t = b_phi^2 w_phi + b_th^2 w_th (Eq. 8 weight)
     // arc data kept for the extensions
     float phc[2], kc[2], dphi[2];
 };
@@ -581,7 +593,7 @@ M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2
     const float2 phc = mul2(f2s(2.0f), fasin2(sv));
     const float2 rphc = mul2(f2s(r), phc);
     const float2 z2 = mul2(z, z);
-    const float2 iden = rcp2(sqrt2(fma2(rphc, rphc, z2)));
+    const float2 iden = rsqrt2(fma2(rphc, rphc, z2));
     const float2 kc = mul2(phc, iden);
     const float2 cthv = mul2(z, iden), sthv = mul2(rphc, iden);
     const float2 cs2 = fma2(make_float2(-sv.x, -sv.y), sv, f2s(1.0f));
@@ -612,8 +624,8 @@ M3E_HD_CALL bool fit_triplet(const DevParams& P, float3 h0, float3 h1, float3 h2
     const float A = T.b_phi * T.b_phi * T.w_phi + T.b_th * T.b_th * T.w_th;
     if (!(A > 0.0f)) return false;
     const float B = T.al_phi * T.b_phi * T.w_phi + T.al_th * T.b_th * T.w_th;
-    T.var = rcp(A);
-    T.khat = T.kref - B * T.var;
+    T.A = A;
+    T.khat = T.kref - B * rcp(A);
     return true;
 }
 
@@ -668,10 +680,10 @@ M3E_HD bool extrapolate(const DevParams& P, float3 h1, float3 h2, float d, const
     const float ex = ux * ch + T.q * uy * sh, ey = uy * ch - T.q * ux * sh;
     // centre: clockwise (q = +1) to the right of the heading
     const float cx = h2.x + T.q * rt * ey, cy = h2.y - T.q * rt * ex;
-    const float C2 = cx * cx + cy * cy, C = fsqrt(C2);
-    if (C == 0.0f) return false;
+    const float C2 = cx * cx + cy * cy;
+    if (C2 == 0.0f) return false;
     // crossings of |p| = r3 and |p - c| = rt: p = a c^ +- hh n^ (no trigonometry)
-    const float iC = rcp(C);
+    const float iC = frsqrt(C2);
     const float a = (P.R3sq - rt * rt + C2) * 0.5f * iC;
     const float hh2 = P.R3sq - a * a;
     if (hh2 < 0.0f) return false;                    // the helix never reaches layer 3
@@ -721,7 +733,7 @@ M3E_HD FitOut fit_candidate_hd(const DevParams& P, const Frame& F, float3 h0, fl
     Triplet T1, T2;
     if (!fit_triplet(P, h0, h1, h2, rtc, dc, T1)) { o.status = 1; return o; }
     o.kappa1 = T1.q * T1.khat;
-    o.var1 = T1.var;
+    o.var1 = rcp(T1.A);
     float3 pred;
     if (!extrapolate(P, h1, h2, dc.y, T1, pred)) { o.status = 2; return o; }
     if (F.n[3] == 0) { o.status = 3; return o; }
@@ -741,9 +753,9 @@ M3E_HD FitOut fit_candidate_hd(const DevParams& P, const Frame& F, float3 h0, fl
         if constexpr (kPairs) {
             int i = 0;
             for (; i + 1 < n3; i += 2) {
-                const float2 ex = f2(x3[i] - pred.x, x3[i + 1] - pred.x);
-                const float2 ey = f2(y3[i] - pred.y, y3[i + 1] - pred.y);
-                const float2 ez = f2(z3[i] - pred.z, z3[i + 1] - pred.z);
+                const float2 ex = add2(f2(x3[i], x3[i + 1]), f2s(-pred.x));
+                const float2 ey = add2(f2(y3[i], y3[i + 1]), f2s(-pred.y));
+                const float2 ez = add2(f2(z3[i], z3[i + 1]), f2s(-pred.z));
                 const float2 d2 = fma2(ez, ez, fma2(ey, ey, mul2(ex, ex)));
                 if (d2.x < best) { best = d2.x; bi = i; }
                 if (d2.y < best) { best = d2.y; bi = i + 1; }
@@ -766,9 +778,9 @@ M3E_HD FitOut fit_candidate_hd(const DevParams& P, const Frame& F, float3 h0, fl
     const float2 dc2 = f2(dc.y, fsqrt(fmaf(h3.x - h2.x, h3.x - h2.x, (h3.y - h2.y) * (h3.y - h2.y))));
     if (!fit_triplet(P, h1, h2, h3, circle_radius_d(h1, h2, h3, dc2), dc2, T2)) { o.status = 4; return o; }
     o.kappa2 = T2.q * T2.khat;
-    o.var2 = T2.var;
+    o.var2 = rcp(T2.A);
     // Eq. 8 weighted mean, Eq. 7 global chi2
-    const float w1 = rcp(T1.var), w2 = rcp(T2.var);
+    const float w1 = T1.A, w2 = T2.A;
     const float kb = (o.kappa1 * w1 + o.kappa2 * w2) * rcp(w1 + w2);
     o.kappa = kb;
     o.chi2 = triplet_chi2(T1, kb) + triplet_chi2(T2, kb);
