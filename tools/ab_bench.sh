@@ -1,5 +1,5 @@
 O=gpurun_out/ab; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
+timeout 900 python -m pytest ${TESTS:-tests/test_gpu_parity.py tests/test_gpu_fullsize.py} -x -q -m gpu > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
 for r in 1 2; do for v in $VARIANTS; do
   M3E_LIB=paper_2206_11535_b200/lib/variants/libm3e_$v.so timeout 300 python bench.py --no-cpu --no-phys --no-e2e --steps 20 > $O/b_${v}_$r.json 2> $O/b_${v}_$r.err
 done; done
