@@ -381,6 +381,9 @@ __device__ __forceinline__ constexpr int kMaxFlatCombos() { return sizeof(MT) ==
 // n1, n2 <= 32 and n0 n1 n2 <= kBigCombos (so the walk of an overflowing frame is
 // bounded); returns false, having written nothing, for the others (per-frame
 // walk).
+#ifndef M3E_SEL_FSETP
+#define M3E_SEL_FSETP 1   // mask bits from predicates (0: from the sign bits of the differences)
+#endif
 template <typename MT>   // bit-mask type: uint32_t (layers 1, 2 up to 32 hits) or unsigned long long (64)
 __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, uint32_t b, uint32_t f0, int nf,
                                                   uint32_t* gl) {
@@ -457,6 +460,9 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             // per-hit arithmetic as select_frame_warp: fmaf for Delta-lambda, cos_sep for
             // Phi_12)
             for (int k0 = 0; k0 < m2; k0 += 4) {
+#if M3E_SEL_FSETP
+                uint32_t nib = 0u;   // pass bits of the four hits k0 .. k0 + 3
+#endif
 #pragma unroll
                 for (int h = 0; h < 4; h += 2) {
                     const int k = k0 + h;
@@ -464,14 +470,23 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
                     const float2 dl = __ffma2_rn(zz, make_float2(P.inv_dr12, P.inv_dr12), make_float2(-u, -u));
                     const float2 c12 = cos_sep2(x1, y1, make_float2(hx[t2 + k], hx[t2 + k + 1]),
                                                 make_float2(hy[t2 + k], hy[t2 + k + 1]), P.inv_r1r2);
-                    // |dl| <= dl_max and c12 >= c12_min as sign bits of exact differences
+                    // |dl| <= dl_max and c12 >= c12_min as signs of exact differences
                     // (a - b is 0 only for a == b and has the sign of a - b: same decisions)
                     const float2 a = __fadd2_rn(c12, make_float2(-P.c12_min, -P.c12_min));
+#if M3E_SEL_FSETP
+                    // compared on predicates (FSETP), the four bits assembled with constant shifts
+                    if (a.x >= 0.0f && fabsf(dl.x) <= P.dl_max) nib |= 1u << h;
+                    if (a.y >= 0.0f && fabsf(dl.y) <= P.dl_max) nib |= 2u << h;
+#else
                     const float2 b = __fadd2_rn(make_float2(P.dl_max, P.dl_max), make_float2(-fabsf(dl.x), -fabsf(dl.y)));
                     const uint32_t fail = ((__float_as_uint(a.x) | __float_as_uint(b.x)) >> 31) |
                                           (((__float_as_uint(a.y) | __float_as_uint(b.y)) >> 30) & 2u);
                     rem |= (MT)(fail ^ 3u) << k;
+#endif
                 }
+#if M3E_SEL_FSETP
+                rem |= (MT)nib << k0;
+#endif
             }
             rem &= m2 >= kMB ? ~(MT)0 : ((MT)1 << m2) - 1;   // hits past the frame's layer 2
         }
@@ -527,16 +542,27 @@ __device__ __forceinline__ bool select_batch_flat(const KArgs& A, WarpSmem& W, u
             z0 = hz[g0];
             // four layer-1 hits per iteration, two per packed fp32 operation (cos_sep)
             for (int k0 = 0; k0 < m1; k0 += 4) {
+#if M3E_SEL_FSETP
+                uint32_t nib = 0u;
+#endif
 #pragma unroll
                 for (int h = 0; h < 4; h += 2) {
                     const int k = k0 + h;
                     const float2 c = cos_sep2(x0, y0, make_float2(hx[t1 + k], hx[t1 + k + 1]),
                                               make_float2(hy[t1 + k], hy[t1 + k + 1]), P.inv_r0r1);
-                    // c >= c01_min as the sign bit of the exact difference
+                    // c >= c01_min as the sign of the exact difference
                     const float2 d = __fadd2_rn(c, make_float2(-P.c01_min, -P.c01_min));
+#if M3E_SEL_FSETP
+                    if (d.x >= 0.0f) nib |= 1u << h;
+                    if (d.y >= 0.0f) nib |= 2u << h;
+#else
                     const uint32_t fail = (__float_as_uint(d.x) >> 31) | ((__float_as_uint(d.y) >> 30) & 2u);
                     rem |= (MT)(fail ^ 3u) << k;
+#endif
                 }
+#if M3E_SEL_FSETP
+                rem |= (MT)nib << k0;
+#endif
             }
             rem &= m1 >= kMB ? ~(MT)0 : ((MT)1 << m1) - 1;   // hits past the frame's layer 1
         }
@@ -1921,7 +1947,10 @@ cudaError_t launch_kept(const KArgs& a, int grid, cudaStream_t s) {
 // track-overflow decision, the frame's track word, and frames with e+ e+ e-
 // appended to the vertex list; the warp-batch's unused slots are marked; its slot
 // then takes the next warp-batch.
-constexpr int kFitHCap = 240;   // hits of a warp-batch staged (larger ones are read from HBM)
+#ifndef M3E_FIT_HCAP
+#define M3E_FIT_HCAP 240
+#endif
+constexpr int kFitHCap = M3E_FIT_HCAP;   // hits of a warp-batch staged (larger ones are read from HBM)
 
 struct __align__(16) FitSlot {
     float hx[kFitHCap], hy[kFitHCap], hz[kFitHCap];
