@@ -1948,7 +1948,7 @@ cudaError_t launch_kept(const KArgs& a, int grid, cudaStream_t s) {
 // appended to the vertex list; the warp-batch's unused slots are marked; its slot
 // then takes the next warp-batch.
 #ifndef M3E_FIT_HCAP
-#define M3E_FIT_HCAP 240
+#define M3E_FIT_HCAP 288   // measured (fit ms): 240 4.35, 288 4.20, 320 4.23, 384 5.21 (2 CTAs per SM)
 #endif
 constexpr int kFitHCap = M3E_FIT_HCAP;   // hits of a warp-batch staged (larger ones are read from HBM)
 
