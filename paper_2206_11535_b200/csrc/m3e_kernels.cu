@@ -248,12 +248,13 @@ __device__ __forceinline__ uint32_t claim_batch(const KArgs& A) {
     return t < *reinterpret_cast<volatile const uint32_t*>(A.ticket + 5) ? A.spill_list[t] : A.nbatch;
 }
 
-__device__ __forceinline__ void issue_load(const KArgs& A, WarpSmem& W, int buf, uint32_t b) {
+// (lo, hi) = the warp-batch's first and end hit, offsets[4 f0] and offsets[4 (f0 + nf)]
+__device__ __forceinline__ void issue_load_w(const KArgs& A, WarpSmem& W, int buf, uint32_t b, uint32_t lo,
+                                             uint32_t hi) {
     W.b_batch[buf] = b;
     if (b >= A.nbatch) return;
     const uint32_t f0 = b * (uint32_t)A.fb;
     const uint32_t nf = min(A.F - f0, (uint32_t)A.fb);
-    const uint32_t lo = A.offsets[4 * f0], hi = A.offsets[4 * (f0 + nf)];
     const uint32_t wlo = lo & ~3u;
     const uint32_t whi = min((hi + 3u) & ~3u, wlo + (uint32_t)kHCap);
     W.b_winlo[buf] = wlo;
@@ -267,6 +268,25 @@ __device__ __forceinline__ void issue_load(const KArgs& A, WarpSmem& W, int buf,
         bulk_g2s(W.hx[buf], A.x + wlo, hb, &W.bar[buf]);
         bulk_g2s(W.hy[buf], A.y + wlo, hb, &W.bar[buf]);
         bulk_g2s(W.hz[buf], A.z + wlo, hb, &W.bar[buf]);
+    }
+}
+__device__ __forceinline__ void issue_load(const KArgs& A, WarpSmem& W, int buf, uint32_t b) {
+    uint32_t lo = 0u, hi = 0u;
+    if (b < A.nbatch) {
+        const uint32_t f0 = b * (uint32_t)A.fb;
+        const uint32_t nf = min(A.F - f0, (uint32_t)A.fb);
+        lo = A.offsets[4 * f0];
+        hi = A.offsets[4 * (f0 + nf)];
+    }
+    issue_load_w(A, W, buf, b, lo, hi);
+}
+// window bounds of warp-batch b (lane 0; loads left in flight until used)
+__device__ __forceinline__ void batch_bounds(const KArgs& A, uint32_t b, uint32_t& lo, uint32_t& hi) {
+    if (b < A.nbatch) {
+        const uint32_t f0 = b * (uint32_t)A.fb;
+        const uint32_t nf = min(A.F - f0, (uint32_t)A.fb);
+        lo = A.offsets[4 * f0];
+        hi = A.offsets[4 * (f0 + nf)];
     }
 }
 
@@ -1034,7 +1054,21 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
         fence_mbar_init();
     }
     __syncthreads();   // the only CTA barrier before the final summary flush
-    if (lane == 0) issue_load(A, W, 0, claim_batch(A));
+    // lane 0 (one staging buffer): claims pipelined two warp-batches ahead, so that
+    // neither the ticket's atomic nor the next batch's window bounds is waited
+    // for when its bulk copies are issued: c1 = the next warp-batch (bounds
+    // loaded), c2 = the one after (claim in flight)
+    // (selection kernel only: the other launches have few or no warp-batches)
+    constexpr bool kAhead = kNBuf == 1 && MODE == kModeSelectC;
+    uint32_t c1 = 0u, c1lo = 0u, c1hi = 0u, c2 = 0u;
+    if (lane == 0) {
+        issue_load(A, W, 0, claim_batch(A));
+        if constexpr (kAhead) {
+            c1 = claim_batch(A);
+            batch_bounds(A, c1, c1lo, c1hi);
+            c2 = claim_batch(A);
+        }
+    }
     __syncwarp();
     int buf = 0;
     uint32_t phase[kNBuf] = {};
@@ -1506,7 +1540,14 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeSelectC ? (BIG ? M3E_MI
         if constexpr (kNBuf == 2) {
             buf ^= 1;
         } else if (lane == 0) {
-            issue_load(A, W, 0, claim_batch(A));
+            if constexpr (kAhead) {
+                issue_load_w(A, W, 0, c1, c1lo, c1hi);
+                c1 = c2;
+                batch_bounds(A, c1, c1lo, c1hi);
+                c2 = claim_batch(A);
+            } else {
+                issue_load(A, W, 0, claim_batch(A));
+            }
         }
         __syncwarp();
     }
