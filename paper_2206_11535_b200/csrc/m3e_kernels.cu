@@ -239,6 +239,9 @@ __device__ __forceinline__ Frame frame_view(const KArgs& A, const WarpSmem& W, i
     return F;
 }
 
+__device__ __forceinline__ void prefetch_bulk_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 // lane 0: claim warp-batch b into buffer buf and start its bulk copies
 // next warp-batch of this launch (>= nbatch: none left); the split path's fused
 // launch only takes the warp-batches the selection kernel could not store
@@ -2016,9 +2019,6 @@ struct FitPre {
     uint32_t w[6];
 };
 
-__device__ __forceinline__ void prefetch_bulk_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
