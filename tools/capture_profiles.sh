@@ -15,9 +15,12 @@ ncu --kernel-name-base demangled -k regex:m3e:: -s 27 -c 9 --clock-control none 
     python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-phys > $O/traffic.log 2>&1
 python tools/ncu_traffic.py $O/traffic.ncu-rep $O/${R}_bench_traffic.json \
     "ncu --metrics <see tools/capture_profiles.sh> python bench.py --steps 1 --warmup 3 (the step after the warm-up)" > $O/traffic.txt 2>&1
-# the bench line reads the counters of these very sources (this box's copy of profiles/)
+# the bench line reads the counters of these very sources (this box's copy of profiles/).
+# Cross-check only: right after the ncu passes the step measured 8.70 ms against 8.62
+# on a fresh box (selection 3.78 vs 3.70 ms); the committed bench line is taken in a
+# separate call once the counters are committed (python bench.py on a fresh box).
 cp $O/${R}_bench_traffic.json profiles/
-python bench.py > $O/bench_line.json 2> $O/bench_line.err
+python bench.py > $O/bench_line_after_ncu.json 2> $O/bench_line.err
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"fit_kernel|filter_kernel" \
     -s 9 -c 2 -o $O/full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-phys > $O/full.log 2>&1
 python tools/ncu_summary.py $O/full.ncu-rep > $O/${R}_bench_ncu_full.txt 2>&1
